@@ -1,0 +1,230 @@
+/*
+ * phub.h -- C ABI of the B200-native PHub parameter-exchange hot path.
+ *
+ * PHub (arXiv 1805.07891) is a parameter server: N workers push per-key
+ * gradients, the server sums them per fixed-size chunk ("tall aggregation")
+ * and applies a Nesterov-SGD update to the chunk's weights and momentum, and
+ * workers pull the updated weights back.  This library implements that hot
+ * path on one B200 (sm_100a) per context; several contexts (one per GPU /
+ * process) shard the chunks by owner.
+ *
+ * Citations: P:n = PAPER.md line n (canonical copy P:377-1120), S:n = SPEC.md
+ * line n.  DESIGN.md lists every reading of the paper used here (R1..R16).
+ *
+ *   problem statement ........ P:634-638 (InitService allocates receive and
+ *                               merge buffers; Push / Pull / PushPull)
+ *   chunking .................. P:693-703 (32 KB mini-chunks, "virtual keys")
+ *   chunk -> owner ............ P:708-717 (assignment computed at init; 4/3
+ *                               set partition)
+ *   aggregation + optimizer ... P:657, P:677-686 (tall: the thread that sums a
+ *                               chunk over all workers also optimizes it),
+ *                               P:783 (Nesterov SGD; recurrence from S:189)
+ *
+ * Conventions (all entry points):
+ *   - extern "C", no C++ exception ever crosses the boundary; every call
+ *     returns a phub_status.  On any validation error the context state is
+ *     unchanged and phub_last_error() explains it.
+ *   - A CUDA runtime error makes the context sticky-failed: the failing call
+ *     and every later call (except the introspection/destroy calls) return
+ *     PHUB_ERR_CUDA.
+ *   - `stream` arguments are a cudaStream_t passed as void* (NULL = legacy
+ *     default stream).  Work is enqueued on it; validation is synchronous on
+ *     the host before anything is enqueued.
+ *   - One host thread per context at a time.  Any number of contexts
+ *     may coexist in a process (multi-tenant analog).
+ *   - Element type is IEEE-754 binary32 ("single-precision").
+ *   - Device layout: keys are stored key-major; key k starts at element
+ *     key_offsets[k] (phub_layout), each start rounded up to 32 elements
+ *     (128 B) so every key is 128-B aligned; E_padded is the padded total.
+ *     Padding elements carry no meaning and are never returned by pull or
+ *     read_state.
+ */
+#ifndef PHUB_H
+#define PHUB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct phub_ctx_s* phub_ctx;    /* opaque; owns every device arena */
+
+typedef enum {
+    PHUB_OK = 0,
+    PHUB_ERR_INVALID_ARGUMENT = 1,   /* null ptr, N<1, lr/mu not finite, mu outside [0,1),
+                                        bad owner/rank/policy/mode, misaligned BORROW pointer */
+    PHUB_ERR_INVALID_MANIFEST = 2,   /* num_keys==0 or some key has 0 elements     */
+    PHUB_ERR_INVALID_CHUNK_SIZE = 3, /* chunk_size_bytes % 4 != 0             */
+    PHUB_ERR_INVALID_INIT = 4,       /* init_num_elements != E                      */
+    PHUB_ERR_BAD_WORKER = 5,         /* worker_id >= N                              */
+    PHUB_ERR_BAD_KEY = 6,            /* key >= num_keys and != PHUB_ALL_KEYS        */
+    PHUB_ERR_LENGTH_MISMATCH = 7,    /* n != n_k, or != E_padded for PHUB_ALL_KEYS  */
+    PHUB_ERR_DUPLICATE_PUSH = 8,     /* same (worker, key) twice in one iteration   */
+    PHUB_ERR_INCOMPLETE = 9,         /* aggregate before all N x K pushes arrived   */
+    PHUB_ERR_CUDA = 10,              /* CUDA runtime/launch error; context sticky-failed    */
+    PHUB_ERR_OUT_OF_MEMORY = 11,     /* device allocation failed                            */
+    PHUB_ERR_UNSUPPORTED = 12        /* option/variant not available for this context       */
+} phub_status;
+
+#define PHUB_ALL_KEYS (-1)            /* whole-model push/pull in the padded layout        */
+
+enum { PHUB_COPY = 0, PHUB_BORROW = 1 };           /* ownership mode of a pushed buffer   */
+enum { PHUB_OWNER_LPT = 0, PHUB_OWNER_CONTIG = 1 };  /* chunk -> owner policy    */
+
+/* One virtual key: chunk `vkey_id` of key `key_id` covers elements
+ * [offset, offset+length) of that key; `owner` is the owning rank. */
+typedef struct {
+    uint32_t vkey_id;
+    uint32_t key_id;
+    uint64_t offset;
+    uint64_t length;
+    int32_t owner;
+    int32_t reserved;
+} phub_chunk;
+
+typedef struct {
+    const uint64_t* key_num_elements; /* manifest: n_k for k in [0,num_keys), key order = id */
+    int32_t num_keys;
+    int32_t num_workers;              /* N >= 1                                            */
+    uint64_t chunk_size_bytes;        /* 0 -> 32768 ("default is 32KB")       */
+    float lr;                         /* eta, finite                                       */
+    float momentum;                   /* mu in [0,1)                               */
+    float rescale;                    /* optimizer input g = s * rescale; 0 -> 1.0f/N      */
+                                      /* (mean of the gradients; reading R2)        */
+    int32_t device;                   /* CUDA device ordinal the context lives on          */
+    int32_t num_owners;               /* G >= 1: ranks the chunks are sharded over         */
+    int32_t owner_rank;               /* this context's rank in [0, G)                     */
+    int32_t owner_policy;             /* PHUB_OWNER_LPT or PHUB_OWNER_CONTIG               */
+    int32_t keep_aggregate;           /* nonzero: also store the sum s (test mode)         */
+    const float* init_weights;        /* NULL -> zeros; else E elements,       */
+                                      /* key-major unpadded, host or device memory         */
+    uint64_t init_num_elements;       /* must equal E when init_weights != NULL            */
+} phub_config;
+
+/* Fill `cfg` with defaults: chunk 32 KB, lr 0.1, mu 0.9, rescale 0 (=1/N),
+ * device 0, G=1, rank 0, CONTIG, no aggregate, zero init weights. */
+void phub_config_default(phub_config* cfg);
+
+/* InitService analog: build the chunk plan, the chunk -> owner
+ * table, the padded device layout, and allocate w, v (and s) in
+ * one shot on cfg->device.  w = init weights or 0, v = 0.
+ * On success *out owns everything; release with phub_destroy. */
+phub_status phub_init(const phub_config* cfg, phub_ctx* out);
+phub_status phub_destroy(phub_ctx ctx);
+
+/* Push: make worker `worker`'s gradient for key `key`
+ * (or PHUB_ALL_KEYS) available for this iteration.
+ *   key == PHUB_ALL_KEYS: `grad` holds n == E_padded elements in the padded
+ *     layout (keys at phub_layout offsets).  Only this context's owned chunks
+ *     are read.
+ *   key in [0, num_keys): `grad` holds n == n_k contiguous elements.
+ *   mode PHUB_BORROW: zero copy -- the pointer is recorded and read by
+ *     the next phub_aggregate_optimize.  `grad` must be device memory
+ *     (this or a peer-mapped GPU), 16-byte aligned.  The caller must keep it
+ *     valid and unmodified until that aggregate has completed on its stream.
+ *   mode PHUB_COPY: the data (host or device memory) is copied into the
+ *     context's receive arena on `stream`; the caller may reuse `grad` once
+ *     the copy has completed on `stream`.
+ * Errors: BAD_WORKER, BAD_KEY, LENGTH_MISMATCH, DUPLICATE_PUSH (this
+ * (worker, key) already pushed in this iteration), INVALID_ARGUMENT. */
+phub_status phub_push(phub_ctx ctx, int32_t worker, int32_t key, const float* grad,
+                      uint64_t n, int32_t mode, void* stream);
+
+/* Aggregate + optimize every owned chunk: for each element i
+ *   s  = (((+0.0f + g_0[i]) + g_1[i]) + ...) + g_{N-1}[i]   (worker-id order)
+ *   g  = s * rescale
+ *   v' = mu * v[i] + g
+ *   w' = w[i] - lr * (g + mu * v')
+ * every operation separately rounded to nearest-even in fp32, no contraction
+ * (readings R3-R6).  One fused kernel launch on `stream`.  Requires every
+ * (worker, key) pushed (else PHUB_ERR_INCOMPLETE, nothing enqueued).  Then
+ * clears the receipts and advances the iteration counter. */
+phub_status phub_aggregate_optimize(phub_ctx ctx, void* stream);
+
+/* Pull: copy the current weights of `key` (n == n_k) or of
+ * the whole padded model (PHUB_ALL_KEYS, n == E_padded) into `dst` (host or
+ * device memory) on `stream`.  Before any aggregate it returns the initial
+ * weights; after k aggregates, iteration k's result. */
+phub_status phub_pull(phub_ctx ctx, int32_t key, float* dst, uint64_t n, void* stream);
+
+/* PushPull: push `grad` for `worker` (COPY or BORROW, as
+ * phub_push with key == PHUB_ALL_KEYS); when that push completes the
+ * iteration (all N x K receipts), run phub_aggregate_optimize and copy the
+ * updated padded model into `dst` (may be NULL).  Otherwise only pushes. */
+phub_status phub_pushpull(phub_ctx ctx, int32_t worker, const float* grad, uint64_t n,
+                          int32_t mode, float* dst, void* stream);
+
+/* Zero-copy pull: the device pointer of the padded weight replica (E_padded
+ * elements).  Valid until phub_destroy.  Writes by the caller (e.g. an
+ * all-gather of other owners' ranges at G > 1) are allowed. */
+phub_status phub_weights(phub_ctx ctx, float** w_dev);
+
+/* Layout: E (real elements), E_padded, and key_offsets[num_keys] (may be NULL). */
+phub_status phub_layout(phub_ctx ctx, uint64_t* E, uint64_t* E_padded, uint64_t* key_offsets);
+
+/* Host-only planning (no device needed): the chunk table phub_init would
+ * build for this manifest, chunk size, G and policy, written to out[0..cap).
+ * *count receives the number of chunks; cap may be 0 (count query).
+ * Errors as phub_init's validation; LENGTH_MISMATCH if cap < count. */
+phub_status phub_plan_chunks(const uint64_t* key_num_elements, int32_t num_keys,
+                             uint64_t chunk_size_bytes, int32_t num_owners, int32_t owner_policy,
+                             phub_chunk* out, uint64_t cap, uint64_t* count);
+
+/* Chunk table (S:125 order: vkey_id, key_id, offset, length, owner). */
+phub_status phub_num_chunks(phub_ctx ctx, uint64_t* n);
+phub_status phub_chunk_table(phub_ctx ctx, phub_chunk* out, uint64_t cap);
+
+/* Padded-layout element range [begin, end) owned by `owner` under the CONTIG
+ * policy (G == 1 or PHUB_OWNER_CONTIG); PHUB_ERR_UNSUPPORTED under LPT.
+ * Ranges of consecutive owners abut; an owner with no chunk gets begin==end. */
+phub_status phub_owner_range(phub_ctx ctx, int32_t owner, uint64_t* begin, uint64_t* end);
+
+/* Owned elements (real, padding excluded) of this context. */
+phub_status phub_owned_elements(phub_ctx ctx, uint64_t* n);
+
+/* Overwrite w and/or v (each E elements, key-major unpadded, host or device,
+ * NULL = leave unchanged).  Synchronous.  Checkpoint-restore analog. */
+phub_status phub_load_state(phub_ctx ctx, const float* w, const float* v);
+
+/* Read w, v and (keep_aggregate) the last sum s into E-element key-major
+ * unpadded buffers (host or device; NULL = skip).  Synchronous (device-wide
+ * synchronize first).  agg must be NULL unless keep_aggregate. */
+phub_status phub_read_state(phub_ctx ctx, float* w, float* v, float* agg);
+
+/* Iterations completed, and kernels this context has launched. */
+phub_status phub_iteration(phub_ctx ctx, uint64_t* iteration);
+phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
+
+/* Options (ablations / tuning).  Values are validated; PHUB_ERR_UNSUPPORTED
+ * when a forced variant cannot run this context's layout. */
+enum {
+    PHUB_OPT_KERNEL = 1,      /* PHUB_KERNEL_*                                           */
+    PHUB_OPT_GRID = 2,        /* CTAs for the flat kernels, 0 = auto (SMs x occupancy)   */
+    PHUB_OPT_TILE_ELEMS = 3,  /* max elements per CTA tile in the chunk-tile kernel      */
+    PHUB_OPT_CACHE = 4        /* PHUB_CACHE_*: L2 policy of the pulled weights   */
+};
+enum {
+    PHUB_KERNEL_AUTO = 0,     /* flat 256-bit kernel when eligible, else chunk tiles     */
+    PHUB_KERNEL_FLAT = 1,     /* flat owned range, 256-bit LDG/STG (needs 32-B alignment) */
+    PHUB_KERNEL_TILES = 2,    /* one CTA per chunk tile, per-(worker,key) pointers       */
+    PHUB_KERNEL_FLAT128 = 3,  /* flat owned range, 128-bit LDG/STG                       */
+    PHUB_KERNEL_WIDE = 4      /* ablation: wide aggregation, N-1 pairwise passes + NAG   */
+                              /* pass (MXNet style)                           */
+};
+enum {
+    PHUB_CACHE_ENABLED = 0,   /* w' stored evict-last (kept in L2 for the pull), grads   */
+                              /* evict-first ("cache-enabled")              */
+    PHUB_CACHE_BYPASS = 1     /* everything streaming / evict-first (non-temporal analog) */
+};
+phub_status phub_set_option(phub_ctx ctx, int32_t option, int64_t value);
+
+const char* phub_status_string(phub_status s);
+/* Detail of the last failed call on `ctx`; with ctx == NULL, of the calling
+ * thread's last failed phub_init / phub_plan_chunks. */
+const char* phub_last_error(phub_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHUB_H */

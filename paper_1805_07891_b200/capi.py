@@ -1,0 +1,239 @@
+"""ctypes binding of include/phub.h -- argument marshalling only.
+
+Every function here has the name of the C entry point it calls and does no
+computation of its own: each step of the hot path runs in libphub.so's sm_100a
+kernels.  There is no fallback: if libphub.so is missing or fails to load,
+importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libphub.so")
+
+# ----------------------------------------------------------------- constants
+PHUB_OK = 0
+STATUS_NAMES = [
+    "PHUB_OK", "PHUB_ERR_INVALID_ARGUMENT", "PHUB_ERR_INVALID_MANIFEST",
+    "PHUB_ERR_INVALID_CHUNK_SIZE", "PHUB_ERR_INVALID_INIT", "PHUB_ERR_BAD_WORKER",
+    "PHUB_ERR_BAD_KEY", "PHUB_ERR_LENGTH_MISMATCH", "PHUB_ERR_DUPLICATE_PUSH",
+    "PHUB_ERR_INCOMPLETE", "PHUB_ERR_CUDA", "PHUB_ERR_OUT_OF_MEMORY", "PHUB_ERR_UNSUPPORTED",
+]
+for _i, _n in enumerate(STATUS_NAMES):
+    globals()[_n] = _i
+PHUB_ALL_KEYS = -1
+PHUB_COPY, PHUB_BORROW = 0, 1
+PHUB_OWNER_LPT, PHUB_OWNER_CONTIG = 0, 1
+PHUB_OPT_KERNEL, PHUB_OPT_GRID, PHUB_OPT_TILE_ELEMS, PHUB_OPT_CACHE = 1, 2, 3, 4
+(PHUB_KERNEL_AUTO, PHUB_KERNEL_FLAT, PHUB_KERNEL_TILES, PHUB_KERNEL_FLAT128,
+ PHUB_KERNEL_WIDE) = range(5)
+PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS = 0, 1
+
+
+class phub_chunk(C.Structure):
+    _fields_ = [("vkey_id", C.c_uint32), ("key_id", C.c_uint32), ("offset", C.c_uint64),
+                ("length", C.c_uint64), ("owner", C.c_int32), ("reserved", C.c_int32)]
+
+
+class phub_config(C.Structure):
+    _fields_ = [
+        ("key_num_elements", C.POINTER(C.c_uint64)),
+        ("num_keys", C.c_int32),
+        ("num_workers", C.c_int32),
+        ("chunk_size_bytes", C.c_uint64),
+        ("lr", C.c_float),
+        ("momentum", C.c_float),
+        ("rescale", C.c_float),
+        ("device", C.c_int32),
+        ("num_owners", C.c_int32),
+        ("owner_rank", C.c_int32),
+        ("owner_policy", C.c_int32),
+        ("keep_aggregate", C.c_int32),
+        ("init_weights", C.c_void_p),
+        ("init_num_elements", C.c_uint64),
+    ]
+
+
+phub_ctx = C.c_void_p
+_u64p = C.POINTER(C.c_uint64)
+
+_SIGS = {
+    "phub_config_default": (None, [C.POINTER(phub_config)]),
+    "phub_init": (C.c_int, [C.POINTER(phub_config), C.POINTER(phub_ctx)]),
+    "phub_destroy": (C.c_int, [phub_ctx]),
+    "phub_push": (C.c_int, [phub_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32,
+                            C.c_void_p]),
+    "phub_aggregate_optimize": (C.c_int, [phub_ctx, C.c_void_p]),
+    "phub_pull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "phub_pushpull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32,
+                                C.c_void_p, C.c_void_p]),
+    "phub_weights": (C.c_int, [phub_ctx, C.POINTER(C.c_void_p)]),
+    "phub_layout": (C.c_int, [phub_ctx, _u64p, _u64p, _u64p]),
+    "phub_num_chunks": (C.c_int, [phub_ctx, _u64p]),
+    "phub_chunk_table": (C.c_int, [phub_ctx, C.POINTER(phub_chunk), C.c_uint64]),
+    "phub_plan_chunks": (C.c_int, [_u64p, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                                   C.POINTER(phub_chunk), C.c_uint64, _u64p]),
+    "phub_owner_range": (C.c_int, [phub_ctx, C.c_int32, _u64p, _u64p]),
+    "phub_owned_elements": (C.c_int, [phub_ctx, _u64p]),
+    "phub_load_state": (C.c_int, [phub_ctx, C.c_void_p, C.c_void_p]),
+    "phub_read_state": (C.c_int, [phub_ctx, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "phub_iteration": (C.c_int, [phub_ctx, _u64p]),
+    "phub_kernel_launches": (C.c_int, [phub_ctx, _u64p]),
+    "phub_set_option": (C.c_int, [phub_ctx, C.c_int32, C.c_int64]),
+    "phub_status_string": (C.c_char_p, [C.c_int]),
+    "phub_last_error": (C.c_char_p, [phub_ctx]),
+}
+EXPORTS = tuple(_SIGS)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python paper_1805_07891_b200/build.py` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+class PhubError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"{where}: {name}" + (f" ({detail})" if detail else ""))
+
+
+def _check(st: int, where: str, ctx=None):
+    if st != PHUB_OK:
+        d = _lib.phub_last_error(ctx)          # ctx None -> this thread's init error
+        raise PhubError(st, where, d.decode() if d else "")
+
+
+# ------------------------------------------------- same-named thin wrappers
+def phub_config_default() -> phub_config:
+    cfg = phub_config()
+    _lib.phub_config_default(C.byref(cfg))
+    return cfg
+
+
+def phub_init(cfg: phub_config):
+    ctx = phub_ctx()
+    _check(_lib.phub_init(C.byref(cfg), C.byref(ctx)), "phub_init")
+    return ctx
+
+
+def phub_destroy(ctx):
+    _check(_lib.phub_destroy(ctx), "phub_destroy")
+
+
+def phub_push(ctx, worker: int, key: int, grad_ptr: int, n: int, mode: int, stream: int = 0):
+    _check(_lib.phub_push(ctx, worker, key, grad_ptr, n, mode, stream), "phub_push", ctx)
+
+
+def phub_aggregate_optimize(ctx, stream: int = 0):
+    _check(_lib.phub_aggregate_optimize(ctx, stream), "phub_aggregate_optimize", ctx)
+
+
+def phub_pull(ctx, key: int, dst_ptr: int, n: int, stream: int = 0):
+    _check(_lib.phub_pull(ctx, key, dst_ptr, n, stream), "phub_pull", ctx)
+
+
+def phub_pushpull(ctx, worker: int, grad_ptr: int, n: int, mode: int, dst_ptr, stream: int = 0):
+    _check(_lib.phub_pushpull(ctx, worker, grad_ptr, n, mode, dst_ptr, stream), "phub_pushpull",
+           ctx)
+
+
+def phub_weights(ctx) -> int:
+    p = C.c_void_p()
+    _check(_lib.phub_weights(ctx, C.byref(p)), "phub_weights", ctx)
+    return int(p.value or 0)
+
+
+def phub_layout(ctx, num_keys: int):
+    E, Ep = C.c_uint64(), C.c_uint64()
+    offs = (C.c_uint64 * num_keys)()
+    _check(_lib.phub_layout(ctx, C.byref(E), C.byref(Ep), offs), "phub_layout", ctx)
+    return int(E.value), int(Ep.value), list(offs)
+
+
+def phub_num_chunks(ctx) -> int:
+    n = C.c_uint64()
+    _check(_lib.phub_num_chunks(ctx, C.byref(n)), "phub_num_chunks", ctx)
+    return int(n.value)
+
+
+def phub_chunk_table(ctx):
+    n = phub_num_chunks(ctx)
+    arr = (phub_chunk * max(n, 1))()
+    _check(_lib.phub_chunk_table(ctx, arr, n), "phub_chunk_table", ctx)
+    return arr, n
+
+
+def phub_plan_chunks(key_sizes, chunk_size_bytes: int, num_owners: int, owner_policy: int):
+    """Host-only chunk table (no device): list-of-structs array and count."""
+    n = (C.c_uint64 * max(len(key_sizes), 1))(*[int(x) for x in key_sizes])
+    cnt = C.c_uint64()
+    _check(_lib.phub_plan_chunks(n, len(key_sizes), chunk_size_bytes, num_owners, owner_policy,
+                                 None, 0, C.byref(cnt)), "phub_plan_chunks", None)
+    arr = (phub_chunk * max(cnt.value, 1))()
+    _check(_lib.phub_plan_chunks(n, len(key_sizes), chunk_size_bytes, num_owners, owner_policy,
+                                 arr, cnt.value, C.byref(cnt)), "phub_plan_chunks", None)
+    return arr, int(cnt.value)
+
+
+def phub_owner_range(ctx, owner: int):
+    b, e = C.c_uint64(), C.c_uint64()
+    _check(_lib.phub_owner_range(ctx, owner, C.byref(b), C.byref(e)), "phub_owner_range", ctx)
+    return int(b.value), int(e.value)
+
+
+def phub_owned_elements(ctx) -> int:
+    n = C.c_uint64()
+    _check(_lib.phub_owned_elements(ctx, C.byref(n)), "phub_owned_elements", ctx)
+    return int(n.value)
+
+
+def phub_load_state(ctx, w_ptr, v_ptr):
+    _check(_lib.phub_load_state(ctx, w_ptr, v_ptr), "phub_load_state", ctx)
+
+
+def phub_read_state(ctx, w_ptr, v_ptr, agg_ptr):
+    _check(_lib.phub_read_state(ctx, w_ptr, v_ptr, agg_ptr), "phub_read_state", ctx)
+
+
+def phub_iteration(ctx) -> int:
+    n = C.c_uint64()
+    _check(_lib.phub_iteration(ctx, C.byref(n)), "phub_iteration", ctx)
+    return int(n.value)
+
+
+def phub_kernel_launches(ctx) -> int:
+    n = C.c_uint64()
+    _check(_lib.phub_kernel_launches(ctx, C.byref(n)), "phub_kernel_launches", ctx)
+    return int(n.value)
+
+
+def phub_set_option(ctx, option: int, value: int):
+    _check(_lib.phub_set_option(ctx, option, value), "phub_set_option", ctx)
+
+
+def phub_status_string(st: int) -> str:
+    return _lib.phub_status_string(st).decode()
+
+
+def phub_last_error(ctx) -> str:
+    r = _lib.phub_last_error(ctx)
+    return r.decode() if r else ""
+
+
+def raw_lib():
+    """The loaded ctypes library (tests check the exported symbols)."""
+    return _lib

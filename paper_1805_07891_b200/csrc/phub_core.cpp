@@ -1,0 +1,771 @@
+// phub_core.cpp -- host side of libphub: the C ABI of include/phub.h.
+//
+//   manifest -> chunk plan -> chunk -> owner table
+//   (LPT S:85 or CONTIG, reading R10) -> padded device layout ->
+//   one-shot arenas -> per-(worker, key) receipts (P:686,
+//   S:137-142) -> one fused kernel launch per round (phub_kernels.cu).
+//
+// Nothing here computes on the model data: every step of the numeric path
+// runs in the sm_100a kernels.  Errors never throw across the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "phub.h"
+#include "phub_kernels.cuh"
+
+using phub::Tile;
+
+namespace {
+
+constexpr uint64_t kKeyAlign = 32;   // key starts rounded to 32 elements (128 B)
+constexpr uint64_t kDefaultChunkBytes = 32768;
+
+struct DeviceGuard {
+    int prev = -1, dev;
+    explicit DeviceGuard(int d) : dev(d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct phub_ctx_s {
+    // configuration
+    int device = 0;
+    int N = 0, K = 0, G = 1, rank = 0, policy = PHUB_OWNER_CONTIG;
+    uint64_t chunk_bytes = kDefaultChunkBytes, ce = kDefaultChunkBytes / 4;
+    float lr = 0.f, mu = 0.f, rescale = 0.f;
+    bool keep_agg = false;
+    int num_sms = 148;
+
+    // layout
+    std::vector<uint64_t> n;          // key sizes
+    std::vector<uint64_t> key_off;    // padded device offset of each key
+    uint64_t E = 0, E_pad = 0;
+
+    // chunk table + ownership
+    std::vector<phub_chunk> chunks;
+    std::vector<uint64_t> own_begin, own_end;   // CONTIG ranges per owner (padded layout)
+    uint64_t owned_elems = 0;
+    uint64_t n_tiles = 0;
+    Tile* d_tiles = nullptr;
+    uint32_t tile_elems = 8192;
+
+    // arenas
+    float* d_w = nullptr;
+    float* d_v = nullptr;
+    float* d_agg = nullptr;
+    float* d_recv = nullptr;          // N x E_pad, allocated on first COPY push
+
+    // push state (iteration-scoped)
+    std::vector<uint8_t> got;         // K x N receipts
+    uint64_t got_count = 0;
+    std::vector<uintptr_t> base;      // N x K: base + 4*dev_off = byte address
+    std::vector<uintptr_t> base_uploaded;
+    uintptr_t* d_base = nullptr;
+
+    // options + counters
+    int kernel = PHUB_KERNEL_AUTO;
+    int grid_override = 0;
+    int cache = PHUB_CACHE_ENABLED;
+    int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
+    uint64_t iteration = 0;
+    int launches = 0;
+    uint64_t launches_total = 0;
+    bool failed = false;
+    std::string err;
+
+    phub_status fail(phub_status s, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        return s;
+    }
+    phub_status cuda_fail(cudaError_t e, const char* where) {
+        failed = true;
+        err = std::string(where) + ": " + cudaGetErrorString(e);
+        return e == cudaErrorMemoryAllocation ? PHUB_ERR_OUT_OF_MEMORY : PHUB_ERR_CUDA;
+    }
+};
+
+static const char* kStatusNames[] = {
+    "PHUB_OK",
+    "PHUB_ERR_INVALID_ARGUMENT",
+    "PHUB_ERR_INVALID_MANIFEST",
+    "PHUB_ERR_INVALID_CHUNK_SIZE",
+    "PHUB_ERR_INVALID_INIT",
+    "PHUB_ERR_BAD_WORKER",
+    "PHUB_ERR_BAD_KEY",
+    "PHUB_ERR_LENGTH_MISMATCH",
+    "PHUB_ERR_DUPLICATE_PUSH",
+    "PHUB_ERR_INCOMPLETE",
+    "PHUB_ERR_CUDA",
+    "PHUB_ERR_OUT_OF_MEMORY",
+    "PHUB_ERR_UNSUPPORTED",
+};
+
+// ------------------------------------------------------------ table logic
+// Chunk plan: per key in key order, ceil(n_k / ce) chunks;
+// then owners: G == 1 -> 0; LPT or CONTIG (reading R10).
+static std::vector<phub_chunk> plan_chunks(const std::vector<uint64_t>& n, uint64_t ce, int G,
+                                           int policy) {
+    std::vector<phub_chunk> chunks;
+    uint64_t E = 0;
+    for (size_t k = 0; k < n.size(); ++k) {
+        E += n[k];
+        for (uint64_t off = 0; off < n[k]; off += ce) {
+            phub_chunk ch{};
+            ch.vkey_id = (uint32_t)chunks.size();
+            ch.key_id = (uint32_t)k;
+            ch.offset = off;
+            ch.length = std::min(ce, n[k] - off);
+            ch.owner = 0;
+            chunks.push_back(ch);
+        }
+    }
+    if (G == 1) return chunks;
+    if (policy == PHUB_OWNER_LPT) {
+        // length desc, ties lower vkey_id; least-loaded owner, ties lower index
+        std::vector<uint32_t> order(chunks.size());
+        for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+            return chunks[a].length > chunks[b].length;
+        });
+        std::vector<uint64_t> load(G, 0);
+        for (uint32_t i : order) {
+            int best = 0;
+            for (int b = 1; b < G; ++b)
+                if (load[b] < load[best]) best = b;
+            chunks[i].owner = best;
+            load[best] += chunks[i].length;
+        }
+    } else {
+        // owner = min(G-1, floor((2p + l) G / 2E)), p = element prefix before the chunk
+        unsigned __int128 p = 0;
+        const unsigned __int128 twoE = (unsigned __int128)2 * E;
+        for (auto& ch : chunks) {
+            unsigned __int128 o = ((2 * p + ch.length) * (unsigned __int128)G) / twoE;
+            ch.owner = o > (unsigned __int128)(G - 1) ? G - 1 : (int32_t)o;
+            p += ch.length;
+        }
+    }
+    return chunks;
+}
+
+static uint64_t chunk_dev_off(phub_ctx c, const phub_chunk& ch) {
+    return c->key_off[ch.key_id] + ch.offset;
+}
+
+// CONTIG ranges in the padded layout: owner o covers from its first chunk's
+// device offset up to the next owner's first chunk (padding included).
+static void build_ranges(phub_ctx c) {
+    c->own_begin.assign(c->G, 0);
+    c->own_end.assign(c->G, 0);
+    if (!(c->G == 1 || c->policy == PHUB_OWNER_CONTIG)) return;
+    std::vector<int64_t> first(c->G, -1);
+    for (const auto& ch : c->chunks)
+        if (first[ch.owner] < 0) first[ch.owner] = (int64_t)chunk_dev_off(c, ch);
+    uint64_t next = c->E_pad;
+    for (int o = c->G - 1; o >= 0; --o) {
+        if (first[o] < 0) {
+            c->own_begin[o] = c->own_end[o] = next;
+        } else {
+            c->own_begin[o] = (uint64_t)first[o];
+            c->own_end[o] = next;
+            next = (uint64_t)first[o];
+        }
+    }
+}
+
+static bool contig_mode(phub_ctx c) { return c->G == 1 || c->policy == PHUB_OWNER_CONTIG; }
+
+// Owned chunks split into CTA tiles of <= tile_elems (chunk-tile kernel).
+static std::vector<Tile> build_tiles(phub_ctx c) {
+    std::vector<Tile> tiles;
+    for (const auto& ch : c->chunks) {
+        if (ch.owner != c->rank) continue;
+        for (uint64_t o = 0; o < ch.length; o += c->tile_elems) {
+            Tile t;
+            t.off = chunk_dev_off(c, ch) + o;
+            t.len = (uint32_t)std::min<uint64_t>(c->tile_elems, ch.length - o);
+            t.key = ch.key_id;
+            tiles.push_back(t);
+        }
+    }
+    return tiles;
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+void phub_config_default(phub_config* cfg) {
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->chunk_size_bytes = kDefaultChunkBytes;
+    cfg->num_workers = 1;
+    cfg->lr = 0.1f;
+    cfg->momentum = 0.9f;
+    cfg->rescale = 0.0f;
+    cfg->num_owners = 1;
+    cfg->owner_policy = PHUB_OWNER_CONTIG;
+}
+
+const char* phub_status_string(phub_status s) {
+    if ((int)s < 0 || (size_t)s >= sizeof kStatusNames / sizeof kStatusNames[0])
+        return "PHUB_ERR_UNKNOWN";
+    return kStatusNames[s];
+}
+
+static thread_local std::string g_init_err;
+
+const char* phub_last_error(phub_ctx ctx) { return ctx ? ctx->err.c_str() : g_init_err.c_str(); }
+
+static phub_status validate_config(const phub_config* cfg, std::string& why) {
+    auto bad = [&](phub_status s, const char* m) { why = m; return s; };
+    if (!cfg) return bad(PHUB_ERR_INVALID_ARGUMENT, "cfg is NULL");
+    if (cfg->num_keys <= 0 || !cfg->key_num_elements)
+        return bad(PHUB_ERR_INVALID_MANIFEST, "manifest has no keys (S:68)");
+    for (int k = 0; k < cfg->num_keys; ++k)
+        if (cfg->key_num_elements[k] == 0)
+            return bad(PHUB_ERR_INVALID_MANIFEST, "a key has zero elements (S:68)");
+    if (cfg->chunk_size_bytes % 4 != 0)
+        return bad(PHUB_ERR_INVALID_CHUNK_SIZE, "chunk_size_bytes must be a multiple of 4 (S:77)");
+    if (cfg->num_workers < 1) return bad(PHUB_ERR_INVALID_ARGUMENT, "num_workers < 1");
+    if (!std::isfinite(cfg->lr)) return bad(PHUB_ERR_INVALID_ARGUMENT, "lr not finite");
+    if (!std::isfinite(cfg->momentum) || cfg->momentum < 0.f || cfg->momentum >= 1.f)
+        return bad(PHUB_ERR_INVALID_ARGUMENT, "momentum must be in [0,1) (S:144)");
+    if (!std::isfinite(cfg->rescale)) return bad(PHUB_ERR_INVALID_ARGUMENT, "rescale not finite");
+    if (cfg->num_owners < 1 || cfg->owner_rank < 0 || cfg->owner_rank >= cfg->num_owners)
+        return bad(PHUB_ERR_INVALID_ARGUMENT, "owner_rank must be in [0, num_owners)");
+    if (cfg->owner_policy != PHUB_OWNER_LPT && cfg->owner_policy != PHUB_OWNER_CONTIG)
+        return bad(PHUB_ERR_INVALID_ARGUMENT, "unknown owner_policy");
+    if (cfg->device < 0) return bad(PHUB_ERR_INVALID_ARGUMENT, "device < 0");
+    return PHUB_OK;
+}
+
+static void free_ctx(phub_ctx c) {
+    if (!c) return;
+    DeviceGuard g(c->device);
+    cudaFree(c->d_w);
+    cudaFree(c->d_v);
+    cudaFree(c->d_agg);
+    cudaFree(c->d_recv);
+    cudaFree(c->d_tiles);
+    cudaFree(c->d_base);
+    delete c;
+}
+
+phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
+    std::string& why = g_init_err;
+    why.clear();
+    if (!out) return why = "out is NULL", PHUB_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    phub_status st = validate_config(cfg, why);
+    if (st != PHUB_OK) return st;
+
+    phub_ctx c = new (std::nothrow) phub_ctx_s();
+    if (!c) return PHUB_ERR_OUT_OF_MEMORY;
+    c->device = cfg->device;
+    c->N = cfg->num_workers;
+    c->K = cfg->num_keys;
+    c->G = cfg->num_owners;
+    c->rank = cfg->owner_rank;
+    c->policy = cfg->owner_policy;
+    c->chunk_bytes = cfg->chunk_size_bytes ? cfg->chunk_size_bytes : kDefaultChunkBytes;
+    c->ce = c->chunk_bytes / 4;
+    c->lr = cfg->lr;
+    c->mu = cfg->momentum;
+    c->rescale = cfg->rescale != 0.f ? cfg->rescale : 1.0f / (float)c->N;
+    c->keep_agg = cfg->keep_aggregate != 0;
+    c->n.assign(cfg->key_num_elements, cfg->key_num_elements + c->K);
+
+    // padded key-major layout: every key starts on a 128-B boundary
+    c->key_off.resize(c->K);
+    uint64_t off = 0;
+    for (int k = 0; k < c->K; ++k) {
+        off = (off + kKeyAlign - 1) / kKeyAlign * kKeyAlign;
+        c->key_off[k] = off;
+        off += c->n[k];
+        c->E += c->n[k];
+    }
+    c->E_pad = (off + kKeyAlign - 1) / kKeyAlign * kKeyAlign;
+    if (cfg->init_weights && cfg->init_num_elements != c->E) {
+        delete c;
+        why = "init_num_elements != E (S:163)";
+        return PHUB_ERR_INVALID_INIT;
+    }
+
+    c->chunks = plan_chunks(c->n, c->ce, c->G, c->policy);
+    build_ranges(c);
+
+    for (const auto& ch : c->chunks)
+        if (ch.owner == c->rank) c->owned_elems += ch.length;
+    std::vector<Tile> tiles = build_tiles(c);
+    c->n_tiles = tiles.size();
+    c->got.assign((size_t)c->K * c->N, 0);
+    c->base.assign((size_t)c->K * c->N, 0);
+
+    DeviceGuard g(c->device);
+    cudaError_t e;
+    int cnt = 0;
+    if ((e = cudaGetDeviceCount(&cnt)) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        why = std::string("no CUDA device: ") + cudaGetErrorString(e);
+        return PHUB_ERR_CUDA;
+    }
+    if (c->device >= cnt) {
+        delete c;
+        why = "device ordinal out of range";
+        return PHUB_ERR_INVALID_ARGUMENT;
+    }
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+    const size_t bytes = c->E_pad * sizeof(float);
+    if ((e = cudaMalloc(&c->d_w, bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_v, bytes)) != cudaSuccess ||
+        (c->keep_agg && (e = cudaMalloc(&c->d_agg, bytes)) != cudaSuccess) ||
+        (e = cudaMalloc(&c->d_base, sizeof(uintptr_t) * c->base.size())) != cudaSuccess ||
+        (c->n_tiles && (e = cudaMalloc(&c->d_tiles, sizeof(Tile) * c->n_tiles)) != cudaSuccess)) {
+        cudaGetLastError();
+        free_ctx(c);
+        why = std::string("device arenas: ") + cudaGetErrorString(e);
+        return PHUB_ERR_OUT_OF_MEMORY;
+    }
+    bool ok = cudaMemset(c->d_w, 0, bytes) == cudaSuccess &&
+              cudaMemset(c->d_v, 0, bytes) == cudaSuccess &&
+              (!c->d_agg || cudaMemset(c->d_agg, 0, bytes) == cudaSuccess) &&
+              (!c->n_tiles || cudaMemcpy(c->d_tiles, tiles.data(), sizeof(Tile) * c->n_tiles,
+                                         cudaMemcpyHostToDevice) == cudaSuccess);
+    if (ok && cfg->init_weights) {
+        uint64_t src = 0;
+        for (int k = 0; ok && k < c->K; ++k) {
+            ok = cudaMemcpy(c->d_w + c->key_off[k], cfg->init_weights + src,
+                            c->n[k] * sizeof(float), cudaMemcpyDefault) == cudaSuccess;
+            src += c->n[k];
+        }
+    }
+    if (!ok || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+        why = std::string("init copies: ") + cudaGetErrorString(cudaGetLastError());
+        free_ctx(c);
+        return PHUB_ERR_CUDA;
+    }
+    for (int vec8 = 0; vec8 < 2; ++vec8)
+        for (int agg = 0; agg < 2; ++agg)
+            c->flat_grid[vec8][agg] =
+                c->num_sms * phub::flat_blocks_per_sm(vec8 ? 8 : 4, c->N, agg, c->cache);
+    *out = c;
+    return PHUB_OK;
+}
+
+phub_status phub_plan_chunks(const uint64_t* key_num_elements, int32_t num_keys,
+                             uint64_t chunk_size_bytes, int32_t num_owners, int32_t owner_policy,
+                             phub_chunk* out, uint64_t cap, uint64_t* count) {
+    std::string& why = g_init_err;
+    why.clear();
+    phub_config cfg;
+    phub_config_default(&cfg);
+    cfg.key_num_elements = key_num_elements;
+    cfg.num_keys = num_keys;
+    cfg.chunk_size_bytes = chunk_size_bytes;
+    cfg.num_owners = num_owners;
+    cfg.owner_policy = owner_policy;
+    phub_status st = validate_config(&cfg, why);
+    if (st != PHUB_OK) return st;
+    if (!count || (cap && !out)) return why = "count/out is NULL", PHUB_ERR_INVALID_ARGUMENT;
+    const uint64_t ce = (chunk_size_bytes ? chunk_size_bytes : kDefaultChunkBytes) / 4;
+    std::vector<uint64_t> n(key_num_elements, key_num_elements + num_keys);
+    std::vector<phub_chunk> ch = plan_chunks(n, ce, num_owners, owner_policy);
+    *count = ch.size();
+    if (cap == 0) return PHUB_OK;
+    if (cap < ch.size()) return why = "cap < number of chunks", PHUB_ERR_LENGTH_MISMATCH;
+    std::copy(ch.begin(), ch.end(), out);
+    return PHUB_OK;
+}
+
+phub_status phub_destroy(phub_ctx ctx) {
+    if (!ctx) return PHUB_ERR_INVALID_ARGUMENT;
+    free_ctx(ctx);
+    return PHUB_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad, uint64_t n,
+                      int32_t mode, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    if (worker < 0 || worker >= c->N)
+        return c->fail(PHUB_ERR_BAD_WORKER, "worker %d not in [0,%d) (S:170)", worker, c->N);
+    const bool all = key == PHUB_ALL_KEYS;
+    if (!all && (key < 0 || key >= c->K))
+        return c->fail(PHUB_ERR_BAD_KEY, "key %d not in [0,%d) and not PHUB_ALL_KEYS", key, c->K);
+    const uint64_t want = all ? c->E_pad : c->n[key];
+    if (n != want)
+        return c->fail(PHUB_ERR_LENGTH_MISMATCH, "push length %llu != %llu (S:172)",
+                       (unsigned long long)n, (unsigned long long)want);
+    if (!grad) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "grad is NULL");
+    if (mode != PHUB_COPY && mode != PHUB_BORROW)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "mode must be PHUB_COPY or PHUB_BORROW");
+    const int k0 = all ? 0 : key, k1 = all ? c->K : key + 1;
+    for (int k = k0; k < k1; ++k)
+        if (c->got[(size_t)k * c->N + worker])
+            return c->fail(PHUB_ERR_DUPLICATE_PUSH,
+                           "worker %d already pushed key %d this iteration (S:176)", worker, k);
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (mode == PHUB_BORROW) {
+        if (!is_device_ptr(grad))
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW needs device memory");
+        if (reinterpret_cast<uintptr_t>(grad) % 16 != 0)
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW pointer must be 16-B aligned");
+        for (int k = k0; k < k1; ++k)
+            c->base[(size_t)worker * c->K + k] =
+                all ? reinterpret_cast<uintptr_t>(grad)
+                    : reinterpret_cast<uintptr_t>(grad) - 4 * c->key_off[k];
+    } else {
+        if (!c->d_recv) {
+            cudaError_t e = cudaMalloc(&c->d_recv, sizeof(float) * c->E_pad * c->N);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                c->d_recv = nullptr;
+                return c->fail(PHUB_ERR_OUT_OF_MEMORY, "receive arena: %s", cudaGetErrorString(e));
+            }
+            if ((e = cudaMemset(c->d_recv, 0, sizeof(float) * c->E_pad * c->N)) != cudaSuccess)
+                return c->cuda_fail(e, "cudaMemset(recv)");
+        }
+        float* slot = c->d_recv + (uint64_t)worker * c->E_pad;
+        cudaError_t e = cudaSuccess;
+        if (all) {
+            uint64_t b = 0, eend = c->E_pad;
+            if (contig_mode(c)) {
+                b = c->own_begin[c->rank];
+                eend = c->own_end[c->rank];
+            }
+            if (eend > b)
+                e = cudaMemcpyAsync(slot + b, grad + b, (eend - b) * sizeof(float),
+                                    cudaMemcpyDefault, s);
+        } else {
+            e = cudaMemcpyAsync(slot + c->key_off[key], grad, c->n[key] * sizeof(float),
+                                cudaMemcpyDefault, s);
+        }
+        if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpyAsync(push)");
+        for (int k = k0; k < k1; ++k)
+            c->base[(size_t)worker * c->K + k] = reinterpret_cast<uintptr_t>(slot);
+    }
+    for (int k = k0; k < k1; ++k) c->got[(size_t)k * c->N + worker] = 1;
+    c->got_count += (uint64_t)(k1 - k0);
+    return PHUB_OK;
+}
+
+phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    if (c->got_count != (uint64_t)c->K * c->N)
+        return c->fail(PHUB_ERR_INCOMPLETE, "%llu of %llu (worker,key) pushes received (S:181)",
+                       (unsigned long long)c->got_count,
+                       (unsigned long long)((uint64_t)c->K * c->N));
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+    // Flat eligibility: contiguous ownership and every worker's keys share one base.
+    bool flat = contig_mode(c) && c->N <= phub::kMaxWorkers && c->ce % 4 == 0;
+    bool align32 = c->ce % 8 == 0;
+    for (int w = 0; flat && w < c->N; ++w) {
+        const uintptr_t b0 = c->base[(size_t)w * c->K];
+        for (int k = 1; k < c->K; ++k)
+            if (c->base[(size_t)w * c->K + k] != b0) {
+                flat = false;
+                break;
+            }
+        align32 &= b0 % 32 == 0;
+    }
+    int variant = c->kernel;
+    if (variant == PHUB_KERNEL_AUTO)
+        variant = !flat ? PHUB_KERNEL_TILES : (align32 ? PHUB_KERNEL_FLAT : PHUB_KERNEL_FLAT128);
+    if ((variant == PHUB_KERNEL_FLAT && !(flat && align32)) ||
+        ((variant == PHUB_KERNEL_FLAT128 || variant == PHUB_KERNEL_WIDE) && !flat))
+        return c->fail(PHUB_ERR_UNSUPPORTED, "forced kernel variant %d needs whole-model pushes, "
+                       "contiguous ownership and aligned chunks", variant);
+    if (variant == PHUB_KERNEL_WIDE && !c->keep_agg)
+        return c->fail(PHUB_ERR_UNSUPPORTED, "wide ablation needs keep_aggregate (merge buffer)");
+
+    cudaError_t e = cudaSuccess;
+    c->launches = 0;
+    const uint64_t b = contig_mode(c) ? c->own_begin[c->rank] : 0;
+    const uint64_t eend = contig_mode(c) ? c->own_end[c->rank] : 0;
+    if (variant == PHUB_KERNEL_FLAT || variant == PHUB_KERNEL_FLAT128) {
+        phub::FlatArgs a{};
+        for (int w = 0; w < c->N; ++w) a.g[w] = reinterpret_cast<const float*>(c->base[(size_t)w * c->K]);
+        a.w = c->d_w;
+        a.v = c->d_v;
+        a.agg = c->keep_agg ? c->d_agg : nullptr;
+        a.begin = b;
+        a.end = eend;
+        a.lr = c->lr;
+        a.mu = c->mu;
+        a.rescale = c->rescale;
+        a.nw = c->N;
+        const int vec = variant == PHUB_KERNEL_FLAT ? 8 : 4;
+        const uint64_t nvec = (eend - b) / vec;
+        int grid = c->grid_override ? c->grid_override : c->flat_grid[vec == 8][c->keep_agg];
+        grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, (nvec + phub::kThreads - 1) /
+                                                                      phub::kThreads));
+        e = phub::launch_flat(a, vec, c->cache, grid, s, &c->launches);
+    } else if (variant == PHUB_KERNEL_WIDE) {
+        phub::WideArgs a{};
+        for (int w = 0; w < c->N; ++w) a.g[w] = reinterpret_cast<const float*>(c->base[(size_t)w * c->K]);
+        a.w = c->d_w;
+        a.v = c->d_v;
+        a.agg = c->d_agg;
+        a.begin = b;
+        a.end = eend;
+        a.lr = c->lr;
+        a.mu = c->mu;
+        a.rescale = c->rescale;
+        a.nw = c->N;
+        int grid = c->grid_override ? c->grid_override : c->num_sms * 8;
+        e = phub::launch_wide(a, grid, s, &c->launches);
+    } else {
+        if (c->base != c->base_uploaded) {
+            // pageable source: returns once staged, so `base` may change afterwards
+            e = cudaMemcpyAsync(c->d_base, c->base.data(), sizeof(uintptr_t) * c->base.size(),
+                                cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpyAsync(base table)");
+            c->base_uploaded = c->base;
+        }
+        phub::TileArgs a{};
+        a.tiles = c->d_tiles;
+        a.ntiles = c->n_tiles;
+        a.base = c->d_base;
+        a.K = c->K;
+        a.nw = c->N;
+        a.w = c->d_w;
+        a.v = c->d_v;
+        a.agg = c->keep_agg ? c->d_agg : nullptr;
+        a.lr = c->lr;
+        a.mu = c->mu;
+        a.rescale = c->rescale;
+        int grid = c->grid_override ? c->grid_override
+                                    : (int)std::min<uint64_t>(c->n_tiles, 1u << 30);
+        e = phub::launch_tiles(a, std::max(grid, 1), s, &c->launches);
+    }
+    c->launches_total += (uint64_t)c->launches;
+    if (e != cudaSuccess) return c->cuda_fail(e, "kernel launch");
+    std::fill(c->got.begin(), c->got.end(), 0);
+    c->got_count = 0;
+    ++c->iteration;
+    return PHUB_OK;
+}
+
+phub_status phub_pull(phub_ctx c, int32_t key, float* dst, uint64_t n, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    const bool all = key == PHUB_ALL_KEYS;
+    if (!all && (key < 0 || key >= c->K))
+        return c->fail(PHUB_ERR_BAD_KEY, "key %d not in [0,%d) and not PHUB_ALL_KEYS", key, c->K);
+    const uint64_t want = all ? c->E_pad : c->n[key];
+    if (n != want)
+        return c->fail(PHUB_ERR_LENGTH_MISMATCH, "pull length %llu != %llu",
+                       (unsigned long long)n, (unsigned long long)want);
+    if (!dst) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "dst is NULL");
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaMemcpyAsync(dst, c->d_w + (all ? 0 : c->key_off[key]), n * sizeof(float),
+                                    cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpyAsync(pull)");
+    return PHUB_OK;
+}
+
+phub_status phub_pushpull(phub_ctx c, int32_t worker, const float* grad, uint64_t n,
+                          int32_t mode, float* dst, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    phub_status st = phub_push(c, worker, PHUB_ALL_KEYS, grad, n, mode, stream);
+    if (st != PHUB_OK) return st;
+    if (c->got_count != (uint64_t)c->K * c->N) return PHUB_OK;
+    st = phub_aggregate_optimize(c, stream);
+    if (st != PHUB_OK || !dst) return st;
+    return phub_pull(c, PHUB_ALL_KEYS, dst, c->E_pad, stream);
+}
+
+phub_status phub_weights(phub_ctx c, float** w_dev) {
+    if (!c || !w_dev) return PHUB_ERR_INVALID_ARGUMENT;
+    *w_dev = c->d_w;
+    return PHUB_OK;
+}
+
+phub_status phub_layout(phub_ctx c, uint64_t* E, uint64_t* E_padded, uint64_t* key_offsets) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (E) *E = c->E;
+    if (E_padded) *E_padded = c->E_pad;
+    if (key_offsets) std::copy(c->key_off.begin(), c->key_off.end(), key_offsets);
+    return PHUB_OK;
+}
+
+phub_status phub_num_chunks(phub_ctx c, uint64_t* n) {
+    if (!c || !n) return PHUB_ERR_INVALID_ARGUMENT;
+    *n = c->chunks.size();
+    return PHUB_OK;
+}
+
+phub_status phub_chunk_table(phub_ctx c, phub_chunk* out, uint64_t cap) {
+    if (!c || !out) return PHUB_ERR_INVALID_ARGUMENT;
+    if (cap < c->chunks.size())
+        return c->fail(PHUB_ERR_LENGTH_MISMATCH, "capacity %llu < %zu chunks",
+                       (unsigned long long)cap, c->chunks.size());
+    std::copy(c->chunks.begin(), c->chunks.end(), out);
+    return PHUB_OK;
+}
+
+phub_status phub_owner_range(phub_ctx c, int32_t owner, uint64_t* begin, uint64_t* end) {
+    if (!c || !begin || !end) return PHUB_ERR_INVALID_ARGUMENT;
+    if (owner < 0 || owner >= c->G) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "bad owner %d", owner);
+    if (!contig_mode(c))
+        return c->fail(PHUB_ERR_UNSUPPORTED, "owner ranges exist only under CONTIG ownership");
+    *begin = c->own_begin[owner];
+    *end = c->own_end[owner];
+    return PHUB_OK;
+}
+
+phub_status phub_owned_elements(phub_ctx c, uint64_t* n) {
+    if (!c || !n) return PHUB_ERR_INVALID_ARGUMENT;
+    *n = c->owned_elems;
+    return PHUB_OK;
+}
+
+static phub_status scatter_keys(phub_ctx c, float* dst_dev, const float* src) {
+    uint64_t s = 0;
+    for (int k = 0; k < c->K; ++k) {
+        cudaError_t e = cudaMemcpy(dst_dev + c->key_off[k], src + s, c->n[k] * sizeof(float),
+                                   cudaMemcpyDefault);
+        if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpy(load_state)");
+        s += c->n[k];
+    }
+    return PHUB_OK;
+}
+
+static phub_status gather_keys(phub_ctx c, float* dst, const float* src_dev) {
+    uint64_t s = 0;
+    for (int k = 0; k < c->K; ++k) {
+        cudaError_t e = cudaMemcpy(dst + s, src_dev + c->key_off[k], c->n[k] * sizeof(float),
+                                   cudaMemcpyDefault);
+        if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpy(read_state)");
+        s += c->n[k];
+    }
+    return PHUB_OK;
+}
+
+phub_status phub_load_state(phub_ctx c, const float* w, const float* v) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return c->cuda_fail(e, "cudaDeviceSynchronize");
+    phub_status st = PHUB_OK;
+    if (w && (st = scatter_keys(c, c->d_w, w)) != PHUB_OK) return st;
+    if (v && (st = scatter_keys(c, c->d_v, v)) != PHUB_OK) return st;
+    return PHUB_OK;
+}
+
+phub_status phub_read_state(phub_ctx c, float* w, float* v, float* agg) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    if (agg && !c->keep_agg)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "agg requested but keep_aggregate is off");
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return c->cuda_fail(e, "cudaDeviceSynchronize");
+    phub_status st = PHUB_OK;
+    if (w && (st = gather_keys(c, w, c->d_w)) != PHUB_OK) return st;
+    if (v && (st = gather_keys(c, v, c->d_v)) != PHUB_OK) return st;
+    if (agg && (st = gather_keys(c, agg, c->d_agg)) != PHUB_OK) return st;
+    return PHUB_OK;
+}
+
+phub_status phub_iteration(phub_ctx c, uint64_t* it) {
+    if (!c || !it) return PHUB_ERR_INVALID_ARGUMENT;
+    *it = c->iteration;
+    return PHUB_OK;
+}
+
+phub_status phub_kernel_launches(phub_ctx c, uint64_t* n) {
+    if (!c || !n) return PHUB_ERR_INVALID_ARGUMENT;
+    *n = c->launches_total;
+    return PHUB_OK;
+}
+
+phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    switch (option) {
+        case PHUB_OPT_KERNEL:
+            if (value < PHUB_KERNEL_AUTO || value > PHUB_KERNEL_WIDE)
+                return c->fail(PHUB_ERR_INVALID_ARGUMENT, "unknown kernel variant");
+            c->kernel = (int)value;
+            return PHUB_OK;
+        case PHUB_OPT_GRID:
+            if (value < 0 || value > (1 << 30)) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "bad grid");
+            c->grid_override = (int)value;
+            return PHUB_OK;
+        case PHUB_OPT_CACHE: {
+            if (value != PHUB_CACHE_ENABLED && value != PHUB_CACHE_BYPASS)
+                return c->fail(PHUB_ERR_INVALID_ARGUMENT, "unknown cache mode");
+            c->cache = (int)value;
+            DeviceGuard g(c->device);
+            for (int vec8 = 0; vec8 < 2; ++vec8)
+                for (int agg = 0; agg < 2; ++agg)
+                    c->flat_grid[vec8][agg] =
+                        c->num_sms * phub::flat_blocks_per_sm(vec8 ? 8 : 4, c->N, agg, c->cache);
+            return PHUB_OK;
+        }
+        case PHUB_OPT_TILE_ELEMS: {
+            if (value < 1 || value > (1 << 30))
+                return c->fail(PHUB_ERR_INVALID_ARGUMENT, "tile elements must be in [1, 2^30]");
+            if (c->failed) return PHUB_ERR_CUDA;
+            DeviceGuard g(c->device);
+            const uint32_t old = c->tile_elems;
+            c->tile_elems = (uint32_t)value;
+            std::vector<Tile> tiles = build_tiles(c);
+            Tile* d = nullptr;
+            cudaError_t e = cudaSuccess;
+            if (!tiles.empty()) {
+                if ((e = cudaMalloc(&d, sizeof(Tile) * tiles.size())) != cudaSuccess) {
+                    cudaGetLastError();
+                    c->tile_elems = old;
+                    return c->fail(PHUB_ERR_OUT_OF_MEMORY, "tile table: %s", cudaGetErrorString(e));
+                }
+                if ((e = cudaDeviceSynchronize()) != cudaSuccess ||
+                    (e = cudaMemcpy(d, tiles.data(), sizeof(Tile) * tiles.size(),
+                                    cudaMemcpyHostToDevice)) != cudaSuccess)
+                    return c->cuda_fail(e, "tile table upload");
+            }
+            cudaFree(c->d_tiles);
+            c->d_tiles = d;
+            c->n_tiles = tiles.size();
+            return PHUB_OK;
+        }
+        default:
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "unknown option %d", option);
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+// phub_kernels.cu -- sm_100a kernels of the PHub hot path.
+//
+// The one hot operation is the fused "tall" aggregation + Nesterov update
+// (the thread that sums a chunk across all workers also
+// optimizes it; P:783 Nesterov SGD; recurrence S:189, reading R1):
+//
+//   s  = (((+0.0f + g_0) + g_1) + ...) + g_{N-1}      worker-id order (R3, R4)
+//   g  = s * rescale                                  (R2)
+//   v' = mu*v + g ;  w' = w - lr*(g + mu*v')
+//
+// every op rounded separately (__fadd_rn/__fmul_rn/__fsub_rn: no FMA
+// contraction, R5; no FTZ, R6).  It is a streaming element-wise update at
+// ~0.3 flop/B, so it is HBM-bound: (4N+16) B per element (N gradient reads,
+// w and v read and written), no tensor cores (nothing is a contraction).
+//
+// Kernels:
+//   k_flat   owned padded range walked as 256-bit (LDG.E.256/STG.E.256, new on
+//            sm_100a) or 128-bit vectors; persistent grid sized to
+//            SMs x resident CTAs; workers' bases in kernel params.
+//   k_tiles  one CTA per chunk tile (PHub's chunk -> core mapping, P:708-713,
+//            with the hardware CTA scheduler as the "core" assigner); worker
+//            pointers per (worker, key) for per-key pushes; 128-bit body +
+//            scalar tail per tile.
+//   k_wide_* ablation of MXNet-style wide aggregation: N-1
+//            pairwise passes then a separate optimizer pass; same arithmetic,
+//            12(N-1)+20 B/elt instead of 4N+16.
+#include "phub_kernels.cuh"
+#include "phub.h"
+
+namespace phub {
+namespace {
+
+template <int VEC>
+struct alignas(VEC * 4) VecT {
+    float x[VEC];
+};
+using V8 = VecT<8>;
+using V4 = VecT<4>;
+
+// ------------------------------------------------------------ memory access
+// Gradients are read exactly once per round: non-coherent path, no L1
+// allocation, L2 evict-first (the 256-bit form is the one that takes an L2
+// eviction-priority qualifier on sm_100a).
+__device__ __forceinline__ V8 ld_grad(const V8* p) {
+    V8 r;
+    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]), "=f"(r.x[5]),
+          "=f"(r.x[6]), "=f"(r.x[7])
+        : "l"(p));
+    return r;
+}
+__device__ __forceinline__ V4 ld_grad(const V4* p) {
+    V4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+        : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3])
+        : "l"(p));
+    return r;
+}
+
+// Model state (w, v): read then rewritten by the same thread.
+template <int CACHE>
+__device__ __forceinline__ V8 ld_state(const V8* p) {
+    V8 r;
+    if (CACHE == PHUB_CACHE_BYPASS)
+        asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
+                       "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
+                     : "l"(p));
+    else
+        asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
+                       "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
+                     : "l"(p));
+    return r;
+}
+template <int CACHE>
+__device__ __forceinline__ V4 ld_state(const V4* p) {
+    V4 r;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3])
+                 : "l"(p));
+    return r;
+}
+
+// Updated weights: under PHUB_CACHE_ENABLED they are stored L2 evict-last so
+// a pull / all-gather that follows is served from L2 ("models can be sent
+// directly from cache after being updated"); under BYPASS they stream.
+template <int CACHE>
+__device__ __forceinline__ void st_w(V8* p, const V8& r) {
+    if (CACHE == PHUB_CACHE_BYPASS)
+        asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                     :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]),
+                        "f"(r.x[5]), "f"(r.x[6]), "f"(r.x[7]) : "memory");
+    else
+        asm volatile("st.global.L1::no_allocate.L2::evict_last.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                     :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]),
+                        "f"(r.x[5]), "f"(r.x[6]), "f"(r.x[7]) : "memory");
+}
+template <int CACHE>
+__device__ __forceinline__ void st_w(V4* p, const V4& r) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]) : "memory");
+}
+// Momentum and the test-mode sum are only re-read next round: stream them.
+__device__ __forceinline__ void st_stream(V8* p, const V8& r) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]),
+                    "f"(r.x[5]), "f"(r.x[6]), "f"(r.x[7]) : "memory");
+}
+__device__ __forceinline__ void st_stream(V4* p, const V4& r) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]) : "memory");
+}
+
+// ------------------------------------------------------------- arithmetic
+// Nesterov step on one element, each op rounded separately (R5).
+__device__ __forceinline__ void nag(float s, float& w, float& v, float lr, float mu,
+                                    float rescale) {
+    const float g = __fmul_rn(s, rescale);
+    const float vn = __fadd_rn(__fmul_rn(mu, v), g);
+    const float t3 = __fadd_rn(g, __fmul_rn(mu, vn));
+    w = __fsub_rn(w, __fmul_rn(lr, t3));
+    v = vn;
+}
+
+// ------------------------------------------------------------ flat kernel
+// NW > 0: worker count fixed at compile time; NW == 0: any count <= 64, in
+// groups of 8 loads issued before their in-order adds.
+template <int NW, int VEC, int CACHE, bool AGG>
+__global__ void __launch_bounds__(kThreads) k_flat(const __grid_constant__ FlatArgs a) {
+    using V = VecT<VEC>;
+    const uint64_t n = (a.end - a.begin) / VEC;
+    V* __restrict__ w = reinterpret_cast<V*>(a.w + a.begin);
+    V* __restrict__ v = reinterpret_cast<V*>(a.v + a.begin);
+    V* __restrict__ sa = AGG ? reinterpret_cast<V*>(a.agg + a.begin) : nullptr;
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+        float acc[VEC];
+        if constexpr (NW > 0) {
+            V gv[NW];
+#pragma unroll
+            for (int k = 0; k < NW; ++k)
+                gv[k] = ld_grad(reinterpret_cast<const V*>(a.g[k] + a.begin) + i);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) {
+                float s = __fadd_rn(0.0f, gv[0].x[j]);
+#pragma unroll
+                for (int k = 1; k < NW; ++k) s = __fadd_rn(s, gv[k].x[j]);
+                acc[j] = s;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[j] = 0.0f;
+            for (int k0 = 0; k0 < a.nw; k0 += 8) {
+                V gv[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (k0 + k < a.nw)
+                        gv[k] = ld_grad(reinterpret_cast<const V*>(a.g[k0 + k] + a.begin) + i);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (k0 + k < a.nw) {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+                    }
+            }
+        }
+        V wv = ld_state<CACHE>(w + i);
+        V vv = ld_state<CACHE>(v + i);
+        V sv;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+            sv.x[j] = acc[j];
+            nag(acc[j], wv.x[j], vv.x[j], a.lr, a.mu, a.rescale);
+        }
+        st_w<CACHE>(w + i, wv);
+        st_stream(v + i, vv);
+        if constexpr (AGG) st_stream(sa + i, sv);
+    }
+}
+
+// ---------------------------------------------------------- chunk tiles
+template <int NW, bool AGG>
+__global__ void __launch_bounds__(kThreads) k_tiles(const __grid_constant__ TileArgs a) {
+    for (uint64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const Tile tl = a.tiles[t];
+        const int nw = NW > 0 ? NW : a.nw;
+        // Vector body only if every stream of this tile is 16-B aligned.
+        bool aligned = (tl.off % 4) == 0;
+        for (int k = 0; k < nw; ++k)
+            aligned &= ((a.base[(uint64_t)k * a.K + tl.key] + 4 * tl.off) % 16) == 0;
+        const uint32_t nvec = aligned ? tl.len / 4 : 0;
+        float* w = a.w + tl.off;
+        float* v = a.v + tl.off;
+        for (uint32_t j = threadIdx.x; j < nvec; j += kThreads) {
+            float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            if constexpr (NW > 0) {
+                V4 gv[NW];
+#pragma unroll
+                for (int k = 0; k < NW; ++k)
+                    gv[k] = ld_grad(reinterpret_cast<const V4*>(
+                                        a.base[(uint64_t)k * a.K + tl.key] + 4 * tl.off) + j);
+#pragma unroll
+                for (int k = 0; k < NW; ++k)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[e] = __fadd_rn(acc[e], gv[k].x[e]);
+            } else {
+                for (int k = 0; k < nw; ++k) {
+                    const V4 gk = ld_grad(reinterpret_cast<const V4*>(
+                                              a.base[(uint64_t)k * a.K + tl.key] + 4 * tl.off) + j);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[e] = __fadd_rn(acc[e], gk.x[e]);
+                }
+            }
+            V4 wv = ld_state<PHUB_CACHE_ENABLED>(reinterpret_cast<const V4*>(w) + j);
+            V4 vv = ld_state<PHUB_CACHE_ENABLED>(reinterpret_cast<const V4*>(v) + j);
+            V4 sv;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                sv.x[e] = acc[e];
+                nag(acc[e], wv.x[e], vv.x[e], a.lr, a.mu, a.rescale);
+            }
+            st_w<PHUB_CACHE_ENABLED>(reinterpret_cast<V4*>(w) + j, wv);
+            st_stream(reinterpret_cast<V4*>(v) + j, vv);
+            if constexpr (AGG) st_stream(reinterpret_cast<V4*>(a.agg + tl.off) + j, sv);
+        }
+        // scalar tail (short last chunk of a key, or a misaligned tile)
+        for (uint32_t e = nvec * 4 + threadIdx.x; e < tl.len; e += kThreads) {
+            float s = 0.0f;
+            for (int k = 0; k < nw; ++k) {
+                const float* gk = reinterpret_cast<const float*>(
+                    a.base[(uint64_t)k * a.K + tl.key] + 4 * tl.off);
+                s = __fadd_rn(s, __ldg(gk + e));
+            }
+            float wv = w[e], vv = v[e];
+            nag(s, wv, vv, a.lr, a.mu, a.rescale);
+            w[e] = wv;
+            v[e] = vv;
+            if constexpr (AGG) a.agg[tl.off + e] = s;
+        }
+    }
+}
+
+// -------------------------------------------------------- wide (ablation)
+// pass 1: merge = (+0 + g0) [+ g1];  pass k: merge = merge + gk;  NAG pass.
+__global__ void __launch_bounds__(kThreads) k_wide_first(const __grid_constant__ WideArgs a) {
+    const uint64_t n = (a.end - a.begin) / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+        const V4 g0 = ld_grad(reinterpret_cast<const V4*>(a.g[0] + a.begin) + i);
+        V4 s;
+        if (a.nw > 1) {
+            const V4 g1 = ld_grad(reinterpret_cast<const V4*>(a.g[1] + a.begin) + i);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) s.x[e] = __fadd_rn(__fadd_rn(0.0f, g0.x[e]), g1.x[e]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) s.x[e] = __fadd_rn(0.0f, g0.x[e]);
+        }
+        reinterpret_cast<V4*>(a.agg + a.begin)[i] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_wide_add(const __grid_constant__ WideArgs a, int k) {
+    const uint64_t n = (a.end - a.begin) / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+        const V4 gk = ld_grad(reinterpret_cast<const V4*>(a.g[k] + a.begin) + i);
+        V4 s = reinterpret_cast<V4*>(a.agg + a.begin)[i];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s.x[e] = __fadd_rn(s.x[e], gk.x[e]);
+        reinterpret_cast<V4*>(a.agg + a.begin)[i] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_wide_nag(const __grid_constant__ WideArgs a) {
+    const uint64_t n = (a.end - a.begin) / 4;
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+        const V4 s = reinterpret_cast<const V4*>(a.agg + a.begin)[i];
+        V4 wv = reinterpret_cast<V4*>(a.w + a.begin)[i];
+        V4 vv = reinterpret_cast<V4*>(a.v + a.begin)[i];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) nag(s.x[e], wv.x[e], vv.x[e], a.lr, a.mu, a.rescale);
+        reinterpret_cast<V4*>(a.w + a.begin)[i] = wv;
+        reinterpret_cast<V4*>(a.v + a.begin)[i] = vv;
+    }
+}
+
+// ------------------------------------------------------------- dispatch
+using FlatFn = void (*)(FlatArgs);
+using TileFn = void (*)(TileArgs);
+
+template <int VEC, int CACHE, bool AGG>
+FlatFn pick_flat_nw(int nw) {
+    switch (nw) {
+        case 1: return k_flat<1, VEC, CACHE, AGG>;
+        case 2: return k_flat<2, VEC, CACHE, AGG>;
+        case 3: return k_flat<3, VEC, CACHE, AGG>;
+        case 4: return k_flat<4, VEC, CACHE, AGG>;
+        case 5: return k_flat<5, VEC, CACHE, AGG>;
+        case 6: return k_flat<6, VEC, CACHE, AGG>;
+        case 7: return k_flat<7, VEC, CACHE, AGG>;
+        case 8: return k_flat<8, VEC, CACHE, AGG>;
+        default: return k_flat<0, VEC, CACHE, AGG>;
+    }
+}
+
+FlatFn pick_flat(int vec, int nw, bool agg, int cache) {
+    if (vec == 8) {
+        if (cache == PHUB_CACHE_BYPASS)
+            return agg ? pick_flat_nw<8, PHUB_CACHE_BYPASS, true>(nw)
+                       : pick_flat_nw<8, PHUB_CACHE_BYPASS, false>(nw);
+        return agg ? pick_flat_nw<8, PHUB_CACHE_ENABLED, true>(nw)
+                   : pick_flat_nw<8, PHUB_CACHE_ENABLED, false>(nw);
+    }
+    return agg ? pick_flat_nw<4, PHUB_CACHE_ENABLED, true>(nw)
+               : pick_flat_nw<4, PHUB_CACHE_ENABLED, false>(nw);
+}
+
+template <bool AGG>
+TileFn pick_tiles_nw(int nw) {
+    switch (nw) {
+        case 1: return k_tiles<1, AGG>;
+        case 2: return k_tiles<2, AGG>;
+        case 3: return k_tiles<3, AGG>;
+        case 4: return k_tiles<4, AGG>;
+        case 5: return k_tiles<5, AGG>;
+        case 6: return k_tiles<6, AGG>;
+        case 7: return k_tiles<7, AGG>;
+        case 8: return k_tiles<8, AGG>;
+        default: return k_tiles<0, AGG>;
+    }
+}
+
+}  // namespace
+
+int flat_blocks_per_sm(int vec, int nw, bool agg, int cache) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &nb, reinterpret_cast<const void*>(pick_flat(vec, nw, agg, cache)), kThreads, 0) !=
+        cudaSuccess)
+        return 1;
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_flat(const FlatArgs& a, int vec, int cache, int grid, cudaStream_t s,
+                        int* launches) {
+    if (a.end <= a.begin) return cudaSuccess;
+    pick_flat(vec, a.nw, a.agg != nullptr, cache)<<<grid, kThreads, 0, s>>>(a);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tiles(const TileArgs& a, int grid, cudaStream_t s, int* launches) {
+    if (a.ntiles == 0) return cudaSuccess;
+    TileFn fn = a.agg ? pick_tiles_nw<true>(a.nw) : pick_tiles_nw<false>(a.nw);
+    fn<<<grid, kThreads, 0, s>>>(a);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wide(const WideArgs& a, int grid, cudaStream_t s, int* launches) {
+    if (a.end <= a.begin) return cudaSuccess;
+    k_wide_first<<<grid, kThreads, 0, s>>>(a);
+    ++*launches;
+    for (int k = 2; k < a.nw; ++k) {
+        k_wide_add<<<grid, kThreads, 0, s>>>(a, k);
+        ++*launches;
+    }
+    k_wide_nag<<<grid, kThreads, 0, s>>>(a);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace phub

@@ -1,0 +1,61 @@
+// Internal launch interface between the host core (phub_core.cpp) and the
+// sm_100a kernels (phub_kernels.cu).  Not part of the C ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace phub {
+
+constexpr int kMaxWorkers = 64;       // flat-kernel pointer array capacity
+constexpr int kThreads = 256;         // CTA size of every hot kernel
+
+// One CTA tile of an owned chunk (chunk-tile kernel).  `off` is the element
+// offset in the padded device layout, `key` the key the chunk belongs to.
+struct Tile {
+    uint64_t off;
+    uint32_t len;
+    uint32_t key;
+};
+
+struct FlatArgs {
+    const float* g[kMaxWorkers];      // worker bases in the padded layout
+    float* w;
+    float* v;
+    float* agg;                       // nullptr unless keep_aggregate
+    uint64_t begin, end;              // owned padded range [begin, end), elements
+    float lr, mu, rescale;
+    int nw;
+};
+
+struct TileArgs {
+    const Tile* tiles;
+    uint64_t ntiles;
+    const uintptr_t* base;            // [nw * K]: base[w*K+k] + 4*off = byte address
+    int K;
+    int nw;
+    float* w;
+    float* v;
+    float* agg;
+    float lr, mu, rescale;
+};
+
+struct WideArgs {                     // ablation: wide aggregation
+    const float* g[kMaxWorkers];
+    float* w;
+    float* v;
+    float* agg;                       // required scratch: the merge buffer
+    uint64_t begin, end;
+    float lr, mu, rescale;
+    int nw;
+};
+
+// vec = 8 (256-bit LDG/STG, sm_100a) or 4 (128-bit).  cache = PHUB_CACHE_*.
+cudaError_t launch_flat(const FlatArgs& a, int vec, int cache, int grid, cudaStream_t s,
+                        int* launches);
+cudaError_t launch_tiles(const TileArgs& a, int grid, cudaStream_t s, int* launches);
+cudaError_t launch_wide(const WideArgs& a, int grid, cudaStream_t s, int* launches);
+
+// Resident CTAs per SM of the flat kernel for (vec, nw, agg) -- grid sizing.
+int flat_blocks_per_sm(int vec, int nw, bool agg, int cache);
+
+}  // namespace phub

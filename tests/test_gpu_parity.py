@@ -1,0 +1,411 @@
+"""GPU parity: the sm_100a path vs the CPU oracle, through the C ABI (-m gpu).
+
+Inputs are generated independently on each side from the same seeded
+counter-based streams (workloads.generate): on the device by values_torch into
+the padded layout (padding filled with NaN so any read of padding would show),
+on the host by values_np for the oracle.  Nothing the CUDA path writes is ever
+fed to the oracle.
+
+Bar (BASELINE.json north_star): chunk table and the worker-order sum
+bit-exact; w' and v' within 1e-6 relative -- this build asserts bit-exact for
+all three (reading R5: no contraction on either side), and reports
+the max relative error when that fails.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import manifest, values_np, grad_stream
+from workloads.generate import values_at_np
+from conftest import read_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+f32 = np.float32
+DEV = "cuda:0"
+
+
+def bits(a):
+    return np.asarray(a, dtype=np.float32).view(np.uint32)
+
+
+def assert_bits_equal(got, ref, what):
+    got, ref = np.asarray(got, f32), np.asarray(ref, f32)
+    if not np.array_equal(bits(got), bits(ref)):
+        bad = np.flatnonzero(bits(got) != bits(ref))
+        rel = np.max(np.abs(got[bad].astype(np.float64) - ref[bad]) /
+                     np.maximum(np.abs(ref[bad].astype(np.float64)), 2.0 ** -126))
+        raise AssertionError(f"{what}: {bad.size} of {ref.size} elements differ bitwise, "
+                             f"first at {bad[:5]}, max rel err {rel:.3e}")
+
+
+def _hub(sizes, N, **kw):
+    from paper_1805_07891_b200 import PHub
+    return PHub(sizes, N, device=0, **kw)
+
+
+def _pad_index(hub):
+    return torch.as_tensor(hub.padded_index(), device=DEV)
+
+
+def device_grads(hub, N, seed=0, shift=25):
+    """N padded device buffers with stream values at real elements, NaN in padding."""
+    from workloads.generate import values_torch
+    idx = _pad_index(hub)
+    out = []
+    for w in range(N):
+        buf = torch.full((hub.E_padded,), float("nan"), dtype=torch.float32, device=DEV)
+        buf[idx] = values_torch(grad_stream(w) + 37 * seed, 0, hub.E, shift, DEV)
+        out.append(buf)
+    return out
+
+
+def host_grads(E, N, seed=0, shift=25):
+    return [values_np(grad_stream(w) + 37 * seed, 0, E, shift) for w in range(N)]
+
+
+def host_state(E, seed=0):
+    return values_np(1 + 37 * seed, 0, E, 20), values_np(2 + 37 * seed, 0, E, 25)
+
+
+def run_round(hub, grads_dev, mode="borrow"):
+    for w, g in enumerate(grads_dev):
+        hub.push(w, g, mode=mode)
+    hub.aggregate_optimize()
+    torch.cuda.synchronize()
+
+
+def check_round(sizes, N, chunk_bytes=32768, kernel=None, seed=0, lr=0.1, mu=0.9, rescale=0.0):
+    from paper_1805_07891_b200 import capi
+    hub = _hub(sizes, N, chunk_size_bytes=chunk_bytes, keep_aggregate=True, lr=lr, momentum=mu,
+               rescale=rescale)
+    w0, v0 = host_state(hub.E, seed)
+    hub.load_state(w0, v0)
+    if kernel is not None:
+        hub.set_option(capi.PHUB_OPT_KERNEL, kernel)
+    gd = device_grads(hub, N, seed)
+    before = hub.kernel_launches
+    run_round(hub, gd)
+    launches = hub.kernel_launches - before
+    w, v, s = hub.read_state()
+    rw, rv, rs = oracle.round_(sizes, host_grads(hub.E, N, seed), w0, v0, lr, mu, rescale,
+                               chunk_bytes=chunk_bytes)
+    assert_bits_equal(s, rs, "sum s")
+    assert_bits_equal(v, rv, "momentum v'")
+    assert_bits_equal(w, rw, "weights w'")
+    return hub, launches
+
+
+SMALL = [3, 3, 9408, 64, 64, 4096, 20000, 1000, 262144, 7]   # 3-element keys break 16-B alignment
+
+
+# ------------------------------------------------------------- basic rounds
+def test_tiny_config_bit_exact():
+    hub, launches = check_round(manifest("tiny"), 4)
+    assert launches == 1                      # one fused kernel per round
+    assert hub.iteration == 1
+
+
+@pytest.mark.parametrize("kernel", ["FLAT", "FLAT128", "TILES", "WIDE"])
+def test_kernel_variants_bit_exact(kernel):
+    from paper_1805_07891_b200 import capi
+    _, launches = check_round(SMALL, 8, kernel=getattr(capi, f"PHUB_KERNEL_{kernel}"))
+    assert launches == (8 if kernel == "WIDE" else 1)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 8, 9, 16, 33])
+def test_worker_counts(N):
+    check_round(SMALL, N, seed=N)
+
+
+@pytest.mark.parametrize("cb", [4, 12, 64, 4096, 32768, 1 << 20])
+def test_chunk_sizes(cb):
+    check_round(SMALL, 4, chunk_bytes=cb)
+
+
+def test_tiles_small_tile_size():
+    from paper_1805_07891_b200 import capi
+    hub = _hub(SMALL, 3, keep_aggregate=True)
+    hub.set_option(capi.PHUB_OPT_TILE_ELEMS, 100)       # ragged tiles inside chunks
+    hub.set_option(capi.PHUB_OPT_KERNEL, capi.PHUB_KERNEL_TILES)
+    w0, v0 = host_state(hub.E)
+    hub.load_state(w0, v0)
+    run_round(hub, device_grads(hub, 3))
+    w, v, s = hub.read_state()
+    rw, rv, rs = oracle.round_(SMALL, host_grads(hub.E, 3), w0, v0, 0.1, 0.9)
+    assert_bits_equal(w, rw, "w")
+    assert_bits_equal(s, rs, "s")
+
+
+def test_rescale_and_hyperparameters():
+    check_round(SMALL, 3, lr=0.37, mu=0.5, rescale=0.25)
+    check_round(SMALL, 6, lr=1e-3, mu=0.0)
+
+
+# ---------------------------------------------------- push / pull semantics
+def test_per_key_and_copy_pushes():
+    sizes = SMALL
+    N = 4
+    hub = _hub(sizes, N, keep_aggregate=True)
+    w0, v0 = host_state(hub.E)
+    hub.load_state(w0, v0)
+    hg = host_grads(hub.E, N)
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    # worker 0: per-key BORROW of unpadded device slices (own allocations)
+    keep = []
+    for k, nk in enumerate(sizes):
+        t = torch.tensor(hg[0][starts[k]:starts[k + 1]], device=DEV)
+        keep.append(t)
+        hub.push(0, t, key=k, mode="borrow")
+    # worker 1: whole-model COPY from a padded host buffer
+    pad = np.full(hub.E_padded, np.nan, f32)
+    pad[hub.padded_index()] = hg[1]
+    hub.push(1, pad, mode="copy")
+    # worker 2: per-key COPY from host, in reverse key order
+    for k in reversed(range(len(sizes))):
+        hub.push(2, np.ascontiguousarray(hg[2][starts[k]:starts[k + 1]]), key=k, mode="copy")
+    # worker 3: whole-model BORROW (device, padded)
+    d3 = device_grads(hub, 4)[3]
+    hub.push(3, d3, mode="borrow")
+    hub.aggregate_optimize()
+    w, v, s = hub.read_state()
+    rw, rv, rs = oracle.round_(sizes, hg, w0, v0, 0.1, 0.9)
+    assert_bits_equal(s, rs, "s")
+    assert_bits_equal(w, rw, "w")
+    assert_bits_equal(v, rv, "v")
+
+
+def test_errors_leave_state_unchanged():
+    from paper_1805_07891_b200 import PhubError, capi
+    sizes = SMALL
+    hub = _hub(sizes, 2, keep_aggregate=True)
+    w0, v0 = host_state(hub.E)
+    hub.load_state(w0, v0)
+    gd = device_grads(hub, 2)
+
+    def status(fn):
+        with pytest.raises(PhubError) as e:
+            fn()
+        return capi.STATUS_NAMES[e.value.status]
+
+    assert status(lambda: hub.aggregate_optimize()) == "PHUB_ERR_INCOMPLETE"
+    hub.push(0, gd[0])
+    assert status(lambda: hub.push(0, gd[0])) == "PHUB_ERR_DUPLICATE_PUSH"
+    assert status(lambda: hub.push(0, gd[0][:sizes[1]], key=1)) == "PHUB_ERR_DUPLICATE_PUSH"
+    assert status(lambda: hub.push(2, gd[1])) == "PHUB_ERR_BAD_WORKER"
+    assert status(lambda: hub.push(1, gd[1], key=len(sizes))) == "PHUB_ERR_BAD_KEY"
+    assert status(lambda: hub.push(1, gd[1][:5], key=0)) == "PHUB_ERR_LENGTH_MISMATCH"
+    assert status(lambda: hub.push(1, gd[1][: hub.E_padded - 32])) == "PHUB_ERR_LENGTH_MISMATCH"
+    assert status(lambda: hub.push(1, np.zeros(hub.E_padded, f32), mode="borrow")) == \
+        "PHUB_ERR_INVALID_ARGUMENT"                                   # host ptr cannot be borrowed
+    assert status(lambda: hub.push(1, gd[1][1:], n=hub.E_padded - 1)) == "PHUB_ERR_LENGTH_MISMATCH"
+    assert status(lambda: hub.push(1, gd[1][1:1 + sizes[0]], key=0)) == \
+        "PHUB_ERR_INVALID_ARGUMENT"                                   # BORROW needs 16-B alignment
+    assert status(lambda: hub.aggregate_optimize()) == "PHUB_ERR_INCOMPLETE"
+    assert hub.iteration == 0
+    hub.push(1, gd[1])
+    hub.aggregate_optimize()
+    w, v, s = hub.read_state()
+    rw, rv, rs = oracle.round_(sizes, host_grads(hub.E, 2), w0, v0, 0.1, 0.9)
+    assert_bits_equal(w, rw, "w after recovered round")
+    assert hub.iteration == 1
+
+
+def test_pull_semantics():
+    sizes = SMALL
+    init = values_np(5, 0, sum(sizes), 20)
+    hub = _hub(sizes, 3, init_weights=init)
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    dst = np.empty(sizes[2], f32)
+    hub.pull(dst, key=2)
+    torch.cuda.synchronize()
+    assert_bits_equal(dst, init[starts[2]:starts[3]], "pull before aggregate (S:365)")
+    gd = device_grads(hub, 3)
+    run_round(hub, gd)
+    rw, _, _ = oracle.round_(sizes, host_grads(hub.E, 3), init, np.zeros_like(init), 0.1, 0.9)
+    full = np.empty(hub.E_padded, f32)
+    hub.pull(full)                                   # host destination
+    torch.cuda.synchronize()
+    assert_bits_equal(full[hub.padded_index()], rw, "ALL_KEYS pull")
+    for k in (0, 6, 9):
+        d = torch.empty(sizes[k], device=DEV)
+        hub.pull(d, key=k)                           # device destination
+        torch.cuda.synchronize()
+        assert_bits_equal(d.cpu().numpy(), rw[starts[k]:starts[k + 1]], f"pull key {k}")
+    wv = hub.weights()                               # zero-copy pull
+    assert_bits_equal(wv.cpu().numpy()[hub.padded_index()], rw, "zero-copy weights")
+
+
+def test_pushpull():
+    sizes = SMALL
+    hub = _hub(sizes, 3)
+    gd = device_grads(hub, 3)
+    out = torch.empty(hub.E_padded, device=DEV)
+    for w in range(3):
+        hub.pushpull(w, gd[w], dst=out)
+        assert hub.iteration == (1 if w == 2 else 0)
+    torch.cuda.synchronize()
+    rw, _, _ = oracle.round_(sizes, host_grads(hub.E, 3), np.zeros(hub.E, f32),
+                             np.zeros(hub.E, f32), 0.1, 0.9)
+    assert_bits_equal(out.cpu().numpy()[hub.padded_index()], rw, "pushpull result")
+
+
+def test_multi_round():
+    sizes = SMALL
+    N = 4
+    hub = _hub(sizes, N, keep_aggregate=True)
+    w, v = host_state(hub.E, 1)
+    hub.load_state(w, v)
+    for r in range(3):
+        run_round(hub, device_grads(hub, N, seed=r))
+        w, v, _ = oracle.round_(sizes, host_grads(hub.E, N, seed=r), w, v, 0.1, 0.9)
+    gw, gv, _ = hub.read_state()
+    assert_bits_equal(gw, w, "w after 3 rounds")
+    assert_bits_equal(gv, v, "v after 3 rounds")
+    assert hub.iteration == 3
+
+
+# -------------------------------------------------------- special cases
+@pytest.mark.parametrize("row", read_golden("nag_cases.txt"), ids=lambda r: r[0])
+def test_nag_golden_on_gpu(row):
+    name, _cite, N, lr, mu, resc, w0, v0, g, ew, ev = row
+    N = int(N)
+    vals = [1.0, 3.0] if name == "s175" else [float(g)] * N
+    hub = _hub([1], N, lr=float(lr), momentum=float(mu), rescale=float(resc),
+               init_weights=np.array([float(w0)], f32))
+    hub.load_state(None, np.array([float(v0)], f32))
+    bufs = []
+    for w in range(N):
+        b = torch.zeros(hub.E_padded, device=DEV)
+        b[0] = vals[w]
+        bufs.append(b)
+    run_round(hub, bufs)
+    gw, gv, _ = hub.read_state()
+    assert bits(gw)[0] == int(ew, 16) and bits(gv)[0] == int(ev, 16)
+
+
+def test_signed_zero_and_dyadic():
+    from workloads import dyadic_np
+    sizes = [5, 1000, 3]
+    hub = _hub(sizes, 8, keep_aggregate=True)
+    idx = _pad_index(hub)
+    zs = []
+    for w in range(8):
+        b = torch.full((hub.E_padded,), float("nan"), device=DEV)
+        b[idx] = -0.0
+        zs.append(b)
+    run_round(hub, zs)
+    _, _, s = hub.read_state()
+    assert not np.any(bits(s))                       # +0 start: never -0 (reading R4)
+    hg = [dyadic_np(60 + w, hub.E) for w in range(8)]
+    bufs = []
+    for w in range(8):
+        b = torch.full((hub.E_padded,), float("nan"), device=DEV)
+        b[idx] = torch.tensor(hg[w], device=DEV)
+        bufs.append(b)
+    run_round(hub, bufs)
+    _, _, s = hub.read_state()
+    exact = np.sum(np.stack(hg).astype(np.float64), axis=0)
+    assert np.array_equal(s.astype(np.float64), exact)
+
+
+def test_lr0_identity():
+    sizes = SMALL
+    hub = _hub(sizes, 5, lr=0.0)
+    w0, v0 = host_state(hub.E, 4)
+    hub.load_state(w0, v0)
+    run_round(hub, device_grads(hub, 5, seed=4))
+    w, _, _ = hub.read_state()
+    assert_bits_equal(w, w0, "lr=0 identity")
+
+
+# ----------------------------------------- owner sharding on one GPU (M2)
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("policy", ["contig", "lpt"])
+def test_owner_sharding_invariance(G, policy):
+    sizes = manifest("resnet50")
+    N = 4
+    E = sum(sizes)
+    w0, v0 = host_state(E, 2)
+    rw, rv, rs = oracle.round_(sizes, host_grads(E, N, 2), w0, v0, 0.1, 0.9)
+    got_w = np.full(E, np.nan, f32)
+    got_v = np.full(E, np.nan, f32)
+    gd = None
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    for r in range(G):
+        hub = _hub(sizes, N, num_owners=G, owner_rank=r, owner_policy=policy)
+        hub.load_state(w0, v0)
+        if gd is None:
+            gd = device_grads(hub, N, 2)
+        run_round(hub, gd)
+        w, v, _ = hub.read_state()
+        tab = hub.chunk_table()
+        for k, off, ln, own in zip(tab["key_id"], tab["offset"], tab["length"], tab["owner"]):
+            if own == r:
+                a = int(starts[k] + off)
+                got_w[a:a + int(ln)] = w[a:a + int(ln)]
+                got_v[a:a + int(ln)] = v[a:a + int(ln)]
+        hub.close()
+    assert_bits_equal(got_w, rw, f"w' union over {G} owners ({policy})")
+    assert_bits_equal(got_v, rv, f"v' union over {G} owners ({policy})")
+
+
+def test_chunk_table_matches_oracle():
+    for name in ("tiny", "resnet269"):
+        m = manifest(name)
+        for G, pol in ((1, "contig"), (4, "lpt"), (8, "contig")):
+            hub = _hub(m, 2, num_owners=G, owner_rank=G - 1, owner_policy=pol)
+            t = hub.chunk_table()
+            ref = oracle.chunk_plan(m)
+            own = np.zeros(len(ref["length"]), np.int32) if G == 1 else \
+                (oracle.owners_lpt if pol == "lpt" else oracle.owners_contig)(ref["length"], G)
+            assert oracle.canonical_text(t, t["owner"]) == oracle.canonical_text(ref, own)
+            hub.close()
+
+
+# ------------------------------ full BASELINE sizes, sampled outputs
+def _sample_indices(sizes, chunk_bytes, rng, n_random=20000):
+    E = sum(sizes)
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    ce = chunk_bytes // 4
+    pts = [rng.integers(0, E, n_random)]
+    pts.append(starts[:-1])                                  # key starts
+    pts.append(starts[1:] - 1)                               # key ends
+    for k in range(len(sizes)):                              # chunk boundaries
+        b = np.arange(starts[k], starts[k + 1], ce)
+        pts.append(b[:64])
+        pts.append(np.maximum(b[:64] - 1, starts[k]))
+    return np.unique(np.concatenate(pts)).astype(np.int64)
+
+
+@pytest.mark.parametrize("name,N,cb", [
+    ("resnet50", 8, 32768), ("alexnet", 8, 32768), ("vgg19", 8, 32768),
+    ("resnet269", 8, 32768), ("resnet269", 8, 4096), ("resnet269", 8, 1 << 20),
+])
+def test_full_size_sampled(name, N, cb):
+    from workloads.generate import values_torch
+    sizes = manifest(name)
+    hub = _hub(sizes, N, chunk_size_bytes=cb)                # bench launch config (AUTO)
+    E = hub.E
+    idx_pad = _pad_index(hub)
+    w0 = values_torch(1, 0, E, 20, DEV)
+    v0 = values_torch(2, 0, E, 25, DEV)
+    hub.load_state(w0, v0)
+    del w0, v0
+    gd = []
+    for w in range(N):
+        b = torch.full((hub.E_padded,), float("nan"), device=DEV)
+        b[idx_pad] = values_torch(grad_stream(w), 0, E, 25, DEV)
+        gd.append(b)
+    run_round(hub, gd)
+    del gd
+    rng = np.random.default_rng(len(sizes) * 7919 + cb)
+    samp = _sample_indices(sizes, cb, rng)
+    w_all, v_all, _ = hub.read_state()
+    # oracle on independently generated inputs at the sampled elements
+    g = np.stack([values_at_np(grad_stream(w), samp, 25) for w in range(N)])
+    rw, rv, _ = oracle.elems(g, values_at_np(1, samp, 20), values_at_np(2, samp, 25), 0.1, 0.9)
+    assert_bits_equal(w_all[samp], rw, f"{name}@{cb} sampled w'")
+    assert_bits_equal(v_all[samp], rv, f"{name}@{cb} sampled v'")
+    hub.close()
