@@ -68,6 +68,7 @@ typedef enum {
 } phub_status;
 
 #define PHUB_ALL_KEYS (-1)            /* whole-model push/pull in the padded layout        */
+#define PHUB_OWNED_RANGE (-2)         /* push of exactly this context's owned padded range  */
 
 enum { PHUB_COPY = 0, PHUB_BORROW = 1 };           /* ownership mode of a pushed buffer   */
 enum { PHUB_OWNER_LPT = 0, PHUB_OWNER_CONTIG = 1 };  /* chunk -> owner policy    */
@@ -118,6 +119,9 @@ phub_status phub_destroy(phub_ctx ctx);
  *   key == PHUB_ALL_KEYS: `grad` holds n == E_padded elements in the padded
  *     layout (keys at phub_layout offsets).  Only this context's owned chunks
  *     are read.
+ *   key == PHUB_OWNED_RANGE (CONTIG ownership or G == 1): `grad` holds
+ *     n == end - begin elements, the padded range phub_owner_range() gives
+ *     for this context's rank -- what an owner receives from a remote worker.
  *   key in [0, num_keys): `grad` holds n == n_k contiguous elements.
  *   mode PHUB_BORROW: zero copy -- the pointer is recorded and read by
  *     the next phub_aggregate_optimize.  `grad` must be device memory
@@ -170,6 +174,13 @@ phub_status phub_layout(phub_ctx ctx, uint64_t* E, uint64_t* E_padded, uint64_t*
 phub_status phub_plan_chunks(const uint64_t* key_num_elements, int32_t num_keys,
                              uint64_t chunk_size_bytes, int32_t num_owners, int32_t owner_policy,
                              phub_chunk* out, uint64_t cap, uint64_t* count);
+
+/* Host-only layout planning (no device): E_padded, key_offsets[num_keys]
+ * (may be NULL) and the CONTIG owner ranges owner_begin/end[num_owners] (may
+ * be NULL) exactly as phub_init / phub_owner_range would give them. */
+phub_status phub_plan_ranges(const uint64_t* key_num_elements, int32_t num_keys,
+                             uint64_t chunk_size_bytes, int32_t num_owners, uint64_t* E_padded,
+                             uint64_t* key_offsets, uint64_t* owner_begin, uint64_t* owner_end);
 
 /* Chunk table (S:125 order: vkey_id, key_id, offset, length, owner). */
 phub_status phub_num_chunks(phub_ctx ctx, uint64_t* n);

@@ -24,6 +24,7 @@ STATUS_NAMES = [
 for _i, _n in enumerate(STATUS_NAMES):
     globals()[_n] = _i
 PHUB_ALL_KEYS = -1
+PHUB_OWNED_RANGE = -2
 PHUB_COPY, PHUB_BORROW = 0, 1
 PHUB_OWNER_LPT, PHUB_OWNER_CONTIG = 0, 1
 PHUB_OPT_KERNEL, PHUB_OPT_GRID, PHUB_OPT_TILE_ELEMS, PHUB_OPT_CACHE = 1, 2, 3, 4
@@ -75,6 +76,8 @@ _SIGS = {
     "phub_chunk_table": (C.c_int, [phub_ctx, C.POINTER(phub_chunk), C.c_uint64]),
     "phub_plan_chunks": (C.c_int, [_u64p, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
                                    C.POINTER(phub_chunk), C.c_uint64, _u64p]),
+    "phub_plan_ranges": (C.c_int, [_u64p, C.c_int32, C.c_uint64, C.c_int32, _u64p, _u64p, _u64p,
+                                   _u64p]),
     "phub_owner_range": (C.c_int, [phub_ctx, C.c_int32, _u64p, _u64p]),
     "phub_owned_elements": (C.c_int, [phub_ctx, _u64p]),
     "phub_load_state": (C.c_int, [phub_ctx, C.c_void_p, C.c_void_p]),
@@ -187,6 +190,19 @@ def phub_plan_chunks(key_sizes, chunk_size_bytes: int, num_owners: int, owner_po
     _check(_lib.phub_plan_chunks(n, len(key_sizes), chunk_size_bytes, num_owners, owner_policy,
                                  arr, cnt.value, C.byref(cnt)), "phub_plan_chunks", None)
     return arr, int(cnt.value)
+
+
+def phub_plan_ranges(key_sizes, chunk_size_bytes: int, num_owners: int):
+    """Host-only: (E_padded, key_offsets, [(begin, end) per owner]) under CONTIG."""
+    K = len(key_sizes)
+    n = (C.c_uint64 * max(K, 1))(*[int(x) for x in key_sizes])
+    Ep = C.c_uint64()
+    offs = (C.c_uint64 * max(K, 1))()
+    b = (C.c_uint64 * num_owners)()
+    e = (C.c_uint64 * num_owners)()
+    _check(_lib.phub_plan_ranges(n, K, chunk_size_bytes, num_owners, C.byref(Ep), offs, b, e),
+           "phub_plan_ranges", None)
+    return int(Ep.value), list(offs)[:K], list(zip(list(b), list(e)))
 
 
 def phub_owner_range(ctx, owner: int):

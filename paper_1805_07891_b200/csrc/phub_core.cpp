@@ -167,6 +167,20 @@ static std::vector<phub_chunk> plan_chunks(const std::vector<uint64_t>& n, uint6
     return chunks;
 }
 
+// Padded key-major layout: every key starts on a 128-B boundary.
+static void layout_keys(phub_ctx c) {
+    c->key_off.resize(c->K);
+    uint64_t off = 0;
+    c->E = 0;
+    for (int k = 0; k < c->K; ++k) {
+        off = (off + kKeyAlign - 1) / kKeyAlign * kKeyAlign;
+        c->key_off[k] = off;
+        off += c->n[k];
+        c->E += c->n[k];
+    }
+    c->E_pad = (off + kKeyAlign - 1) / kKeyAlign * kKeyAlign;
+}
+
 static uint64_t chunk_dev_off(phub_ctx c, const phub_chunk& ch) {
     return c->key_off[ch.key_id] + ch.offset;
 }
@@ -294,16 +308,7 @@ phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
     c->keep_agg = cfg->keep_aggregate != 0;
     c->n.assign(cfg->key_num_elements, cfg->key_num_elements + c->K);
 
-    // padded key-major layout: every key starts on a 128-B boundary
-    c->key_off.resize(c->K);
-    uint64_t off = 0;
-    for (int k = 0; k < c->K; ++k) {
-        off = (off + kKeyAlign - 1) / kKeyAlign * kKeyAlign;
-        c->key_off[k] = off;
-        off += c->n[k];
-        c->E += c->n[k];
-    }
-    c->E_pad = (off + kKeyAlign - 1) / kKeyAlign * kKeyAlign;
+    layout_keys(c);
     if (cfg->init_weights && cfg->init_num_elements != c->E) {
         delete c;
         why = "init_num_elements != E (S:163)";
@@ -397,6 +402,36 @@ phub_status phub_plan_chunks(const uint64_t* key_num_elements, int32_t num_keys,
     return PHUB_OK;
 }
 
+phub_status phub_plan_ranges(const uint64_t* key_num_elements, int32_t num_keys,
+                             uint64_t chunk_size_bytes, int32_t num_owners, uint64_t* E_padded,
+                             uint64_t* key_offsets, uint64_t* owner_begin, uint64_t* owner_end) {
+    std::string& why = g_init_err;
+    why.clear();
+    phub_config cfg;
+    phub_config_default(&cfg);
+    cfg.key_num_elements = key_num_elements;
+    cfg.num_keys = num_keys;
+    cfg.chunk_size_bytes = chunk_size_bytes;
+    cfg.num_owners = num_owners;
+    phub_status st = validate_config(&cfg, why);
+    if (st != PHUB_OK) return st;
+    // a host-only context: layout + table + ranges, no device state
+    phub_ctx_s c;
+    c.K = num_keys;
+    c.G = num_owners;
+    c.policy = PHUB_OWNER_CONTIG;
+    c.ce = (chunk_size_bytes ? chunk_size_bytes : kDefaultChunkBytes) / 4;
+    c.n.assign(key_num_elements, key_num_elements + num_keys);
+    layout_keys(&c);
+    c.chunks = plan_chunks(c.n, c.ce, c.G, c.policy);
+    build_ranges(&c);
+    if (E_padded) *E_padded = c.E_pad;
+    if (key_offsets) std::copy(c.key_off.begin(), c.key_off.end(), key_offsets);
+    if (owner_begin) std::copy(c.own_begin.begin(), c.own_begin.end(), owner_begin);
+    if (owner_end) std::copy(c.own_end.begin(), c.own_end.end(), owner_end);
+    return PHUB_OK;
+}
+
 phub_status phub_destroy(phub_ctx ctx) {
     if (!ctx) return PHUB_ERR_INVALID_ARGUMENT;
     free_ctx(ctx);
@@ -418,10 +453,15 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
     if (c->failed) return PHUB_ERR_CUDA;
     if (worker < 0 || worker >= c->N)
         return c->fail(PHUB_ERR_BAD_WORKER, "worker %d not in [0,%d) (S:170)", worker, c->N);
-    const bool all = key == PHUB_ALL_KEYS;
+    const bool ranged = key == PHUB_OWNED_RANGE;
+    const bool all = key == PHUB_ALL_KEYS || ranged;
     if (!all && (key < 0 || key >= c->K))
-        return c->fail(PHUB_ERR_BAD_KEY, "key %d not in [0,%d) and not PHUB_ALL_KEYS", key, c->K);
-    const uint64_t want = all ? c->E_pad : c->n[key];
+        return c->fail(PHUB_ERR_BAD_KEY, "key %d not in [0,%d), PHUB_ALL_KEYS or PHUB_OWNED_RANGE",
+                       key, c->K);
+    if (ranged && !contig_mode(c))
+        return c->fail(PHUB_ERR_UNSUPPORTED, "PHUB_OWNED_RANGE needs CONTIG ownership");
+    const uint64_t rb = ranged ? c->own_begin[c->rank] : 0;
+    const uint64_t want = ranged ? c->own_end[c->rank] - rb : (all ? c->E_pad : c->n[key]);
     if (n != want)
         return c->fail(PHUB_ERR_LENGTH_MISMATCH, "push length %llu != %llu (S:172)",
                        (unsigned long long)n, (unsigned long long)want);
@@ -440,10 +480,12 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW needs device memory");
         if (reinterpret_cast<uintptr_t>(grad) % 16 != 0)
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW pointer must be 16-B aligned");
+        // base + 4*dev_off is the byte address of padded element dev_off
         for (int k = k0; k < k1; ++k)
             c->base[(size_t)worker * c->K + k] =
-                all ? reinterpret_cast<uintptr_t>(grad)
-                    : reinterpret_cast<uintptr_t>(grad) - 4 * c->key_off[k];
+                ranged ? reinterpret_cast<uintptr_t>(grad) - 4 * rb
+                : all  ? reinterpret_cast<uintptr_t>(grad)
+                       : reinterpret_cast<uintptr_t>(grad) - 4 * c->key_off[k];
     } else {
         if (!c->d_recv) {
             cudaError_t e = cudaMalloc(&c->d_recv, sizeof(float) * c->E_pad * c->N);
@@ -457,7 +499,9 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
         }
         float* slot = c->d_recv + (uint64_t)worker * c->E_pad;
         cudaError_t e = cudaSuccess;
-        if (all) {
+        if (ranged) {
+            if (n) e = cudaMemcpyAsync(slot + rb, grad, n * sizeof(float), cudaMemcpyDefault, s);
+        } else if (all) {
             uint64_t b = 0, eend = c->E_pad;
             if (contig_mode(c)) {
                 b = c->own_begin[c->rank];

@@ -1,5 +1,174 @@
-"""Multi-GPU (one process per GPU) sharded exchange -- see bench_main."""
+"""Chunks sharded by owner over the GPUs of one box (PAPER.md P:708-717,
+P:743 "micro-shards inside a box").
+
+One process per GPU.  Rank r owns the CONTIG chunk range [b_r, e_r) of the
+padded layout (chunk granular, reading R10) and hosts workers
+[r*N/G, (r+1)*N/G) -- contiguous blocks, so rank order is worker order.
+
+A round (mode M3) is:
+  push   every hosted worker's slice [b_o, e_o) goes to owner o: one NCCL group
+         of send/recv (a reduce-scatter by transport, not ncclReduceScatter, so
+         the owner still sums in worker-id order, reading R3);
+  agg    the owner's fused sm_100a kernel over its range (libphub);
+  pull   the owners' updated ranges are exchanged in one NCCL group
+         (all-gather-v) straight into every rank's weight replica.
+
+torch.distributed is plumbing only (device memory, streams, the NCCL group);
+the exchange schedule below is device-agnostic so the host logic runs under
+gloo on CPU in the tests.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import capi
 
 
-def bench_main(*a, **k):  # pragma: no cover
-    raise NotImplementedError("multi-GPU bench arrives in the next milestone")
+@dataclass
+class ExchangePlan:
+    """Who sends which padded slice to whom (pure host logic)."""
+    rank: int
+    world: int
+    num_workers: int
+    E_padded: int
+    ranges: list            # [(begin, end)] per owner, abutting, covering [0, E_padded)
+
+    @classmethod
+    def build(cls, key_sizes, num_workers, chunk_size_bytes, rank, world):
+        if num_workers % world != 0:
+            raise ValueError(f"{num_workers} workers cannot be hosted evenly on {world} ranks")
+        Ep, _offs, ranges = capi.phub_plan_ranges(key_sizes, chunk_size_bytes, world)
+        return cls(rank, world, num_workers, Ep, ranges)
+
+    @property
+    def per_rank(self):
+        return self.num_workers // self.world
+
+    def host_of(self, worker):
+        return worker // self.per_rank
+
+    def hosted(self, rank=None):
+        r = self.rank if rank is None else rank
+        return list(range(r * self.per_rank, (r + 1) * self.per_rank))
+
+    def owned(self, rank=None):
+        return self.ranges[self.rank if rank is None else rank]
+
+    def nvlink_bytes_out(self):
+        """Bytes this rank sends per round (push slices + pulled range copies)."""
+        b, e = self.owned()
+        push = sum(4 * (oe - ob) for o, (ob, oe) in enumerate(self.ranges) if o != self.rank) \
+            * self.per_rank
+        pull = 4 * (e - b) * (self.world - 1)
+        return push + pull
+
+    def nvlink_bytes_in(self):
+        b, e = self.owned()
+        push = 4 * (e - b) * (self.num_workers - self.per_rank)
+        pull = sum(4 * (oe - ob) for o, (ob, oe) in enumerate(self.ranges) if o != self.rank)
+        return push + pull
+
+
+def push_exchange(plan: ExchangePlan, grads: dict, recv: dict, group=None):
+    """Send hosted workers' owner slices; receive remote workers' slices of the
+    owned range into recv[w] (length e_r - b_r).  Returns after the receives
+    are ordered before later work on the current stream."""
+    import torch.distributed as dist
+    ops = []
+    for w in plan.hosted():
+        for o, (b, e) in enumerate(plan.ranges):
+            if o != plan.rank and e > b:
+                ops.append(dist.P2POp(dist.isend, grads[w][b:e], o, group))
+    b, e = plan.owned()
+    if e > b:
+        for w in range(plan.num_workers):
+            if plan.host_of(w) != plan.rank:
+                ops.append(dist.P2POp(dist.irecv, recv[w], plan.host_of(w), group))
+    if ops:
+        for work in dist.batch_isend_irecv(ops):
+            work.wait()
+
+
+def pull_exchange(plan: ExchangePlan, replica, group=None):
+    """All-gather-v of the owners' updated ranges into every rank's replica."""
+    import torch.distributed as dist
+    ops = []
+    b, e = plan.owned()
+    for p in range(plan.world):
+        if p == plan.rank:
+            continue
+        if e > b:
+            ops.append(dist.P2POp(dist.isend, replica[b:e], p, group))
+        pb, pe = plan.ranges[p]
+        if pe > pb:
+            ops.append(dist.P2POp(dist.irecv, replica[pb:pe], p, group))
+    if ops:
+        for work in dist.batch_isend_irecv(ops):
+            work.wait()
+
+
+class ShardedPHub:
+    """The sharded parameter exchange on this rank's GPU (public multi-GPU API).
+
+        sh = ShardedPHub(key_sizes, num_workers=8)        # after init_process_group("nccl")
+        sh.exchange({w: grad_w for w in sh.hosted})        # push -> aggregate -> pull
+        sh.weights()                                       # full updated replica (padded)
+    """
+
+    def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
+                 rescale=0.0, device=None, group=None):
+        import torch
+        import torch.distributed as dist
+        from .phub import PHub
+        self.group = group
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, rank, world)
+        self.hub = PHub(key_sizes, num_workers, chunk_size_bytes=chunk_size_bytes, lr=lr,
+                        momentum=momentum, rescale=rescale, device=self.device,
+                        num_owners=world, owner_rank=rank, owner_policy="contig")
+        assert self.hub.E_padded == self.plan.E_padded
+        assert tuple(self.hub.owner_range()) == tuple(self.plan.owned())
+        b, e = self.plan.owned()
+        self.recv = {w: torch.empty(e - b, dtype=torch.float32, device=self.device)
+                     for w in range(num_workers) if self.plan.host_of(w) != rank}
+        self.replica = self.hub.weights()
+
+    @property
+    def hosted(self):
+        return self.plan.hosted()
+
+    def push(self, grads: dict):
+        push_exchange(self.plan, grads, self.recv, self.group)
+        for w in range(self.plan.num_workers):
+            if self.plan.host_of(w) == self.plan.rank:
+                self.hub.push(w, grads[w], key=capi.PHUB_ALL_KEYS)       # own slice, zero copy
+            else:
+                self.hub.push(w, self.recv[w], key=capi.PHUB_OWNED_RANGE)
+
+    def aggregate_optimize(self):
+        self.hub.aggregate_optimize()
+
+    def pull(self):
+        pull_exchange(self.plan, self.replica, self.group)
+
+    def exchange(self, grads: dict):
+        self.push(grads)
+        self.aggregate_optimize()
+        self.pull()
+
+    def exchange_host(self, host_grads: dict, dev_grads: dict, host_out: dict):
+        """End-to-end round from host memory: H2D copy of each hosted worker's
+        gradient (pinned host -> device staging), the exchange, and a D2H copy
+        of the updated replica for each hosted worker."""
+        for w in self.hosted:
+            dev_grads[w].copy_(host_grads[w], non_blocking=True)
+        self.exchange(dev_grads)
+        for w in self.hosted:
+            host_out[w].copy_(self.replica, non_blocking=True)
+
+    def weights(self):
+        return self.replica
+
+    def close(self):
+        self.hub.close()

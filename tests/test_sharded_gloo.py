@@ -1,0 +1,47 @@
+"""Multi-process (gloo, CPU) tests of the sharded exchange's host logic."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+WORKER = os.path.join(ROOT, "tests", "dist", "gloo_exchange_worker.py")
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world,name,N,cb", [
+    (2, "small", 4, 32768), (2, "tiny", 4, 4096), (4, "tiny", 8, 32768), (2, "small", 2, 64),
+])
+def test_gloo_exchange(world, name, N, cb):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", WORKER, name, str(N), str(cb)]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count(" ok: ") == world
+
+
+def test_plan_bytes_and_hosting():
+    from paper_1805_07891_b200.sharded import ExchangePlan
+    from workloads import manifest
+    m = manifest("vgg19")
+    E = sum(m)
+    for G in (2, 4, 8):
+        plans = [ExchangePlan.build(m, 8, 32768, r, G) for r in range(G)]
+        assert sorted(w for p in plans for w in p.hosted()) == list(range(8))
+        assert all(p.host_of(w) == p.rank for p in plans for w in p.hosted())
+        tot_out = sum(p.nvlink_bytes_out() for p in plans)
+        tot_in = sum(p.nvlink_bytes_in() for p in plans)
+        assert tot_out == tot_in
+        # per-GPU bytes out = 32E(G-1)/G^2 + 4E(G-1)/G (+ padding)
+        expect = 32 * E * (G - 1) / G ** 2 + 4 * E * (G - 1) / G
+        assert abs(max(p.nvlink_bytes_out() for p in plans) / expect - 1) < 2e-3
