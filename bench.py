@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
+    ap.add_argument("--mode", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 exchange: fused peer-memory kernel (p2p) or NCCL send/recv")
     return ap.parse_args()
 
 
@@ -237,10 +239,13 @@ NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction 
 
 
 def bench_multi(args, mname, N, cb):
-    """M3: 8 workers hosted N/G per GPU, chunks sharded by owner, NCCL push/pull."""
+    """M3: 8 workers hosted N/G per GPU, chunks sharded by owner.
+    mode p2p : one fused kernel per owner reads peers' gradients and writes peers'
+               replicas over NVLink (stream-ordered NCCL barrier before/after);
+    mode nccl: NCCL grouped send/recv push, fused kernel, NCCL all-gather-v pull."""
     import torch
     import torch.distributed as dist
-    from paper_1805_07891_b200.sharded import ShardedPHub
+    from paper_1805_07891_b200.sharded import P2PShardedPHub, ShardedPHub
     from workloads import grad_stream, manifest
     from workloads.generate import values_torch
 
@@ -250,38 +255,52 @@ def bench_multi(args, mname, N, cb):
     dist.init_process_group("nccl", device_id=dev)
     rank, G = dist.get_rank(), dist.get_world_size()
     sizes = manifest(mname)
-    sh = ShardedPHub(sizes, N, chunk_size_bytes=cb, device=local)
+    p2p = args.mode == "p2p"
+    sh = (P2PShardedPHub if p2p else ShardedPHub)(sizes, N, chunk_size_bytes=cb, device=local)
     hub, plan = sh.hub, sh.plan
     E, Ep = hub.E, hub.E_padded
     idx = torch.as_tensor(hub.padded_index(), device=dev)
     hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
-    grads = {}
+    grads = sh.gradients() if p2p else {}
     for w in sh.hosted:
-        b = torch.zeros(Ep, dtype=torch.float32, device=dev)
+        b = grads[w] if p2p else torch.zeros(Ep, dtype=torch.float32, device=dev)
         b[idx] = values_torch(grad_stream(w), 0, E, 25, dev)
         grads[w] = b
     del idx
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
+
+    def one(i=None):
+        if p2p:
+            sh.barrier()
+            sh.push()
+        else:
+            sh.push(grads)
+        if i is not None:
+            ev[i][0].record(stream)
+        hub.aggregate_optimize()
+        if i is not None:
+            ev[i][1].record(stream)
+        if p2p:
+            sh.barrier()
+        else:
+            sh.pull()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
     for _ in range(args.warmup):
-        sh.exchange(grads)
+        one()
     torch.cuda.synchronize()
     dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
     k0 = hub.kernel_launches
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     dist.barrier()
     t0.record(stream)
     for i in range(args.steps):
-        sh.push(grads)
-        ev[i][0].record(stream)
-        sh.aggregate_optimize()
-        ev[i][1].record(stream)
-        sh.pull()
+        one(i)
     t1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -300,13 +319,20 @@ def bench_multi(args, mname, N, cb):
         for w in sh.hosted:
             host_g[w].copy_(grads[w])
         host_o = {w: torch.empty(Ep, dtype=torch.float32, pin_memory=True) for w in sh.hosted}
-        sh.exchange_host(host_g, grads, host_o)
+
+        def e2e_step():
+            if p2p:
+                sh.exchange_host(host_g, host_o)
+            else:
+                sh.exchange_host(host_g, grads, host_o)
+
+        e2e_step()
         torch.cuda.synchronize()
         dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.e2e_steps):
-            sh.exchange_host(host_g, grads, host_o)
+            e2e_step()
         b.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / args.e2e_steps], device=dev)
@@ -315,8 +341,8 @@ def bench_multi(args, mname, N, cb):
         e2e = {"value": round(N * 4 * E / te / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": N * 4 * Ep, "d2h_bytes_per_step": N * 4 * Ep,
                "steps": args.e2e_steps, "ms_per_step": round(te * 1e3, 3),
-               "path": "ShardedPHub.exchange_host: H2D of hosted grads -> NCCL push -> "
-                       "phub_aggregate_optimize -> NCCL all-gather-v -> D2H per hosted worker"}
+               "path": f"{type(sh).__name__}.exchange_host: H2D of hosted grads -> exchange "
+                       f"({args.mode}) -> D2H of the replica per hosted worker"}
     if rank == 0:
         ms_step = max(r["ms"] for r in allr)
         k_ms = max(r["k_ms"] for r in allr)
@@ -337,17 +363,30 @@ def bench_multi(args, mname, N, cb):
             "exchanges_per_s": round(N / t_step, 1),
             "config": {"workload": args.config, "keys": len(sizes), "E": E, "E_padded": Ep,
                        "workers": N, "workers_per_gpu": N // G, "chunk_bytes": cb,
-                       "mode": "M3 (full exchange: NCCL grouped send/recv push, fused kernel "
-                               "on owner range, NCCL all-gather-v pull)",
+                       "mode": ("M3 (full exchange) p2p: one fused kernel per owner reads peer "
+                                "gradients + writes peer replicas over NVLink, NCCL barrier "
+                                "before/after") if p2p else
+                               ("M3 (full exchange) nccl: NCCL grouped send/recv push, fused "
+                                "kernel on owner range, NCCL all-gather-v pull"),
                        "parallelism": f"owner-sharded x{G}",
                        "l2": "no flush: inputs exceed L2"},
-            "owner_phase": {"mode": "M2 (kernel only, max over ranks)", "kernel_ms": round(k_ms, 4),
-                            "value": round(N * 4 * E / (k_ms / 1e3) / 1e9, 1), "unit": "GB/s"},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": ncu_traffic(args.config, "flat"),
-                         "kernel": "phub_agg_nag (k_flat) on the slowest owner",
-                         "kernel_ms": round(slow["k_ms"], 4), "peak_source": peak_src},
+            "owner_phase": None if p2p else {
+                "mode": "M2 (kernel only, max over ranks)", "kernel_ms": round(k_ms, 4),
+                "value": round(N * 4 * E / (k_ms / 1e3) / 1e9, 1), "unit": "GB/s"},
+            "roofline": ({"bound": "nvlink", "achieved": round(nv_bytes / (k_ms / 1e3) / 1e9, 1),
+                          "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                          "frac": round(nv_bytes / (k_ms / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
+                          "traffic": None,
+                          "kernel": "fused exchange kernel (k_flat with peer loads/stores), "
+                                    "slowest owner", "kernel_ms": round(k_ms, 4),
+                          "bytes_per_launch_max_dir": nv_bytes,
+                          "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per "
+                                         "direction"} if p2p else
+                         {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                          "unit": "GB/s", "frac": round(achieved / peak, 4),
+                          "traffic": ncu_traffic(args.config, "flat"),
+                          "kernel": "phub_agg_nag (k_flat) on the slowest owner",
+                          "kernel_ms": round(slow["k_ms"], 4), "peak_source": peak_src}),
             "roofline_nvlink": {"bound": "nvlink", "achieved": round(nv_ach, 1),
                                 "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                                 "frac": round(nv_ach / NVLINK_PEER_GBS, 4),

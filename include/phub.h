@@ -207,6 +207,39 @@ phub_status phub_read_state(phub_ctx ctx, float* w, float* v, float* agg);
 phub_status phub_iteration(phub_ctx ctx, uint64_t* iteration);
 phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
 
+/* ---------------------------------------------------------------------------
+ * Peer-memory exchange (multi-GPU, one process per GPU)
+ *
+ * The owner's fused kernel can read remote workers' gradients and write the
+ * updated weights into remote replicas directly over NVLink: push a peer-mapped
+ * gradient pointer with PHUB_BORROW, and register peer-mapped replicas here.
+ * Then one kernel does aggregate + optimize + the all-gather of the pull
+ * ("transmitted back to the workers on its originating path").
+ * The caller orders rounds across GPUs (e.g. a stream-ordered barrier before
+ * and after phub_aggregate_optimize); the library never spins on peers.
+ * ------------------------------------------------------------------------- */
+
+/* Every later phub_aggregate_optimize also stores w' of the owned range into
+ * replicas[0..count) (padded layout, E_padded elements each; device pointers,
+ * typically peer-mapped with phub_ipc_open).  count == 0 clears.  count <= 16.
+ * Requires CONTIG ownership (or G == 1) and the flat kernel (whole-model or
+ * owned-range pushes, 32-B aligned chunk layout), else PHUB_ERR_UNSUPPORTED
+ * at aggregate time. */
+phub_status phub_set_replicas(phub_ctx ctx, float* const* replicas, int32_t count);
+
+/* Shared device allocations that can be exported to peer processes.
+ * phub_alloc_shared: cudaMalloc of `bytes` on `device` (whole allocation, so an
+ * IPC handle maps exactly this buffer).  phub_free_shared releases it. */
+phub_status phub_alloc_shared(int32_t device, uint64_t bytes, void** dev_ptr);
+phub_status phub_free_shared(int32_t device, void* dev_ptr);
+
+/* CUDA IPC: export a phub_alloc_shared pointer (or phub_weights) as a 64-byte
+ * handle; open a peer's handle on `device` (peer access enabled lazily);
+ * close an opened mapping. */
+phub_status phub_ipc_get_handle(int32_t device, const void* dev_ptr, void* handle64);
+phub_status phub_ipc_open(int32_t device, const void* handle64, void** dev_ptr);
+phub_status phub_ipc_close(int32_t device, void* dev_ptr);
+
 /* Options (ablations / tuning).  Values are validated; PHUB_ERR_UNSUPPORTED
  * when a forced variant cannot run this context's layout. */
 enum {

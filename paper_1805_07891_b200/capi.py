@@ -85,6 +85,12 @@ _SIGS = {
     "phub_iteration": (C.c_int, [phub_ctx, _u64p]),
     "phub_kernel_launches": (C.c_int, [phub_ctx, _u64p]),
     "phub_set_option": (C.c_int, [phub_ctx, C.c_int32, C.c_int64]),
+    "phub_set_replicas": (C.c_int, [phub_ctx, C.POINTER(C.c_void_p), C.c_int32]),
+    "phub_alloc_shared": (C.c_int, [C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "phub_free_shared": (C.c_int, [C.c_int32, C.c_void_p]),
+    "phub_ipc_get_handle": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p]),
+    "phub_ipc_open": (C.c_int, [C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "phub_ipc_close": (C.c_int, [C.c_int32, C.c_void_p]),
     "phub_status_string": (C.c_char_p, [C.c_int]),
     "phub_last_error": (C.c_char_p, [phub_ctx]),
 }
@@ -239,6 +245,38 @@ def phub_kernel_launches(ctx) -> int:
 
 def phub_set_option(ctx, option: int, value: int):
     _check(_lib.phub_set_option(ctx, option, value), "phub_set_option", ctx)
+
+
+def phub_set_replicas(ctx, ptrs):
+    arr = (C.c_void_p * max(len(ptrs), 1))(*ptrs)
+    _check(_lib.phub_set_replicas(ctx, arr, len(ptrs)), "phub_set_replicas", ctx)
+
+
+def phub_alloc_shared(device: int, nbytes: int) -> int:
+    p = C.c_void_p()
+    _check(_lib.phub_alloc_shared(device, nbytes, C.byref(p)), "phub_alloc_shared", None)
+    return int(p.value)
+
+
+def phub_free_shared(device: int, ptr: int):
+    _check(_lib.phub_free_shared(device, ptr), "phub_free_shared", None)
+
+
+def phub_ipc_get_handle(device: int, ptr: int) -> bytes:
+    buf = C.create_string_buffer(64)
+    _check(_lib.phub_ipc_get_handle(device, ptr, buf), "phub_ipc_get_handle", None)
+    return buf.raw
+
+
+def phub_ipc_open(device: int, handle: bytes) -> int:
+    p = C.c_void_p()
+    buf = C.create_string_buffer(bytes(handle), 64)
+    _check(_lib.phub_ipc_open(device, buf, C.byref(p)), "phub_ipc_open", None)
+    return int(p.value)
+
+
+def phub_ipc_close(device: int, ptr: int):
+    _check(_lib.phub_ipc_close(device, ptr), "phub_ipc_close", None)
 
 
 def phub_status_string(st: int) -> str:

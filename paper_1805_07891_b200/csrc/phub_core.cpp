@@ -75,6 +75,7 @@ struct phub_ctx_s {
     std::vector<uintptr_t> base;      // N x K: base + 4*dev_off = byte address
     std::vector<uintptr_t> base_uploaded;
     uintptr_t* d_base = nullptr;
+    std::vector<float*> replicas;     // peer weight replicas written by the kernel
 
     // options + counters
     int kernel = PHUB_KERNEL_AUTO;
@@ -552,6 +553,9 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
         ((variant == PHUB_KERNEL_FLAT128 || variant == PHUB_KERNEL_WIDE) && !flat))
         return c->fail(PHUB_ERR_UNSUPPORTED, "forced kernel variant %d needs whole-model pushes, "
                        "contiguous ownership and aligned chunks", variant);
+    if (!c->replicas.empty() && variant != PHUB_KERNEL_FLAT && variant != PHUB_KERNEL_FLAT128)
+        return c->fail(PHUB_ERR_UNSUPPORTED, "replica stores need the flat kernel (whole-model "
+                       "or owned-range pushes under CONTIG ownership)");
     if (variant == PHUB_KERNEL_WIDE && !c->keep_agg)
         return c->fail(PHUB_ERR_UNSUPPORTED, "wide ablation needs keep_aggregate (merge buffer)");
 
@@ -571,6 +575,8 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
         a.mu = c->mu;
         a.rescale = c->rescale;
         a.nw = c->N;
+        a.nrep = (int)c->replicas.size();
+        for (int r = 0; r < a.nrep; ++r) a.rep[r] = c->replicas[r];
         const int vec = variant == PHUB_KERNEL_FLAT ? 8 : 4;
         const uint64_t nvec = (eend - b) / vec;
         int grid = c->grid_override ? c->grid_override : c->flat_grid[vec == 8][c->keep_agg];
@@ -755,6 +761,90 @@ phub_status phub_iteration(phub_ctx c, uint64_t* it) {
 phub_status phub_kernel_launches(phub_ctx c, uint64_t* n) {
     if (!c || !n) return PHUB_ERR_INVALID_ARGUMENT;
     *n = c->launches_total;
+    return PHUB_OK;
+}
+
+phub_status phub_set_replicas(phub_ctx c, float* const* replicas, int32_t count) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (count < 0 || count > phub::kMaxReplicas || (count && !replicas))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "replica count must be in [0,%d]",
+                       phub::kMaxReplicas);
+    for (int r = 0; r < count; ++r) {
+        if (!replicas[r] || reinterpret_cast<uintptr_t>(replicas[r]) % 32 != 0)
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "replica %d is NULL or not 32-B aligned", r);
+        DeviceGuard g(c->device);
+        if (!is_device_ptr(replicas[r]))
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "replica %d is not device memory", r);
+    }
+    if (count && !contig_mode(c))
+        return c->fail(PHUB_ERR_UNSUPPORTED, "replicas need CONTIG ownership");
+    c->replicas.assign(replicas, replicas + count);
+    return PHUB_OK;
+}
+
+phub_status phub_alloc_shared(int32_t device, uint64_t bytes, void** dev_ptr) {
+    if (!dev_ptr || device < 0) return PHUB_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(device);
+    cudaError_t e = cudaMalloc(dev_ptr, bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        g_init_err = cudaGetErrorString(e);
+        *dev_ptr = nullptr;
+        return PHUB_ERR_OUT_OF_MEMORY;
+    }
+    return PHUB_OK;
+}
+
+phub_status phub_free_shared(int32_t device, void* dev_ptr) {
+    if (device < 0) return PHUB_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(device);
+    cudaError_t e = cudaFree(dev_ptr);
+    if (e != cudaSuccess) {
+        g_init_err = cudaGetErrorString(e);
+        return PHUB_ERR_CUDA;
+    }
+    return PHUB_OK;
+}
+
+phub_status phub_ipc_get_handle(int32_t device, const void* dev_ptr, void* handle64) {
+    if (!dev_ptr || !handle64 || device < 0) return PHUB_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        g_init_err = std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e);
+        return PHUB_ERR_CUDA;
+    }
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, sizeof h);
+    return PHUB_OK;
+}
+
+phub_status phub_ipc_open(int32_t device, const void* handle64, void** dev_ptr) {
+    if (!handle64 || !dev_ptr || device < 0) return PHUB_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        g_init_err = std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e);
+        *dev_ptr = nullptr;
+        return PHUB_ERR_CUDA;
+    }
+    return PHUB_OK;
+}
+
+phub_status phub_ipc_close(int32_t device, void* dev_ptr) {
+    if (!dev_ptr || device < 0) return PHUB_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(device);
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        g_init_err = std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e);
+        return PHUB_ERR_CUDA;
+    }
     return PHUB_OK;
 }
 

@@ -16,7 +16,10 @@
 // Kernels:
 //   k_flat   owned padded range walked as 256-bit (LDG.E.256/STG.E.256, new on
 //            sm_100a) or 128-bit vectors; persistent grid sized to
-//            SMs x resident CTAs; workers' bases in kernel params.
+//            SMs x resident CTAs; workers' bases in kernel params.  Bases may
+//            be peer-mapped (NVLink loads) and w' may also be stored into peer
+//            replicas: the push, the aggregate+optimize and the pull's
+//            all-gather fused in one kernel over peer memory.
 //   k_tiles  one CTA per chunk tile (PHub's chunk -> core mapping, P:708-713,
 //            with the hardware CTA scheduler as the "core" assigner); worker
 //            pointers per (worker, key) for per-key pushes; 128-bit body +
@@ -176,7 +179,11 @@ __global__ void __launch_bounds__(kThreads) k_flat(const __grid_constant__ FlatA
         st_w<CACHE>(w + i, wv);
         st_stream(v + i, vv);
         if constexpr (AGG) st_stream(sa + i, sv);
+        // fused pull: w' straight into every registered (peer) replica over NVLink
+        for (int r = 0; r < a.nrep; ++r)
+            reinterpret_cast<V*>(a.rep[r] + a.begin)[i] = wv;
     }
+    if (a.nrep) __threadfence_system();   // peer stores performed before the grid retires
 }
 
 // ---------------------------------------------------------- chunk tiles

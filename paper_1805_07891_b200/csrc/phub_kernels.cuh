@@ -7,6 +7,7 @@
 namespace phub {
 
 constexpr int kMaxWorkers = 64;       // flat-kernel pointer array capacity
+constexpr int kMaxReplicas = 16;      // peer weight replicas written by the flat kernel
 constexpr int kThreads = 256;         // CTA size of every hot kernel
 
 // One CTA tile of an owned chunk (chunk-tile kernel).  `off` is the element
@@ -25,6 +26,8 @@ struct FlatArgs {
     uint64_t begin, end;              // owned padded range [begin, end), elements
     float lr, mu, rescale;
     int nw;
+    int nrep;                         // extra replicas (peer-mapped) that also receive w'
+    float* rep[kMaxReplicas];
 };
 
 struct TileArgs {

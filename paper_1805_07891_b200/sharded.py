@@ -172,3 +172,103 @@ class ShardedPHub:
 
     def close(self):
         self.hub.close()
+
+
+class P2PShardedPHub:
+    """Peer-memory form of the sharded exchange: ONE kernel
+    per round on each owner reads its workers' slices straight out of the
+    peers' gradient buffers over NVLink (in worker-id order, so the sum stays
+    bit-exact), applies Nesterov, and stores w' into its own replica and into
+    every peer replica -- push, aggregate+optimize and the pull's all-gather
+    fused, no NCCL data movement.
+
+    Hosted workers write their gradients into ``gradients()[w]`` (buffers
+    allocated by libphub so they can be exported with CUDA IPC).  Rounds are
+    ordered across GPUs by a stream-ordered NCCL barrier (a 1-element
+    all-reduce) before and after the kernel; no kernel ever spins on a peer.
+    """
+
+    def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
+                 rescale=0.0, device=None, group=None):
+        import torch
+        import torch.distributed as dist
+        from .phub import PHub, _CudaArray
+        self.group = group
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, rank, world)
+        self.hub = PHub(key_sizes, num_workers, chunk_size_bytes=chunk_size_bytes, lr=lr,
+                        momentum=momentum, rescale=rescale, device=self.device,
+                        num_owners=world, owner_rank=rank, owner_policy="contig")
+        Ep = self.hub.E_padded
+        dev = self.device
+        self._own = {w: capi.phub_alloc_shared(dev, 4 * Ep) for w in self.plan.hosted()}
+        self._grads = {w: torch.as_tensor(_CudaArray(p, Ep, self), device=f"cuda:{dev}")
+                       for w, p in self._own.items()}
+        for t in self._grads.values():
+            t.zero_()
+        mine = (rank, {w: capi.phub_ipc_get_handle(dev, p) for w, p in self._own.items()},
+                capi.phub_ipc_get_handle(dev, self.hub.weights_ptr()))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self._peer_grad, self._peer_w = {}, []
+        for r, hs, wh in sorted(allh, key=lambda x: x[0]):
+            if r == rank:
+                continue
+            for w, h in hs.items():
+                self._peer_grad[w] = capi.phub_ipc_open(dev, h)
+            self._peer_w.append(capi.phub_ipc_open(dev, wh))
+        capi.phub_set_replicas(self.hub.ctx, self._peer_w)
+        self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
+        self.replica = self.hub.weights()
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+    @property
+    def hosted(self):
+        return self.plan.hosted()
+
+    def gradients(self) -> dict:
+        """Device buffers (padded layout) the hosted workers write their gradients into."""
+        return self._grads
+
+    def barrier(self):
+        import torch.distributed as dist
+        dist.all_reduce(self._flag, group=self.group)
+
+    def push(self):
+        Ep = self.hub.E_padded
+        for w in range(self.plan.num_workers):
+            ptr = self._own[w] if w in self._own else self._peer_grad[w]
+            self.hub.push(w, ptr, key=capi.PHUB_ALL_KEYS, mode="borrow", n=Ep)
+
+    def exchange(self):
+        self.barrier()                  # every rank's gradients of this round are in place
+        self.push()                     # zero-copy: local and peer-mapped pointers
+        self.hub.aggregate_optimize()   # NVLink loads + NAG + NVLink replica stores
+        self.barrier()                  # every owner's stores into this replica are done
+
+    def exchange_host(self, host_grads: dict, host_out: dict):
+        for w in self.hosted:
+            self._grads[w].copy_(host_grads[w], non_blocking=True)
+        self.exchange()
+        for w in self.hosted:
+            host_out[w].copy_(self.replica, non_blocking=True)
+
+    def weights(self):
+        return self.replica
+
+    def close(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        capi.phub_set_replicas(self.hub.ctx, [])
+        for p in list(self._peer_grad.values()) + self._peer_w:
+            capi.phub_ipc_close(self.device, p)
+        dist.barrier(group=self.group)
+        self._grads = {}
+        for p in self._own.values():
+            capi.phub_free_shared(self.device, p)
+        self._own = {}
+        self.hub.close()

@@ -1,0 +1,65 @@
+"""Multi-GPU parity worker (torchrun, NCCL): ShardedPHub vs the CPU oracle.
+
+Each rank hosts N/G workers, pushes through NCCL to the chunk owners, runs the
+fused kernel on its owned range and pulls the all-gather-v; after R rounds
+every rank's full replica must equal R oracle rounds bit for bit.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_1805_07891_b200.sharded import P2PShardedPHub, ShardedPHub  # noqa: E402
+from workloads import grad_stream, manifest, values_np  # noqa: E402
+from workloads.generate import values_torch  # noqa: E402
+
+
+def main():
+    name, N, cb, rounds = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+    mode = sys.argv[5] if len(sys.argv) > 5 else "nccl"
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    dist.init_process_group("nccl", device_id=dev)
+    rank, G = dist.get_rank(), dist.get_world_size()
+    sizes = manifest(name) if name != "small" else [3, 3, 9408, 64, 64, 4096, 20000, 1000, 7]
+    E = sum(sizes)
+    cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
+    sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
+    w_ref, v_ref = values_np(1, 0, E, 20), values_np(2, 0, E, 25)
+    sh.hub.load_state(w_ref, v_ref)
+    idx = torch.as_tensor(sh.hub.padded_index(), device=dev)
+    for r in range(rounds):
+        grads = sh.gradients() if mode == "p2p" else {}
+        for w in sh.hosted:
+            b = grads[w] if mode == "p2p" else torch.empty(sh.hub.E_padded, device=dev)
+            b.fill_(float("nan"))
+            b[idx] = values_torch(grad_stream(w) + 37 * r, 0, E, 25, dev)
+            grads[w] = b
+        if mode == "p2p":
+            sh.exchange()
+        else:
+            sh.exchange(grads)
+        hg = [values_np(grad_stream(w) + 37 * r, 0, E, 25) for w in range(N)]
+        w_ref, v_ref, _ = oracle.round_(sizes, hg, w_ref, v_ref, 0.1, 0.9, chunk_bytes=cb)
+    torch.cuda.synchronize()
+    got = sh.weights()[idx].cpu().numpy()
+    ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
+    bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    sh.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"rank {rank}/{G}: {'ok' if ok else f'MISMATCH {bad} elements'}")
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,40 @@
+"""Multi-GPU parity of the sharded NCCL exchange (-m gpu, needs >= 2 GPUs)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+WORKER = os.path.join(ROOT, "tests", "dist", "nccl_exchange_worker.py")
+
+
+def _ngpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("mode", ["nccl", "p2p"])
+@pytest.mark.parametrize("G,name,N,cb,rounds", [
+    (2, "small", 8, 32768, 2), (2, "tiny", 4, 4096, 1), (4, "resnet50", 8, 32768, 2),
+    (8, "resnet50", 8, 32768, 2), (8, "small", 8, 64, 1),
+])
+def test_sharded_exchange_bit_exact(G, name, N, cb, rounds, mode):
+    if _ngpus() < G:
+        pytest.skip(f"needs {G} GPUs, have {_ngpus()}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", WORKER, name, str(N), str(cb),
+           str(rounds), mode]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count(": ok") == G
