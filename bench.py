@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
-    ap.add_argument("--mode", default="p2p", choices=["p2p", "nccl"],
+    ap.add_argument("--mode", default="p2p", choices=["p2p", "nccl", "allreduce"],
                     help="N>1 exchange: fused peer-memory kernel (p2p) or NCCL send/recv")
     return ap.parse_args()
 
@@ -245,7 +245,7 @@ def bench_multi(args, mname, N, cb):
     mode nccl: NCCL grouped send/recv push, fused kernel, NCCL all-gather-v pull."""
     import torch
     import torch.distributed as dist
-    from paper_1805_07891_b200.sharded import P2PShardedPHub, ShardedPHub
+    from paper_1805_07891_b200.sharded import AllReduceBaseline, P2PShardedPHub, ShardedPHub
     from workloads import grad_stream, manifest
     from workloads.generate import values_torch
 
@@ -256,7 +256,9 @@ def bench_multi(args, mname, N, cb):
     rank, G = dist.get_rank(), dist.get_world_size()
     sizes = manifest(mname)
     p2p = args.mode == "p2p"
-    sh = (P2PShardedPHub if p2p else ShardedPHub)(sizes, N, chunk_size_bytes=cb, device=local)
+    ar = args.mode == "allreduce"
+    cls = {"p2p": P2PShardedPHub, "nccl": ShardedPHub, "allreduce": AllReduceBaseline}[args.mode]
+    sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
     hub, plan = sh.hub, sh.plan
     E, Ep = hub.E, hub.E_padded
     idx = torch.as_tensor(hub.padded_index(), device=dev)
@@ -271,7 +273,14 @@ def bench_multi(args, mname, N, cb):
     stream = torch.cuda.current_stream(dev)
 
     def one(i=None):
-        if p2p:
+        if ar:
+            hosted = sh.hosted
+            sh.sum.copy_(grads[hosted[0]])
+            for w in hosted[1:]:
+                sh.sum.add_(grads[w])
+            dist.all_reduce(sh.sum)
+            hub.push(0, sh.sum)
+        elif p2p:
             sh.barrier()
             sh.push()
         else:
@@ -283,7 +292,7 @@ def bench_multi(args, mname, N, cb):
             ev[i][1].record(stream)
         if p2p:
             sh.barrier()
-        else:
+        elif not ar:
             sh.pull()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -314,7 +323,7 @@ def bench_multi(args, mname, N, cb):
     dist.all_gather_object(allr, mine)
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not ar:
         host_g = {w: torch.empty(Ep, dtype=torch.float32, pin_memory=True) for w in sh.hosted}
         for w in sh.hosted:
             host_g[w].copy_(grads[w])
@@ -351,7 +360,8 @@ def bench_multi(args, mname, N, cb):
         slow = max(allr, key=lambda r: r["k_ms"])
         achieved = (4 * N + 16) * slow["owned"] / (slow["k_ms"] / 1e3) / 1e9
         peak, peak_src = measured_peaks()
-        nv_bytes = max(max(r["out"], r["in"]) for r in allr)
+        nv_bytes = max(max(r["out"], r["in"]) for r in allr) if not ar else \
+            int(2 * (G - 1) / G * 4 * Ep)              # ring all-reduce bytes per direction
         nv_ach = nv_bytes / t_step / 1e9
         reasons = sorted(set(x for r in allr for x in r["clocks"].get("reasons", [])))
         sm = [r["clocks"]["sm_mhz"] for r in allr if r["clocks"].get("sm_mhz")]
@@ -366,11 +376,14 @@ def bench_multi(args, mname, N, cb):
                        "mode": ("M3 (full exchange) p2p: one fused kernel per owner reads peer "
                                 "gradients + writes peer replicas over NVLink, NCCL barrier "
                                 "before/after") if p2p else
+                               ("BASELINE (not exact, NEXT-3): local torch sum of hosted workers, "
+                                "NCCL all-reduce, libphub NAG on the whole model on every GPU")
+                               if ar else
                                ("M3 (full exchange) nccl: NCCL grouped send/recv push, fused "
                                 "kernel on owner range, NCCL all-gather-v pull"),
                        "parallelism": f"owner-sharded x{G}",
                        "l2": "no flush: inputs exceed L2"},
-            "owner_phase": None if p2p else {
+            "owner_phase": None if (p2p or ar) else {
                 "mode": "M2 (kernel only, max over ranks)", "kernel_ms": round(k_ms, 4),
                 "value": round(N * 4 * E / (k_ms / 1e3) / 1e9, 1), "unit": "GB/s"},
             "roofline": ({"bound": "nvlink", "achieved": round(nv_bytes / (k_ms / 1e3) / 1e9, 1),

@@ -272,3 +272,48 @@ class P2PShardedPHub:
             capi.phub_free_shared(self.device, p)
         self._own = {}
         self.hub.close()
+
+
+class AllReduceBaseline:
+    """Comparison baseline (the paper's Gloo comparison,
+    P:1080-1085: "we ran our SGD/Nesterov optimizer on all nodes after
+    reduction"): every GPU sums its hosted workers, NCCL all-reduces the sums
+    (ring/tree/NVLS order -- NOT worker order, so results match the oracle only
+    within rounding, reading R3), then runs the Nesterov step on the WHOLE model
+    (libphub kernel with one pushed gradient, rescale 1/N).  Not the product
+    path; it exists to be measured against it."""
+
+    def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
+                 device=None, group=None):
+        import torch
+        import torch.distributed as dist
+        from .phub import PHub
+        self.group = group
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, rank, world)
+        self.hub = PHub(key_sizes, 1, chunk_size_bytes=chunk_size_bytes, lr=lr,
+                        momentum=momentum, rescale=1.0 / num_workers, device=self.device)
+        self.sum = torch.zeros(self.hub.E_padded, dtype=torch.float32,
+                               device=f"cuda:{self.device}")
+        self.replica = self.hub.weights()
+
+    @property
+    def hosted(self):
+        return self.plan.hosted()
+
+    def exchange(self, grads: dict):
+        import torch.distributed as dist
+        hosted = self.hosted
+        self.sum.copy_(grads[hosted[0]])
+        for w in hosted[1:]:
+            self.sum.add_(grads[w])
+        dist.all_reduce(self.sum, group=self.group)
+        self.hub.push(0, self.sum)
+        self.hub.aggregate_optimize()
+
+    def weights(self):
+        return self.replica
+
+    def close(self):
+        self.hub.close()
