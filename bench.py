@@ -42,9 +42,12 @@ def parse():
     ap.add_argument("--config", default="vgg19")
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--chunk-bytes", type=int, default=None)
-    ap.add_argument("--kernel", default="auto", choices=["auto", "flat", "flat128", "tiles", "wide"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "flat", "flat128", "tiles", "wide", "bulk"])
     ap.add_argument("--cache", default="enabled", choices=["enabled", "bypass"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--grid", type=int, default=0, help="CTAs for the flat kernel (0 = auto)")
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the round replayed from a captured CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -430,13 +433,15 @@ def bench_single(args, mname, N, cb):
     hub = PHub(sizes, N, chunk_size_bytes=cb, device=0)
     kern = {"auto": capi.PHUB_KERNEL_AUTO, "flat": capi.PHUB_KERNEL_FLAT,
             "flat128": capi.PHUB_KERNEL_FLAT128, "tiles": capi.PHUB_KERNEL_TILES,
-            "wide": capi.PHUB_KERNEL_WIDE}[args.kernel]
+            "wide": capi.PHUB_KERNEL_WIDE, "bulk": capi.PHUB_KERNEL_BULK}[args.kernel]
     if kern == capi.PHUB_KERNEL_WIDE:
         hub.close()
         hub = PHub(sizes, N, chunk_size_bytes=cb, device=0, keep_aggregate=True)
     hub.set_option(capi.PHUB_OPT_KERNEL, kern)
     hub.set_option(capi.PHUB_OPT_CACHE, capi.PHUB_CACHE_BYPASS if args.cache == "bypass"
                    else capi.PHUB_CACHE_ENABLED)
+    if args.grid:
+        hub.set_option(capi.PHUB_OPT_GRID, args.grid)
     E, Ep = hub.E, hub.E_padded
     idx = torch.as_tensor(hub.padded_index(), device=dev)
     hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
@@ -484,7 +489,11 @@ def bench_single(args, mname, N, cb):
     algo_bytes = (4 * N + 16) * owned
     achieved = algo_bytes / (k_ms_mean / 1e3) / 1e9
     peak, peak_src = measured_peaks()
-    kname = {0: "auto", 1: "flat", 2: "tiles", 3: "flat128", 4: "wide"}[kern]
+    kname = {0: "auto", 1: "flat", 2: "tiles", 3: "flat128", 4: "wide", 5: "bulk"}[kern]
+
+    graph = None
+    if args.graph:
+        graph = bench_graph(hub, grads, N, E, stream, args.steps)
 
     # ---- end to end through the public API with host buffers (pinned), H2D/D2H inside
     e2e = None
@@ -518,11 +527,42 @@ def bench_single(args, mname, N, cb):
                      "bytes_per_element": 4 * N + 16, "peak_source": peak_src},
         "clocks": clocks.summary(),
         "gpu_launches": launches,
+        "graph": graph,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
     print(json.dumps(out))
     hub.close()
+
+
+def bench_graph(hub, grads, N, E, stream, steps, rounds_per_graph=20):
+    """Launch-bound configs: the push bookkeeping is host-only, so a round's GPU
+    work is one kernel; capture `rounds_per_graph` rounds' kernels in one CUDA
+    graph and replay it (the receipts/iteration bookkeeping runs once per
+    captured round at capture time, not per replay)."""
+    import torch
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(stream)
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(rounds_per_graph):
+                for w in range(N):
+                    hub.push(w, grads[w])
+                hub.aggregate_optimize()
+    torch.cuda.synchronize()
+    reps = max(1, steps // rounds_per_graph)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3 / (reps * rounds_per_graph)
+    return {"us_per_round": round(t * 1e6, 3), "value": round(N * 4 * E / t / 1e9, 2),
+            "unit": "GB/s", "rounds_per_graph": rounds_per_graph, "replays": reps}
 
 
 def bench_e2e(hub, grads, N, E, Ep, stream, steps):

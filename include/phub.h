@@ -253,8 +253,10 @@ enum {
     PHUB_KERNEL_FLAT = 1,     /* flat owned range, 256-bit LDG/STG (needs 32-B alignment) */
     PHUB_KERNEL_TILES = 2,    /* one CTA per chunk tile, per-(worker,key) pointers       */
     PHUB_KERNEL_FLAT128 = 3,  /* flat owned range, 128-bit LDG/STG                       */
-    PHUB_KERNEL_WIDE = 4      /* ablation: wide aggregation, N-1 pairwise passes + NAG   */
+    PHUB_KERNEL_WIDE = 4,     /* ablation: wide aggregation, N-1 pairwise passes + NAG   */
                               /* pass (MXNet style)                           */
+    PHUB_KERNEL_BULK = 5      /* flat range staged through shared memory by 1-D bulk     */
+                              /* async copies (TMA engine, mbarrier ring); N <= 8        */
 };
 enum {
     PHUB_CACHE_ENABLED = 0,   /* w' stored evict-last (kept in L2 for the pull), grads   */

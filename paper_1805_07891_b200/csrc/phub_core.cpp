@@ -549,11 +549,15 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
     int variant = c->kernel;
     if (variant == PHUB_KERNEL_AUTO)
         variant = !flat ? PHUB_KERNEL_TILES : (align32 ? PHUB_KERNEL_FLAT : PHUB_KERNEL_FLAT128);
+    if (variant == PHUB_KERNEL_BULK && !(flat && align32 && c->N <= 8))
+        return c->fail(PHUB_ERR_UNSUPPORTED, "bulk kernel needs whole-model pushes, contiguous "
+                       "ownership, 32-B aligned chunks and N <= 8");
     if ((variant == PHUB_KERNEL_FLAT && !(flat && align32)) ||
         ((variant == PHUB_KERNEL_FLAT128 || variant == PHUB_KERNEL_WIDE) && !flat))
         return c->fail(PHUB_ERR_UNSUPPORTED, "forced kernel variant %d needs whole-model pushes, "
                        "contiguous ownership and aligned chunks", variant);
-    if (!c->replicas.empty() && variant != PHUB_KERNEL_FLAT && variant != PHUB_KERNEL_FLAT128)
+    if (!c->replicas.empty() && variant != PHUB_KERNEL_FLAT && variant != PHUB_KERNEL_FLAT128 &&
+        variant != PHUB_KERNEL_BULK)
         return c->fail(PHUB_ERR_UNSUPPORTED, "replica stores need the flat kernel (whole-model "
                        "or owned-range pushes under CONTIG ownership)");
     if (variant == PHUB_KERNEL_WIDE && !c->keep_agg)
@@ -563,7 +567,8 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
     c->launches = 0;
     const uint64_t b = contig_mode(c) ? c->own_begin[c->rank] : 0;
     const uint64_t eend = contig_mode(c) ? c->own_end[c->rank] : 0;
-    if (variant == PHUB_KERNEL_FLAT || variant == PHUB_KERNEL_FLAT128) {
+    if (variant == PHUB_KERNEL_FLAT || variant == PHUB_KERNEL_FLAT128 ||
+        variant == PHUB_KERNEL_BULK) {
         phub::FlatArgs a{};
         for (int w = 0; w < c->N; ++w) a.g[w] = reinterpret_cast<const float*>(c->base[(size_t)w * c->K]);
         a.w = c->d_w;
@@ -582,7 +587,11 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
         int grid = c->grid_override ? c->grid_override : c->flat_grid[vec == 8][c->keep_agg];
         grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, (nvec + phub::kThreads - 1) /
                                                                       phub::kThreads));
-        e = phub::launch_flat(a, vec, c->cache, grid, s, &c->launches);
+        if (variant == PHUB_KERNEL_BULK)
+            e = phub::launch_bulk(a, c->grid_override ? c->grid_override : c->num_sms, s,
+                                  &c->launches);
+        else
+            e = phub::launch_flat(a, vec, c->cache, grid, s, &c->launches);
     } else if (variant == PHUB_KERNEL_WIDE) {
         phub::WideArgs a{};
         for (int w = 0; w < c->N; ++w) a.g[w] = reinterpret_cast<const float*>(c->base[(size_t)w * c->K]);
@@ -852,7 +861,7 @@ phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
     switch (option) {
         case PHUB_OPT_KERNEL:
-            if (value < PHUB_KERNEL_AUTO || value > PHUB_KERNEL_WIDE)
+            if (value < PHUB_KERNEL_AUTO || value > PHUB_KERNEL_BULK)
                 return c->fail(PHUB_ERR_INVALID_ARGUMENT, "unknown kernel variant");
             c->kernel = (int)value;
             return PHUB_OK;

@@ -248,6 +248,134 @@ __global__ void __launch_bounds__(kThreads) k_tiles(const __grid_constant__ Tile
     }
 }
 
+// ------------------------------------------------ bulk-copy (TMA) staging
+// Variant with the loads taken off the register file: one producer thread per
+// CTA streams each tile's N gradient slices and the w, v slices into a
+// shared-memory ring with 1-D bulk async copies (cp.async.bulk, SASS UBLKCP,
+// completion counted on an mbarrier), while 8 consumer warps compute from
+// shared memory and store w', v' with 256-bit STG.  Same arithmetic and order.
+constexpr int kBulkTile = 2048;                  // elements per stream per stage (8 KB)
+constexpr int kBulkStages = 2;
+constexpr int kBulkConsumers = 256;              // 8 warps; +1 producer warp
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}"
+        :: "r"(smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;"
+        :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+
+template <int NW, bool AGG>
+__global__ void __launch_bounds__(kBulkConsumers + 32, 1) k_bulk(const __grid_constant__ FlatArgs a) {
+    constexpr int S = NW + 2;                           // streams per tile: grads, w, v
+    extern __shared__ __align__(128) float smem[];      // [stage][stream][kBulkTile]
+    __shared__ uint64_t full[kBulkStages], empty[kBulkStages];
+    const uint64_t n = a.end - a.begin;
+    const uint64_t ntiles = (n + kBulkTile - 1) / kBulkTile;
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kBulkStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kBulkConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kBulkConsumers / 32) {                   // ---- producer warp
+        if ((threadIdx.x & 31) == 0) {
+            uint64_t pol_first;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+            int stage = 0;
+            uint32_t phase = 0;
+            for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                const uint64_t off = a.begin + t * kBulkTile;
+                const uint32_t len = (uint32_t)(a.end - off < (uint64_t)kBulkTile ? a.end - off : (uint64_t)kBulkTile);
+                const uint32_t bytes = len * 4;
+                mbar_expect_tx(&full[stage], bytes * S);
+                float* st = smem + (size_t)stage * S * kBulkTile;
+#pragma unroll
+                for (int k = 0; k < NW; ++k)
+                    bulk_g2s(st + k * kBulkTile, a.g[k] + off, bytes, &full[stage], pol_first);
+                bulk_g2s(st + NW * kBulkTile, a.w + off, bytes, &full[stage], pol_first);
+                bulk_g2s(st + (NW + 1) * kBulkTile, a.v + off, bytes, &full[stage], pol_first);
+                if (++stage == kBulkStages) { stage = 0; phase ^= 1; }
+            }
+        }
+        return;
+    }
+    // ---- consumer warps: 8 elements per thread per tile (one 256-bit vector)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&full[stage], phase);
+        const uint64_t off = a.begin + t * kBulkTile;
+        const uint32_t len = (uint32_t)(a.end - off < (uint64_t)kBulkTile ? a.end - off : (uint64_t)kBulkTile);
+        const float* st = smem + (size_t)stage * S * kBulkTile;
+        for (uint32_t e = threadIdx.x * 8; e < len; e += kBulkConsumers * 8) {
+            V8 acc = *reinterpret_cast<const V8*>(st + e);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc.x[j] = __fadd_rn(0.0f, acc.x[j]);
+#pragma unroll
+            for (int k = 1; k < NW; ++k) {
+                const V8 gk = *reinterpret_cast<const V8*>(st + k * kBulkTile + e);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc.x[j] = __fadd_rn(acc.x[j], gk.x[j]);
+            }
+            V8 wv = *reinterpret_cast<const V8*>(st + NW * kBulkTile + e);
+            V8 vv = *reinterpret_cast<const V8*>(st + (NW + 1) * kBulkTile + e);
+            V8 sv = acc;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) nag(acc.x[j], wv.x[j], vv.x[j], a.lr, a.mu, a.rescale);
+            st_w<PHUB_CACHE_ENABLED>(reinterpret_cast<V8*>(a.w + off + e), wv);
+            st_stream(reinterpret_cast<V8*>(a.v + off + e), vv);
+            if constexpr (AGG) st_stream(reinterpret_cast<V8*>(a.agg + off + e), sv);
+            for (int r = 0; r < a.nrep; ++r) *reinterpret_cast<V8*>(a.rep[r] + off + e) = wv;
+        }
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kBulkStages) { stage = 0; phase ^= 1; }
+    }
+    if (a.nrep) __threadfence_system();
+}
+
+template <bool AGG>
+void* pick_bulk(int nw) {
+    switch (nw) {
+        case 1: return (void*)k_bulk<1, AGG>;
+        case 2: return (void*)k_bulk<2, AGG>;
+        case 3: return (void*)k_bulk<3, AGG>;
+        case 4: return (void*)k_bulk<4, AGG>;
+        case 5: return (void*)k_bulk<5, AGG>;
+        case 6: return (void*)k_bulk<6, AGG>;
+        case 7: return (void*)k_bulk<7, AGG>;
+        case 8: return (void*)k_bulk<8, AGG>;
+        default: return nullptr;
+    }
+}
+
 // -------------------------------------------------------- wide (ablation)
 // pass 1: merge = (+0 + g0) [+ g1];  pass k: merge = merge + gk;  NAG pass.
 __global__ void __launch_bounds__(kThreads) k_wide_first(const __grid_constant__ WideArgs a) {
@@ -365,6 +493,21 @@ cudaError_t launch_tiles(const TileArgs& a, int grid, cudaStream_t s, int* launc
     fn<<<grid, kThreads, 0, s>>>(a);
     ++*launches;
     return cudaGetLastError();
+}
+
+size_t bulk_smem_bytes(int nw) { return (size_t)kBulkStages * (nw + 2) * kBulkTile * sizeof(float); }
+
+cudaError_t launch_bulk(const FlatArgs& a, int grid, cudaStream_t s, int* launches) {
+    if (a.end <= a.begin) return cudaSuccess;
+    void* fn = a.agg ? pick_bulk<true>(a.nw) : pick_bulk<false>(a.nw);
+    if (!fn) return cudaErrorInvalidValue;
+    const size_t smem = bulk_smem_bytes(a.nw);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    void* args[] = {const_cast<FlatArgs*>(&a)};
+    e = cudaLaunchKernel(fn, dim3(grid), dim3(kBulkConsumers + 32), args, smem, s);
+    ++*launches;
+    return e;
 }
 
 cudaError_t launch_wide(const WideArgs& a, int grid, cudaStream_t s, int* launches) {

@@ -56,6 +56,9 @@ struct WideArgs {                     // ablation: wide aggregation
 cudaError_t launch_flat(const FlatArgs& a, int vec, int cache, int grid, cudaStream_t s,
                         int* launches);
 cudaError_t launch_tiles(const TileArgs& a, int grid, cudaStream_t s, int* launches);
+// TMA-style staging: 1-D bulk async copies into a shared-memory ring (nw <= 8).
+cudaError_t launch_bulk(const FlatArgs& a, int grid, cudaStream_t s, int* launches);
+size_t bulk_smem_bytes(int nw);
 cudaError_t launch_wide(const WideArgs& a, int grid, cudaStream_t s, int* launches);
 
 // Resident CTAs per SM of the flat kernel for (vec, nw, agg) -- grid sizing.

@@ -107,7 +107,7 @@ def test_tiny_config_bit_exact():
     assert hub.iteration == 1
 
 
-@pytest.mark.parametrize("kernel", ["FLAT", "FLAT128", "TILES", "WIDE"])
+@pytest.mark.parametrize("kernel", ["FLAT", "FLAT128", "TILES", "WIDE", "BULK"])
 def test_kernel_variants_bit_exact(kernel):
     from paper_1805_07891_b200 import capi
     _, launches = check_round(SMALL, 8, kernel=getattr(capi, f"PHUB_KERNEL_{kernel}"))
@@ -117,6 +117,13 @@ def test_kernel_variants_bit_exact(kernel):
 @pytest.mark.parametrize("N", [1, 2, 3, 5, 7, 8, 9, 16, 33])
 def test_worker_counts(N):
     check_round(SMALL, N, seed=N)
+
+
+@pytest.mark.parametrize("N", [1, 3, 8])
+@pytest.mark.parametrize("name", ["tiny", "resnet50"])
+def test_bulk_kernel_configs(N, name):
+    from paper_1805_07891_b200 import capi
+    check_round(manifest(name), N, kernel=capi.PHUB_KERNEL_BULK, seed=N)
 
 
 @pytest.mark.parametrize("cb", [4, 12, 64, 4096, 32768, 1 << 20])
@@ -409,3 +416,62 @@ def test_full_size_sampled(name, N, cb):
     assert_bits_equal(w_all[samp], rw, f"{name}@{cb} sampled w'")
     assert_bits_equal(v_all[samp], rv, f"{name}@{cb} sampled v'")
     hub.close()
+
+
+# -------------------------------------------- fused replica stores (P2P pull)
+def test_replica_stores_single_gpu():
+    """The fused pull path (phub_set_replicas) stores w' of the owned range into
+    extra replicas; on one GPU local buffers stand in for peer replicas."""
+    from paper_1805_07891_b200 import capi
+    sizes = manifest("resnet50")
+    G, N = 4, 4
+    E = sum(sizes)
+    w0, v0 = host_state(E, 3)
+    rw, _, _ = oracle.round_(sizes, host_grads(E, N, 3), w0, v0, 0.1, 0.9)
+    reps = None
+    gd = None
+    for r in range(G):
+        hub = _hub(sizes, N, num_owners=G, owner_rank=r, owner_policy="contig")
+        hub.load_state(w0, v0)
+        if reps is None:
+            reps = [torch.full((hub.E_padded,), float("nan"), device=DEV) for _ in range(2)]
+            gd = device_grads(hub, N, 3)
+        capi.phub_set_replicas(hub.ctx, [t.data_ptr() for t in reps])
+        run_round(hub, gd)
+        hub.close()
+    from paper_1805_07891_b200 import PHub
+    h = PHub(sizes, N, device=0)
+    pidx = h.padded_index()
+    h.close()
+    for t in reps:
+        assert_bits_equal(t.cpu().numpy()[pidx], rw, "replica assembled from 4 owners")
+
+
+def test_replica_errors():
+    from paper_1805_07891_b200 import PhubError, capi
+    hub = _hub(SMALL, 2, num_owners=2, owner_rank=0, owner_policy="lpt")
+    t = torch.zeros(hub.E_padded, device=DEV)
+    with pytest.raises(PhubError):
+        capi.phub_set_replicas(hub.ctx, [t.data_ptr()])              # LPT: no contiguous range
+    hub.close()
+    hub = _hub(SMALL, 2)
+    with pytest.raises(PhubError):
+        capi.phub_set_replicas(hub.ctx, [t.data_ptr() + 4])          # misaligned
+    with pytest.raises(PhubError):
+        capi.phub_set_replicas(hub.ctx, [np.zeros(4, f32).ctypes.data])   # host memory
+    capi.phub_set_replicas(hub.ctx, [t.data_ptr()])
+    hub.set_option(capi.PHUB_OPT_KERNEL, capi.PHUB_KERNEL_TILES)
+    for w, g in enumerate(device_grads(hub, 2)):
+        hub.push(w, g)
+    with pytest.raises(PhubError) as e:
+        hub.aggregate_optimize()                                        # replicas need flat
+    assert capi.STATUS_NAMES[e.value.status] == "PHUB_ERR_UNSUPPORTED"
+    hub.close()
+
+
+def test_shared_alloc_and_ipc_handle():
+    from paper_1805_07891_b200 import capi
+    p = capi.phub_alloc_shared(0, 1 << 20)
+    h = capi.phub_ipc_get_handle(0, p)
+    assert len(h) == 64 and any(h)
+    capi.phub_free_shared(0, p)
