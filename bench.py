@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--cache", default="enabled", choices=["enabled", "bypass"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--grid", type=int, default=0, help="CTAs for the flat kernel (0 = auto)")
+    ap.add_argument("--seg", type=int, default=-1, help="flat kernel CTA segment (vectors)")
+    ap.add_argument("--minb", type=int, default=0, help="flat kernel resident-CTA build")
+    ap.add_argument("--tile-elems", type=int, default=0, help="chunk-tile kernel tile size")
     ap.add_argument("--graph", action="store_true",
                     help="also time the round replayed from a captured CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
@@ -442,6 +445,12 @@ def bench_single(args, mname, N, cb):
                    else capi.PHUB_CACHE_ENABLED)
     if args.grid:
         hub.set_option(capi.PHUB_OPT_GRID, args.grid)
+    if args.seg >= 0:
+        hub.set_option(capi.PHUB_OPT_FLAT_SEG, args.seg)
+    if args.minb:
+        hub.set_option(capi.PHUB_OPT_FLAT_MINB, args.minb)
+    if args.tile_elems:
+        hub.set_option(capi.PHUB_OPT_TILE_ELEMS, args.tile_elems)
     E, Ep = hub.E, hub.E_padded
     idx = torch.as_tensor(hub.padded_index(), device=dev)
     hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
@@ -512,7 +521,9 @@ def bench_single(args, mname, N, cb):
         "vs_baseline": round(value / PAPER_GBS, 2), "dtype": "f32", "data": "synthetic",
         "exchanges_per_s": round(N / t_step, 1),
         "config": {"workload": args.config, "keys": len(sizes), "E": E, "E_padded": Ep,
-                   "workers": N, "chunk_bytes": cb, "mode": "M1 (1 GPU, pushes resident, "
+                   "workers": N, "chunk_bytes": cb, "seg": args.seg, "minb": args.minb,
+                   "grid": args.grid, "tile_elems": args.tile_elems,
+                   "mode": "M1 (1 GPU, pushes resident, "
                    "zero-copy BORROW)", "kernel": kname, "cache": args.cache,
                    "l2": f"no flush: inputs exceed L2 ({(4 * N + 16) * E / 1e9:.2f} GB/round "
                          f"vs 126 MB L2)" if (4 * N + 16) * E > 4 * 126e6 else

@@ -146,6 +146,18 @@ phub_status phub_push(phub_ctx ctx, int32_t worker, int32_t key, const float* gr
  * clears the receipts and advances the iteration counter. */
 phub_status phub_aggregate_optimize(phub_ctx ctx, void* stream);
 
+/* Streaming aggregation ("when a chunk is received from all workers, it
+ * can be optimized"; "streaming aggregation and optimization"): launch
+ * the fused kernel on the chunks of every key whose N pushes have all arrived
+ * and that has not been aggregated in this iteration (chunk-tile kernel, one
+ * launch per run of consecutive ready keys); *keys_done (nullable) receives
+ * how many keys were launched.  When every key of the iteration has been
+ * aggregated the receipts clear and the iteration advances.  A later
+ * phub_aggregate_optimize processes only the keys not yet aggregated.
+ * Results are bit-identical to one phub_aggregate_optimize (element-wise,
+ * P:657).  Not combinable with phub_set_replicas (PHUB_ERR_UNSUPPORTED). */
+phub_status phub_aggregate_ready(phub_ctx ctx, void* stream, uint64_t* keys_done);
+
 /* Pull: copy the current weights of `key` (n == n_k) or of
  * the whole padded model (PHUB_ALL_KEYS, n == E_padded) into `dst` (host or
  * device memory) on `stream`.  Before any aggregate it returns the initial
@@ -246,7 +258,11 @@ enum {
     PHUB_OPT_KERNEL = 1,      /* PHUB_KERNEL_*                                           */
     PHUB_OPT_GRID = 2,        /* CTAs for the flat kernels, 0 = auto (SMs x occupancy)   */
     PHUB_OPT_TILE_ELEMS = 3,  /* max elements per CTA tile in the chunk-tile kernel      */
-    PHUB_OPT_CACHE = 4        /* PHUB_CACHE_*: L2 policy of the pulled weights   */
+    PHUB_OPT_CACHE = 4,       /* PHUB_CACHE_*: L2 policy of the pulled weights   */
+    PHUB_OPT_FLAT_SEG = 5,    /* flat kernels: 0 = grid-stride, else CTA-contiguous      */
+                              /* segments of this many vectors                           */
+    PHUB_OPT_FLAT_MINB = 6    /* tuning: 0 = default build; 1,2,4,6,8 = N=8 256-bit flat */
+                              /* kernel compiled for that many resident CTAs per SM      */
 };
 enum {
     PHUB_KERNEL_AUTO = 0,     /* flat 256-bit kernel when eligible, else chunk tiles     */

@@ -28,6 +28,7 @@ PHUB_OWNED_RANGE = -2
 PHUB_COPY, PHUB_BORROW = 0, 1
 PHUB_OWNER_LPT, PHUB_OWNER_CONTIG = 0, 1
 PHUB_OPT_KERNEL, PHUB_OPT_GRID, PHUB_OPT_TILE_ELEMS, PHUB_OPT_CACHE = 1, 2, 3, 4
+PHUB_OPT_FLAT_SEG, PHUB_OPT_FLAT_MINB = 5, 6
 (PHUB_KERNEL_AUTO, PHUB_KERNEL_FLAT, PHUB_KERNEL_TILES, PHUB_KERNEL_FLAT128,
  PHUB_KERNEL_WIDE, PHUB_KERNEL_BULK) = range(6)
 PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS = 0, 1
@@ -67,6 +68,7 @@ _SIGS = {
     "phub_push": (C.c_int, [phub_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32,
                             C.c_void_p]),
     "phub_aggregate_optimize": (C.c_int, [phub_ctx, C.c_void_p]),
+    "phub_aggregate_ready": (C.c_int, [phub_ctx, C.c_void_p, _u64p]),
     "phub_pull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
     "phub_pushpull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32,
                                 C.c_void_p, C.c_void_p]),
@@ -149,6 +151,12 @@ def phub_push(ctx, worker: int, key: int, grad_ptr: int, n: int, mode: int, stre
 
 def phub_aggregate_optimize(ctx, stream: int = 0):
     _check(_lib.phub_aggregate_optimize(ctx, stream), "phub_aggregate_optimize", ctx)
+
+
+def phub_aggregate_ready(ctx, stream: int = 0) -> int:
+    n = C.c_uint64()
+    _check(_lib.phub_aggregate_ready(ctx, stream, C.byref(n)), "phub_aggregate_ready", ctx)
+    return int(n.value)
 
 
 def phub_pull(ctx, key: int, dst_ptr: int, n: int, stream: int = 0):

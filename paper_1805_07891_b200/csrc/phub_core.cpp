@@ -61,6 +61,7 @@ struct phub_ctx_s {
     uint64_t owned_elems = 0;
     uint64_t n_tiles = 0;
     Tile* d_tiles = nullptr;
+    std::vector<uint64_t> key_tile_begin, key_tile_end;   // owned tiles of key k, in order
     uint32_t tile_elems = 8192;
 
     // arenas
@@ -72,6 +73,8 @@ struct phub_ctx_s {
     // push state (iteration-scoped)
     std::vector<uint8_t> got;         // K x N receipts
     uint64_t got_count = 0;
+    std::vector<uint8_t> done;        // key aggregated this iteration (streaming, NEXT-1)
+    uint64_t done_count = 0;
     std::vector<uintptr_t> base;      // N x K: base + 4*dev_off = byte address
     std::vector<uintptr_t> base_uploaded;
     uintptr_t* d_base = nullptr;
@@ -80,6 +83,8 @@ struct phub_ctx_s {
     // options + counters
     int kernel = PHUB_KERNEL_AUTO;
     int grid_override = 0;
+    uint64_t flat_seg = 0;
+    int flat_minb = 0;
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     uint64_t iteration = 0;
@@ -210,10 +215,14 @@ static void build_ranges(phub_ctx c) {
 static bool contig_mode(phub_ctx c) { return c->G == 1 || c->policy == PHUB_OWNER_CONTIG; }
 
 // Owned chunks split into CTA tiles of <= tile_elems (chunk-tile kernel).
+// Tiles stay in vkey order, so each key's tiles are one index range.
 static std::vector<Tile> build_tiles(phub_ctx c) {
     std::vector<Tile> tiles;
+    c->key_tile_begin.assign(c->K, 0);
+    c->key_tile_end.assign(c->K, 0);
     for (const auto& ch : c->chunks) {
         if (ch.owner != c->rank) continue;
+        if (c->key_tile_end[ch.key_id] == 0) c->key_tile_begin[ch.key_id] = tiles.size();
         for (uint64_t o = 0; o < ch.length; o += c->tile_elems) {
             Tile t;
             t.off = chunk_dev_off(c, ch) + o;
@@ -221,6 +230,7 @@ static std::vector<Tile> build_tiles(phub_ctx c) {
             t.key = ch.key_id;
             tiles.push_back(t);
         }
+        c->key_tile_end[ch.key_id] = tiles.size();
     }
     return tiles;
 }
@@ -324,6 +334,7 @@ phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
     std::vector<Tile> tiles = build_tiles(c);
     c->n_tiles = tiles.size();
     c->got.assign((size_t)c->K * c->N, 0);
+    c->done.assign(c->K, 0);
     c->base.assign((size_t)c->K * c->N, 0);
 
     DeviceGuard g(c->device);
@@ -524,6 +535,92 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
     return PHUB_OK;
 }
 
+// Chunk-tile kernel over owned tiles [t0, t1) (per-(worker,key) base table).
+static cudaError_t launch_tile_range(phub_ctx c, cudaStream_t s, uint64_t t0, uint64_t t1) {
+    if (t1 <= t0) return cudaSuccess;
+    if (c->base != c->base_uploaded) {
+        // pageable source: returns once staged, so `base` may change afterwards
+        cudaError_t e = cudaMemcpyAsync(c->d_base, c->base.data(),
+                                        sizeof(uintptr_t) * c->base.size(),
+                                        cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return e;
+        c->base_uploaded = c->base;
+    }
+    phub::TileArgs a{};
+    a.tiles = c->d_tiles + t0;
+    a.ntiles = t1 - t0;
+    a.base = c->d_base;
+    a.K = c->K;
+    a.nw = c->N;
+    a.w = c->d_w;
+    a.v = c->d_v;
+    a.agg = c->keep_agg ? c->d_agg : nullptr;
+    a.lr = c->lr;
+    a.mu = c->mu;
+    a.rescale = c->rescale;
+    int grid = c->grid_override ? c->grid_override : (int)std::min<uint64_t>(t1 - t0, 1u << 30);
+    return phub::launch_tiles(a, std::max(grid, 1), s, &c->launches);
+}
+
+// Tiles of every key in [k0, k1) that is not yet aggregated, as maximal runs.
+static cudaError_t launch_keys(phub_ctx c, cudaStream_t s, const std::vector<uint8_t>& pick) {
+    cudaError_t e = cudaSuccess;
+    int k = 0;
+    while (k < c->K && e == cudaSuccess) {
+        if (!pick[k]) { ++k; continue; }
+        int k1 = k;
+        uint64_t t0 = UINT64_MAX, t1 = 0;
+        while (k1 < c->K && pick[k1]) {
+            if (c->key_tile_end[k1] > c->key_tile_begin[k1]) {
+                t0 = std::min(t0, c->key_tile_begin[k1]);
+                t1 = std::max(t1, c->key_tile_end[k1]);
+            }
+            ++k1;
+        }
+        if (t1 > 0) e = launch_tile_range(c, s, t0, t1);
+        k = k1;
+    }
+    return e;
+}
+
+static void end_iteration(phub_ctx c) {
+    std::fill(c->got.begin(), c->got.end(), 0);
+    c->got_count = 0;
+    std::fill(c->done.begin(), c->done.end(), 0);
+    c->done_count = 0;
+    ++c->iteration;
+}
+
+phub_status phub_aggregate_ready(phub_ctx c, void* stream, uint64_t* keys_done) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    if (!c->replicas.empty())
+        return c->fail(PHUB_ERR_UNSUPPORTED, "streaming aggregation does not store replicas");
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<uint8_t> pick(c->K, 0);
+    uint64_t n = 0;
+    for (int k = 0; k < c->K; ++k) {
+        if (c->done[k]) continue;
+        bool all = true;
+        for (int w = 0; all && w < c->N; ++w) all = c->got[(size_t)k * c->N + w] != 0;
+        if (all) {
+            pick[k] = 1;
+            ++n;
+        }
+    }
+    c->launches = 0;
+    cudaError_t e = n ? launch_keys(c, s, pick) : cudaSuccess;
+    c->launches_total += (uint64_t)c->launches;
+    if (e != cudaSuccess) return c->cuda_fail(e, "kernel launch");
+    for (int k = 0; k < c->K; ++k)
+        if (pick[k]) c->done[k] = 1;
+    c->done_count += n;
+    if (keys_done) *keys_done = n;
+    if (c->done_count == (uint64_t)c->K) end_iteration(c);
+    return PHUB_OK;
+}
+
 phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
     if (c->failed) return PHUB_ERR_CUDA;
@@ -565,6 +662,18 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
 
     cudaError_t e = cudaSuccess;
     c->launches = 0;
+    if (c->done_count > 0) {
+        // part of the iteration was already aggregated by phub_aggregate_ready
+        if (!c->replicas.empty())
+            return c->fail(PHUB_ERR_UNSUPPORTED, "streaming aggregation does not store replicas");
+        std::vector<uint8_t> pick(c->K, 0);
+        for (int k = 0; k < c->K; ++k) pick[k] = !c->done[k];
+        e = launch_keys(c, s, pick);
+        c->launches_total += (uint64_t)c->launches;
+        if (e != cudaSuccess) return c->cuda_fail(e, "kernel launch");
+        end_iteration(c);
+        return PHUB_OK;
+    }
     const uint64_t b = contig_mode(c) ? c->own_begin[c->rank] : 0;
     const uint64_t eend = contig_mode(c) ? c->own_end[c->rank] : 0;
     if (variant == PHUB_KERNEL_FLAT || variant == PHUB_KERNEL_FLAT128 ||
@@ -587,9 +696,16 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
         int grid = c->grid_override ? c->grid_override : c->flat_grid[vec == 8][c->keep_agg];
         grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, (nvec + phub::kThreads - 1) /
                                                                       phub::kThreads));
+        a.seg = c->flat_seg;
         if (variant == PHUB_KERNEL_BULK)
             e = phub::launch_bulk(a, c->grid_override ? c->grid_override : c->num_sms, s,
                                   &c->launches);
+        else if (c->flat_minb && vec == 8 && c->N == 8 && !c->keep_agg)
+            e = phub::launch_flat_minb(
+                a, c->flat_minb,
+                c->grid_override ? c->grid_override
+                                 : c->num_sms * phub::flat_minb_blocks_per_sm(c->flat_minb),
+                s, &c->launches);
         else
             e = phub::launch_flat(a, vec, c->cache, grid, s, &c->launches);
     } else if (variant == PHUB_KERNEL_WIDE) {
@@ -607,34 +723,11 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
         int grid = c->grid_override ? c->grid_override : c->num_sms * 8;
         e = phub::launch_wide(a, grid, s, &c->launches);
     } else {
-        if (c->base != c->base_uploaded) {
-            // pageable source: returns once staged, so `base` may change afterwards
-            e = cudaMemcpyAsync(c->d_base, c->base.data(), sizeof(uintptr_t) * c->base.size(),
-                                cudaMemcpyHostToDevice, s);
-            if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpyAsync(base table)");
-            c->base_uploaded = c->base;
-        }
-        phub::TileArgs a{};
-        a.tiles = c->d_tiles;
-        a.ntiles = c->n_tiles;
-        a.base = c->d_base;
-        a.K = c->K;
-        a.nw = c->N;
-        a.w = c->d_w;
-        a.v = c->d_v;
-        a.agg = c->keep_agg ? c->d_agg : nullptr;
-        a.lr = c->lr;
-        a.mu = c->mu;
-        a.rescale = c->rescale;
-        int grid = c->grid_override ? c->grid_override
-                                    : (int)std::min<uint64_t>(c->n_tiles, 1u << 30);
-        e = phub::launch_tiles(a, std::max(grid, 1), s, &c->launches);
+        e = launch_tile_range(c, s, 0, c->n_tiles);
     }
     c->launches_total += (uint64_t)c->launches;
     if (e != cudaSuccess) return c->cuda_fail(e, "kernel launch");
-    std::fill(c->got.begin(), c->got.end(), 0);
-    c->got_count = 0;
-    ++c->iteration;
+    end_iteration(c);
     return PHUB_OK;
 }
 
@@ -880,6 +973,15 @@ phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
                         c->num_sms * phub::flat_blocks_per_sm(vec8 ? 8 : 4, c->N, agg, c->cache);
             return PHUB_OK;
         }
+        case PHUB_OPT_FLAT_SEG:
+            if (value < 0) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "segment must be >= 0");
+            c->flat_seg = (uint64_t)value;
+            return PHUB_OK;
+        case PHUB_OPT_FLAT_MINB:
+            if (!(value == 0 || value == 1 || value == 2 || value == 4 || value == 6 || value == 8))
+                return c->fail(PHUB_ERR_INVALID_ARGUMENT, "minb must be 0,1,2,4,6,8");
+            c->flat_minb = (int)value;
+            return PHUB_OK;
         case PHUB_OPT_TILE_ELEMS: {
             if (value < 1 || value > (1 << 30))
                 return c->fail(PHUB_ERR_INVALID_ARGUMENT, "tile elements must be in [1, 2^30]");

@@ -129,15 +129,15 @@ __device__ __forceinline__ void nag(float s, float& w, float& v, float lr, float
 // ------------------------------------------------------------ flat kernel
 // NW > 0: worker count fixed at compile time; NW == 0: any count <= 64, in
 // groups of 8 loads issued before their in-order adds.
+// One vector position i of the owned range: N gradient loads, in-order sum,
+// Nesterov, stores (local w, v, optional s, optional peer replicas).
 template <int NW, int VEC, int CACHE, bool AGG>
-__global__ void __launch_bounds__(kThreads) k_flat(const __grid_constant__ FlatArgs a) {
+__device__ __forceinline__ void flat_body(const FlatArgs& a, uint64_t i) {
     using V = VecT<VEC>;
-    const uint64_t n = (a.end - a.begin) / VEC;
     V* __restrict__ w = reinterpret_cast<V*>(a.w + a.begin);
     V* __restrict__ v = reinterpret_cast<V*>(a.v + a.begin);
     V* __restrict__ sa = AGG ? reinterpret_cast<V*>(a.agg + a.begin) : nullptr;
-    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    {
         float acc[VEC];
         if constexpr (NW > 0) {
             V gv[NW];
@@ -183,7 +183,36 @@ __global__ void __launch_bounds__(kThreads) k_flat(const __grid_constant__ FlatA
         for (int r = 0; r < a.nrep; ++r)
             reinterpret_cast<V*>(a.rep[r] + a.begin)[i] = wv;
     }
+}
+
+// Schedules: seg == 0 -> grid-stride over vectors (all CTAs sweep the range
+// together); seg > 0 -> each CTA takes contiguous segments of `seg` vectors
+// (CTAs spread over the range, like one CTA per chunk tile).
+template <int NW, int VEC, int CACHE, bool AGG>
+__device__ __forceinline__ void flat_loop(const FlatArgs& a) {
+    const uint64_t n = (a.end - a.begin) / VEC;
+    if (a.seg == 0) {
+        const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+        for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
+            flat_body<NW, VEC, CACHE, AGG>(a, i);
+    } else {
+        for (uint64_t b0 = (uint64_t)blockIdx.x * a.seg; b0 < n; b0 += (uint64_t)gridDim.x * a.seg) {
+            const uint64_t b1 = b0 + a.seg < n ? b0 + a.seg : n;
+            for (uint64_t i = b0 + threadIdx.x; i < b1; i += kThreads)
+                flat_body<NW, VEC, CACHE, AGG>(a, i);
+        }
+    }
     if (a.nrep) __threadfence_system();   // peer stores performed before the grid retires
+}
+
+template <int NW, int VEC, int CACHE, bool AGG>
+__global__ void __launch_bounds__(kThreads) k_flat(const __grid_constant__ FlatArgs a) {
+    flat_loop<NW, VEC, CACHE, AGG>(a);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_flat_minb(const __grid_constant__ FlatArgs a) {
+    flat_loop<8, 8, PHUB_CACHE_ENABLED, false>(a);
 }
 
 // ---------------------------------------------------------- chunk tiles
@@ -469,6 +498,35 @@ TileFn pick_tiles_nw(int nw) {
 }
 
 }  // namespace
+
+static const void* minb_fn(int minb) {
+    switch (minb) {
+        case 1: return reinterpret_cast<const void*>(k_flat_minb<1>);
+        case 2: return reinterpret_cast<const void*>(k_flat_minb<2>);
+        case 4: return reinterpret_cast<const void*>(k_flat_minb<4>);
+        case 6: return reinterpret_cast<const void*>(k_flat_minb<6>);
+        case 8: return reinterpret_cast<const void*>(k_flat_minb<8>);
+        default: return nullptr;
+    }
+}
+
+int flat_minb_blocks_per_sm(int minb) {
+    int nb = 0;
+    const void* fn = minb_fn(minb);
+    if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess)
+        return 1;
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_flat_minb(const FlatArgs& a, int minb, int grid, cudaStream_t s, int* launches) {
+    if (a.end <= a.begin) return cudaSuccess;
+    const void* fn = minb_fn(minb);
+    if (!fn || a.nw != 8 || a.agg) return cudaErrorInvalidValue;
+    void* args[] = {const_cast<FlatArgs*>(&a)};
+    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);
+    ++*launches;
+    return e;
+}
 
 int flat_blocks_per_sm(int vec, int nw, bool agg, int cache) {
     int nb = 0;

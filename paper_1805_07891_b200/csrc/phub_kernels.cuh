@@ -28,6 +28,7 @@ struct FlatArgs {
     int nw;
     int nrep;                         // extra replicas (peer-mapped) that also receive w'
     float* rep[kMaxReplicas];
+    uint64_t seg;                     // 0: grid-stride; else CTA-contiguous segments (vectors)
 };
 
 struct TileArgs {
@@ -63,5 +64,10 @@ cudaError_t launch_wide(const WideArgs& a, int grid, cudaStream_t s, int* launch
 
 // Resident CTAs per SM of the flat kernel for (vec, nw, agg) -- grid sizing.
 int flat_blocks_per_sm(int vec, int nw, bool agg, int cache);
+
+// Tuning experiment: the N=8, 256-bit flat kernel compiled for `minb` resident
+// CTAs per SM (launch bounds 1, 2, 4, 6 or 8).
+cudaError_t launch_flat_minb(const FlatArgs& a, int minb, int grid, cudaStream_t s, int* launches);
+int flat_minb_blocks_per_sm(int minb);
 
 }  // namespace phub

@@ -109,6 +109,10 @@ class PHub:
     def aggregate_optimize(self, stream=None):
         capi.phub_aggregate_optimize(self.ctx, self._stream(stream))
 
+    def aggregate_ready(self, stream=None) -> int:
+        """Streaming: aggregate every fully-pushed key not yet aggregated."""
+        return capi.phub_aggregate_ready(self.ctx, self._stream(stream))
+
     def pull(self, dst, key=PHUB_ALL_KEYS, n=None, stream=None):
         p, cnt = _ptr_len(dst, n)
         capi.phub_pull(self.ctx, int(key), p, cnt, self._stream(stream))

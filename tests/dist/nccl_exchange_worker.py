@@ -28,7 +28,8 @@ def main():
     dev = torch.device(f"cuda:{local}")
     dist.init_process_group("nccl", device_id=dev)
     rank, G = dist.get_rank(), dist.get_world_size()
-    sizes = manifest(name) if name != "small" else [3, 3, 9408, 64, 64, 4096, 20000, 1000, 7]
+    special = {"small": [3, 3, 9408, 64, 64, 4096, 20000, 1000, 7], "one": [5]}
+    sizes = special[name] if name in special else manifest(name)
     E = sum(sizes)
     cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
     sh = cls(sizes, N, chunk_size_bytes=cb, device=local)

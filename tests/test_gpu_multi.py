@@ -27,7 +27,8 @@ def _port():
 @pytest.mark.parametrize("mode", ["nccl", "p2p"])
 @pytest.mark.parametrize("G,name,N,cb,rounds", [
     (2, "small", 8, 32768, 2), (2, "tiny", 4, 4096, 1), (4, "resnet50", 8, 32768, 2),
-    (8, "resnet50", 8, 32768, 2), (8, "small", 8, 64, 1),
+    (8, "resnet50", 8, 32768, 2), (8, "small", 8, 64, 1), (2, "one", 2, 32768, 2),
+    (4, "one", 4, 32768, 1),
 ])
 def test_sharded_exchange_bit_exact(G, name, N, cb, rounds, mode):
     if _ngpus() < G:

@@ -475,3 +475,70 @@ def test_shared_alloc_and_ipc_handle():
     h = capi.phub_ipc_get_handle(0, p)
     assert len(h) == 64 and any(h)
     capi.phub_free_shared(0, p)
+
+
+# ------------------------------------------- streaming aggregation (NEXT-1)
+def test_streaming_aggregate_ready_backward_order():
+    """Keys arrive in reverse order (a backward pass); each key is aggregated as
+    soon as all N workers pushed it.  Same bits as one round."""
+    sizes = SMALL
+    N = 3
+    hub = _hub(sizes, N, keep_aggregate=True)
+    w0, v0 = host_state(hub.E, 5)
+    hub.load_state(w0, v0)
+    hg = host_grads(hub.E, N, 5)
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    keep = []
+    total = 0
+    for k in reversed(range(len(sizes))):
+        for w in range(N):
+            t = torch.tensor(hg[w][starts[k]:starts[k + 1]], device=DEV)
+            keep.append(t)
+            hub.push(w, t, key=k)
+            if w < N - 1:
+                assert hub.aggregate_ready() == 0        # not all workers yet
+        total += hub.aggregate_ready()
+        assert hub.iteration == (1 if k == 0 else 0)
+    assert total == len(sizes)
+    torch.cuda.synchronize()
+    w, v, s = hub.read_state()
+    rw, rv, rs = oracle.round_(sizes, hg, w0, v0, 0.1, 0.9)
+    assert_bits_equal(s, rs, "streamed s")
+    assert_bits_equal(w, rw, "streamed w")
+    assert_bits_equal(v, rv, "streamed v")
+
+
+def test_streaming_then_aggregate_rest():
+    sizes = SMALL
+    N = 2
+    hub = _hub(sizes, N)
+    w0, v0 = host_state(hub.E, 6)
+    hub.load_state(w0, v0)
+    gd = device_grads(hub, N, 6)
+    hg = host_grads(hub.E, N, 6)
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    keep = []
+    for k in (2, 3, 7):                                   # a few keys stream early
+        for w in range(N):
+            t = torch.tensor(hg[w][starts[k]:starts[k + 1]], device=DEV)
+            keep.append(t)
+            hub.push(w, t, key=k)
+    assert hub.aggregate_ready() == 3
+    for k in range(len(sizes)):
+        if k in (2, 3, 7):
+            continue
+        for w in range(N):
+            t = torch.tensor(hg[w][starts[k]:starts[k + 1]], device=DEV)
+            keep.append(t)
+            hub.push(w, t, key=k)
+    hub.aggregate_optimize()                              # only the remaining keys
+    assert hub.iteration == 1
+    w, v, _ = hub.read_state()
+    rw, rv, _ = oracle.round_(sizes, hg, w0, v0, 0.1, 0.9)
+    assert_bits_equal(w, rw, "w")
+    assert_bits_equal(v, rv, "v")
+    # the next iteration starts clean: whole-model pushes, flat kernel
+    run_round(hub, gd)
+    w2, _, _ = hub.read_state()
+    rw2, _, _ = oracle.round_(sizes, hg, rw, rv, 0.1, 0.9)
+    assert_bits_equal(w2, rw2, "w after next round")

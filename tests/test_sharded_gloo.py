@@ -19,6 +19,7 @@ def _free_port():
 
 @pytest.mark.parametrize("world,name,N,cb", [
     (2, "small", 4, 32768), (2, "tiny", 4, 4096), (4, "tiny", 8, 32768), (2, "small", 2, 64),
+    (4, "one", 4, 32768),            # one chunk: three owners own nothing
 ])
 def test_gloo_exchange(world, name, N, cb):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
