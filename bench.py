@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--seg", type=int, default=-1, help="flat kernel CTA segment (vectors)")
     ap.add_argument("--minb", type=int, default=0, help="flat kernel resident-CTA build")
     ap.add_argument("--tile-elems", type=int, default=0, help="chunk-tile kernel tile size")
+    ap.add_argument("--oneshot", type=int, default=-1, help="flat kernel one-vector-per-thread grid")
     ap.add_argument("--graph", action="store_true",
                     help="also time the round replayed from a captured CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
@@ -266,6 +267,23 @@ def bench_multi(args, mname, N, cb):
     cls = {"p2p": P2PShardedPHub, "nccl": ShardedPHub, "allreduce": AllReduceBaseline}[args.mode]
     sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
     hub, plan = sh.hub, sh.plan
+    from paper_1805_07891_b200 import capi
+    if args.grid:
+        hub.set_option(capi.PHUB_OPT_GRID, args.grid)
+    if args.seg >= 0:
+        hub.set_option(capi.PHUB_OPT_FLAT_SEG, args.seg)
+    if args.minb:
+        hub.set_option(capi.PHUB_OPT_FLAT_MINB, args.minb)
+    if args.oneshot >= 0:
+        hub.set_option(capi.PHUB_OPT_FLAT_ONESHOT, args.oneshot)
+    if args.tile_elems:
+        hub.set_option(capi.PHUB_OPT_TILE_ELEMS, args.tile_elems)
+    if args.kernel != "auto":
+        hub.set_option(capi.PHUB_OPT_KERNEL, {"flat": capi.PHUB_KERNEL_FLAT,
+                                              "flat128": capi.PHUB_KERNEL_FLAT128,
+                                              "tiles": capi.PHUB_KERNEL_TILES,
+                                              "wide": capi.PHUB_KERNEL_WIDE,
+                                              "bulk": capi.PHUB_KERNEL_BULK}[args.kernel])
     E, Ep = hub.E, hub.E_padded
     idx = torch.as_tensor(hub.padded_index(), device=dev)
     hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
@@ -387,7 +405,8 @@ def bench_multi(args, mname, N, cb):
                                if ar else
                                ("M3 (full exchange) nccl: NCCL grouped send/recv push, fused "
                                 "kernel on owner range, NCCL all-gather-v pull"),
-                       "parallelism": f"owner-sharded x{G}",
+                       "parallelism": f"owner-sharded x{G}", "kernel": args.kernel,
+                       "seg": args.seg, "minb": args.minb, "grid": args.grid,
                        "l2": "no flush: inputs exceed L2"},
             "owner_phase": None if (p2p or ar) else {
                 "mode": "M2 (kernel only, max over ranks)", "kernel_ms": round(k_ms, 4),
@@ -451,6 +470,8 @@ def bench_single(args, mname, N, cb):
         hub.set_option(capi.PHUB_OPT_FLAT_MINB, args.minb)
     if args.tile_elems:
         hub.set_option(capi.PHUB_OPT_TILE_ELEMS, args.tile_elems)
+    if args.oneshot >= 0:
+        hub.set_option(capi.PHUB_OPT_FLAT_ONESHOT, args.oneshot)
     E, Ep = hub.E, hub.E_padded
     idx = torch.as_tensor(hub.padded_index(), device=dev)
     hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
@@ -522,7 +543,7 @@ def bench_single(args, mname, N, cb):
         "exchanges_per_s": round(N / t_step, 1),
         "config": {"workload": args.config, "keys": len(sizes), "E": E, "E_padded": Ep,
                    "workers": N, "chunk_bytes": cb, "seg": args.seg, "minb": args.minb,
-                   "grid": args.grid, "tile_elems": args.tile_elems,
+                   "grid": args.grid, "tile_elems": args.tile_elems, "oneshot": args.oneshot,
                    "mode": "M1 (1 GPU, pushes resident, "
                    "zero-copy BORROW)", "kernel": kname, "cache": args.cache,
                    "l2": f"no flush: inputs exceed L2 ({(4 * N + 16) * E / 1e9:.2f} GB/round "
@@ -577,9 +598,13 @@ def bench_graph(hub, grads, N, E, stream, steps, rounds_per_graph=20):
 
 
 def bench_e2e(hub, grads, N, E, Ep, stream, steps):
-    """Same metric through the public C ABI with pinned HOST buffers: every step
-    copies the N pushes host->device (PHUB_COPY) and pulls the model back to the
-    host for each worker (PHUB_ALL_KEYS pull), all inside the timed region."""
+    """Same metric through the public C ABI with pinned HOST buffers: every round
+    copies the N pushes host->device (PHUB_COPY), runs the kernel, and pulls
+    the model back to the host once per worker (PHUB_ALL_KEYS pull) -- all
+    inside the timed region.  Rounds are pipelined on three streams: the H2D
+    pushes of round k+1 (receive slot (k+1) % 2) overlap the D2H pulls of
+    round k on the full-duplex PCIe link; each kernel waits for its pushes and
+    for the previous round's pulls (it overwrites w)."""
     import torch
     host_g = []
     for w in range(N):
@@ -588,29 +613,49 @@ def bench_e2e(hub, grads, N, E, Ep, stream, steps):
         host_g.append(h)
     host_w = torch.empty(Ep, dtype=torch.float32, pin_memory=True)
     torch.cuda.synchronize()
+    s_in, s_c, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    total = steps + 1
 
-    def step():
-        for w in range(N):
-            hub.push(w, host_g[w], mode="copy")
-        hub.aggregate_optimize()
-        for w in range(N):
-            hub.pull(host_w)
+    def ev():
+        return torch.cuda.Event(enable_timing=False)
 
-    step()
+    ev_in = [ev() for _ in range(total)]
+    ev_c = [ev() for _ in range(total)]
+    ev_out = [ev() for _ in range(total)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def round_(k):
+        if k >= 2:
+            s_in.wait_event(ev_c[k - 2])           # receive slot k % 2 is free again
+        for w in range(N):
+            hub.push(w, host_g[w], mode="copy", stream=s_in)
+        ev_in[k].record(s_in)
+        s_c.wait_event(ev_in[k])
+        if k >= 1:
+            s_c.wait_event(ev_out[k - 1])          # previous pulls have read w
+        hub.aggregate_optimize(stream=s_c)
+        ev_c[k].record(s_c)
+        s_out.wait_event(ev_c[k])
+        for w in range(N):
+            hub.pull(host_w, stream=s_out)
+        ev_out[k].record(s_out)
+
+    round_(0)                                      # warm-up round
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(steps):
-        step()
-    b.record(stream)
+    t0.record(s_in)
+    s_c.wait_event(t0)
+    s_out.wait_event(t0)
+    for k in range(1, total):
+        round_(k)
+    t1.record(s_out)
     torch.cuda.synchronize()
-    t = a.elapsed_time(b) / 1e3 / steps
+    t = t0.elapsed_time(t1) / 1e3 / steps
     del host_g, host_w
     return {"value": round(N * 4 * E / t / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": N * 4 * Ep, "d2h_bytes_per_step": N * 4 * Ep,
             "steps": steps, "ms_per_step": round(t * 1e3, 3),
             "path": "phub_push(PHUB_COPY, pinned host) x N -> phub_aggregate_optimize -> "
-                    "phub_pull(host) x N"}
+                    "phub_pull(host) x N; rounds pipelined on 3 streams (H2D of k+1 || D2H of k)"}
 
 
 if __name__ == "__main__":

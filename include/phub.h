@@ -129,7 +129,11 @@ phub_status phub_destroy(phub_ctx ctx);
  *     valid and unmodified until that aggregate has completed on its stream.
  *   mode PHUB_COPY: the data (host or device memory) is copied into the
  *     context's receive arena on `stream`; the caller may reuse `grad` once
- *     the copy has completed on `stream`.
+ *     the copy has completed on `stream`.  The arena has two slots (iteration
+ *     i uses slot i % 2, 2 x N x E_padded floats, allocated on the first COPY
+ *     push), so iteration i+1's copies may run on another stream while
+ *     iteration i's kernel runs; the caller orders the streams (the copies of
+ *     i+1 must not start before the kernel of i-1 has finished).
  * Errors: BAD_WORKER, BAD_KEY, LENGTH_MISMATCH, DUPLICATE_PUSH (this
  * (worker, key) already pushed in this iteration), INVALID_ARGUMENT. */
 phub_status phub_push(phub_ctx ctx, int32_t worker, int32_t key, const float* grad,
@@ -261,8 +265,11 @@ enum {
     PHUB_OPT_CACHE = 4,       /* PHUB_CACHE_*: L2 policy of the pulled weights   */
     PHUB_OPT_FLAT_SEG = 5,    /* flat kernels: 0 = grid-stride, else CTA-contiguous      */
                               /* segments of this many vectors                           */
-    PHUB_OPT_FLAT_MINB = 6    /* tuning: 0 = default build; 1,2,4,6,8 = N=8 256-bit flat */
+    PHUB_OPT_FLAT_MINB = 6,   /* tuning: 0 = default build; 1,2,4,6,8 = N=8 256-bit flat */
                               /* kernel compiled for that many resident CTAs per SM      */
+    PHUB_OPT_FLAT_ONESHOT = 7 /* flat kernels: 1 = one vector per thread, grid covering  */
+                              /* the range (hardware CTA scheduler balances); 0 = the    */
+                              /* persistent grid (SMs x resident CTAs)                   */
 };
 enum {
     PHUB_KERNEL_AUTO = 0,     /* flat 256-bit kernel when eligible, else chunk tiles     */

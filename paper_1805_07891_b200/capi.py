@@ -28,7 +28,7 @@ PHUB_OWNED_RANGE = -2
 PHUB_COPY, PHUB_BORROW = 0, 1
 PHUB_OWNER_LPT, PHUB_OWNER_CONTIG = 0, 1
 PHUB_OPT_KERNEL, PHUB_OPT_GRID, PHUB_OPT_TILE_ELEMS, PHUB_OPT_CACHE = 1, 2, 3, 4
-PHUB_OPT_FLAT_SEG, PHUB_OPT_FLAT_MINB = 5, 6
+PHUB_OPT_FLAT_SEG, PHUB_OPT_FLAT_MINB, PHUB_OPT_FLAT_ONESHOT = 5, 6, 7
 (PHUB_KERNEL_AUTO, PHUB_KERNEL_FLAT, PHUB_KERNEL_TILES, PHUB_KERNEL_FLAT128,
  PHUB_KERNEL_WIDE, PHUB_KERNEL_BULK) = range(6)
 PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS = 0, 1

@@ -85,6 +85,7 @@ struct phub_ctx_s {
     int grid_override = 0;
     uint64_t flat_seg = 0;
     int flat_minb = 0;
+    int flat_oneshot = 0;
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     uint64_t iteration = 0;
@@ -500,16 +501,18 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
                        : reinterpret_cast<uintptr_t>(grad) - 4 * c->key_off[k];
     } else {
         if (!c->d_recv) {
-            cudaError_t e = cudaMalloc(&c->d_recv, sizeof(float) * c->E_pad * c->N);
+            // two slots: iteration i lands in slot i % 2, so the copies of
+            // iteration i+1 may overlap the kernel of iteration i
+            cudaError_t e = cudaMalloc(&c->d_recv, sizeof(float) * c->E_pad * c->N * 2);
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 c->d_recv = nullptr;
                 return c->fail(PHUB_ERR_OUT_OF_MEMORY, "receive arena: %s", cudaGetErrorString(e));
             }
-            if ((e = cudaMemset(c->d_recv, 0, sizeof(float) * c->E_pad * c->N)) != cudaSuccess)
+            if ((e = cudaMemset(c->d_recv, 0, sizeof(float) * c->E_pad * c->N * 2)) != cudaSuccess)
                 return c->cuda_fail(e, "cudaMemset(recv)");
         }
-        float* slot = c->d_recv + (uint64_t)worker * c->E_pad;
+        float* slot = c->d_recv + ((c->iteration & 1) * (uint64_t)c->N + worker) * c->E_pad;
         cudaError_t e = cudaSuccess;
         if (ranged) {
             if (n) e = cudaMemcpyAsync(slot + rb, grad, n * sizeof(float), cudaMemcpyDefault, s);
@@ -693,9 +696,11 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
         for (int r = 0; r < a.nrep; ++r) a.rep[r] = c->replicas[r];
         const int vec = variant == PHUB_KERNEL_FLAT ? 8 : 4;
         const uint64_t nvec = (eend - b) / vec;
-        int grid = c->grid_override ? c->grid_override : c->flat_grid[vec == 8][c->keep_agg];
-        grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, (nvec + phub::kThreads - 1) /
-                                                                      phub::kThreads));
+        const uint64_t cover = (nvec + phub::kThreads - 1) / phub::kThreads;
+        int grid = c->grid_override ? c->grid_override
+                   : c->flat_oneshot ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
+                                     : c->flat_grid[vec == 8][c->keep_agg];
+        grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, cover));
         a.seg = c->flat_seg;
         if (variant == PHUB_KERNEL_BULK)
             e = phub::launch_bulk(a, c->grid_override ? c->grid_override : c->num_sms, s,
@@ -976,6 +981,10 @@ phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
         case PHUB_OPT_FLAT_SEG:
             if (value < 0) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "segment must be >= 0");
             c->flat_seg = (uint64_t)value;
+            return PHUB_OK;
+        case PHUB_OPT_FLAT_ONESHOT:
+            if (value != 0 && value != 1) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "0 or 1");
+            c->flat_oneshot = (int)value;
             return PHUB_OK;
         case PHUB_OPT_FLAT_MINB:
             if (!(value == 0 || value == 1 || value == 2 || value == 4 || value == 6 || value == 8))

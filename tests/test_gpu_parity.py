@@ -542,3 +542,41 @@ def test_streaming_then_aggregate_rest():
     w2, _, _ = hub.read_state()
     rw2, _, _ = oracle.round_(sizes, hg, rw, rv, 0.1, 0.9)
     assert_bits_equal(w2, rw2, "w after next round")
+
+
+def test_copy_push_two_slots_pipelined():
+    """COPY pushes alternate between two receive slots, so round k+1's H2D
+    copies may overlap round k's kernel (the bench's e2e pipeline)."""
+    sizes = SMALL
+    N = 3
+    hub = _hub(sizes, N)
+    w, v = host_state(hub.E, 7)
+    hub.load_state(w, v)
+    pidx = hub.padded_index()
+    s_in, s_c = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_c = []
+    host = []
+    for r in range(4):
+        hg = host_grads(hub.E, N, 10 + r)
+        bufs = []
+        for g in hg:
+            h = torch.full((hub.E_padded,), float("nan"), pin_memory=True)
+            h.numpy()[pidx] = g
+            bufs.append(h)
+        host.append(bufs)
+        if r >= 2:
+            s_in.wait_event(ev_c[r - 2])
+        for k, h in enumerate(bufs):
+            hub.push(k, h, mode="copy", stream=s_in)
+        e_in = torch.cuda.Event()
+        e_in.record(s_in)
+        s_c.wait_event(e_in)
+        hub.aggregate_optimize(stream=s_c)
+        e = torch.cuda.Event()
+        e.record(s_c)
+        ev_c.append(e)
+        w, v, _ = oracle.round_(sizes, hg, w, v, 0.1, 0.9)
+    torch.cuda.synchronize()
+    gw, gv, _ = hub.read_state()
+    assert_bits_equal(gw, w, "w after 4 pipelined COPY rounds")
+    assert_bits_equal(gv, v, "v after 4 pipelined COPY rounds")
