@@ -267,9 +267,10 @@ enum {
                               /* segments of this many vectors                           */
     PHUB_OPT_FLAT_MINB = 6,   /* tuning: 0 = default build; 1,2,4,6,8 = N=8 256-bit flat */
                               /* kernel compiled for that many resident CTAs per SM      */
-    PHUB_OPT_FLAT_ONESHOT = 7 /* flat kernels: 1 = one vector per thread, grid covering  */
-                              /* the range (hardware CTA scheduler balances); 0 = the    */
-                              /* persistent grid (SMs x resident CTAs)                   */
+    PHUB_OPT_FLAT_ONESHOT = 7 /* flat kernels: 1 (default) = one vector per thread, grid */
+                              /* covering the range (the hardware CTA scheduler balances */
+                              /* like PHub's chunk -> core map); 0 = persistent grid     */
+                              /* (SMs x resident CTAs, grid-stride)                      */
 };
 enum {
     PHUB_KERNEL_AUTO = 0,     /* flat 256-bit kernel when eligible, else chunk tiles     */

@@ -85,7 +85,7 @@ struct phub_ctx_s {
     int grid_override = 0;
     uint64_t flat_seg = 0;
     int flat_minb = 0;
-    int flat_oneshot = 0;
+    int flat_oneshot = 1;             // measured best: one vector per thread (profiles/r01_tune)
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     uint64_t iteration = 0;
