@@ -265,7 +265,14 @@ def bench_multi(args, mname, N, cb):
     p2p = args.mode == "p2p"
     ar = args.mode == "allreduce"
     cls = {"p2p": P2PShardedPHub, "nccl": ShardedPHub, "allreduce": AllReduceBaseline}[args.mode]
-    sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
+    try:
+        sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
+    except Exception as e:  # noqa: BLE001 -- every rank raises together (see sharded.py)
+        if not p2p:
+            raise
+        print(f"[bench] p2p exchange unavailable ({e}); using the NCCL exchange", file=sys.stderr)
+        args.mode, p2p = "nccl", False
+        sh = ShardedPHub(sizes, N, chunk_size_bytes=cb, device=local)
     hub, plan = sh.hub, sh.plan
     from paper_1805_07891_b200 import capi
     if args.grid:

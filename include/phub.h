@@ -122,6 +122,8 @@ phub_status phub_destroy(phub_ctx ctx);
  *   key == PHUB_OWNED_RANGE (CONTIG ownership or G == 1): `grad` holds
  *     n == end - begin elements, the padded range phub_owner_range() gives
  *     for this context's rank -- what an owner receives from a remote worker.
+ *     If that range is empty (an owner with no chunk) n == 0 and `grad`
+ *     may be NULL.
  *   key in [0, num_keys): `grad` holds n == n_k contiguous elements.
  *   mode PHUB_BORROW: zero copy -- the pointer is recorded and read by
  *     the next phub_aggregate_optimize.  `grad` must be device memory
@@ -267,10 +269,12 @@ enum {
                               /* segments of this many vectors                           */
     PHUB_OPT_FLAT_MINB = 6,   /* tuning: 0 = default build; 1,2,4,6,8 = N=8 256-bit flat */
                               /* kernel compiled for that many resident CTAs per SM      */
-    PHUB_OPT_FLAT_ONESHOT = 7 /* flat kernels: 1 (default) = one vector per thread, grid */
-                              /* covering the range (the hardware CTA scheduler balances */
-                              /* like PHub's chunk -> core map); 0 = persistent grid     */
-                              /* (SMs x resident CTAs, grid-stride)                      */
+    PHUB_OPT_FLAT_ONESHOT = 7 /* flat kernels: 1 = one vector per thread, grid covering */
+                              /* the range (the hardware CTA scheduler balances like     */
+                              /* PHub's chunk -> core map); 0 = persistent grid (SMs x   */
+                              /* resident CTAs, grid-stride); -1 (default) = one-shot    */
+                              /* unless peer replicas are registered (NVLink latency     */
+                              /* favours the persistent grid)                            */
 };
 enum {
     PHUB_KERNEL_AUTO = 0,     /* flat 256-bit kernel when eligible, else chunk tiles     */

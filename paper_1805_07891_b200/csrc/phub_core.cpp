@@ -85,7 +85,9 @@ struct phub_ctx_s {
     int grid_override = 0;
     uint64_t flat_seg = 0;
     int flat_minb = 0;
-    int flat_oneshot = 1;             // measured best: one vector per thread (profiles/r01_tune)
+    int flat_oneshot = -1;            // -1 auto: one-shot for local HBM streams (profiles/
+                                      // r01_tune2), persistent grid when peer replicas are
+                                      // registered (NVLink latency; profiles/r01_multi2)
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     uint64_t iteration = 0;
@@ -478,7 +480,7 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
     if (n != want)
         return c->fail(PHUB_ERR_LENGTH_MISMATCH, "push length %llu != %llu (S:172)",
                        (unsigned long long)n, (unsigned long long)want);
-    if (!grad) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "grad is NULL");
+    if (!grad && n) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "grad is NULL");
     if (mode != PHUB_COPY && mode != PHUB_BORROW)
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "mode must be PHUB_COPY or PHUB_BORROW");
     const int k0 = all ? 0 : key, k1 = all ? c->K : key + 1;
@@ -488,7 +490,9 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
                            "worker %d already pushed key %d this iteration (S:176)", worker, k);
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (mode == PHUB_BORROW) {
+    if (mode == PHUB_BORROW && n == 0) {
+        // an empty owned range: nothing will be read (the owner has no chunk)
+    } else if (mode == PHUB_BORROW) {
         if (!is_device_ptr(grad))
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW needs device memory");
         if (reinterpret_cast<uintptr_t>(grad) % 16 != 0)
@@ -698,7 +702,8 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
         const uint64_t nvec = (eend - b) / vec;
         const uint64_t cover = (nvec + phub::kThreads - 1) / phub::kThreads;
         int grid = c->grid_override ? c->grid_override
-                   : c->flat_oneshot ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
+                   : (c->flat_oneshot > 0 || (c->flat_oneshot < 0 && c->replicas.empty()))
+                         ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
                                      : c->flat_grid[vec == 8][c->keep_agg];
         grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, cover));
         a.seg = c->flat_seg;
@@ -983,7 +988,7 @@ phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
             c->flat_seg = (uint64_t)value;
             return PHUB_OK;
         case PHUB_OPT_FLAT_ONESHOT:
-            if (value != 0 && value != 1) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "0 or 1");
+            if (value < -1 || value > 1) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "-1, 0 or 1");
             c->flat_oneshot = (int)value;
             return PHUB_OK;
         case PHUB_OPT_FLAT_MINB:

@@ -174,6 +174,10 @@ class ShardedPHub:
         self.hub.close()
 
 
+class PeerMappingError(RuntimeError):
+    """CUDA IPC peer mapping is unavailable on at least one rank (all ranks raise)."""
+
+
 class P2PShardedPHub:
     """Peer-memory form of the sharded exchange: ONE kernel
     per round on each owner reads its workers' slices straight out of the
@@ -212,13 +216,31 @@ class P2PShardedPHub:
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         self._peer_grad, self._peer_w = {}, []
-        for r, hs, wh in sorted(allh, key=lambda x: x[0]):
-            if r == rank:
-                continue
-            for w, h in hs.items():
-                self._peer_grad[w] = capi.phub_ipc_open(dev, h)
-            self._peer_w.append(capi.phub_ipc_open(dev, wh))
-        capi.phub_set_replicas(self.hub.ctx, self._peer_w)
+        err = None
+        try:
+            for r, hs, wh in sorted(allh, key=lambda x: x[0]):
+                if r == rank:
+                    continue
+                for w, h in hs.items():
+                    self._peer_grad[w] = capi.phub_ipc_open(dev, h)
+                self._peer_w.append(capi.phub_ipc_open(dev, wh))
+            capi.phub_set_replicas(self.hub.ctx, self._peer_w)
+        except capi.PhubError as e:
+            err = e
+        # every rank must agree before anyone relies on peer mappings
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=f"cuda:{dev}")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            for p in list(self._peer_grad.values()) + self._peer_w:
+                try:
+                    capi.phub_ipc_close(dev, p)
+                except capi.PhubError:
+                    pass
+            self._grads = {}
+            for p in self._own.values():
+                capi.phub_free_shared(dev, p)
+            self.hub.close()
+            raise PeerMappingError(f"peer mapping failed on some rank ({err or 'other rank'})")
         self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
         self.replica = self.hub.weights()
         torch.cuda.synchronize(dev)
