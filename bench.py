@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
-    ap.add_argument("--mode", default="p2p", choices=["p2p", "nccl", "allreduce"],
+    ap.add_argument("--pieces", type=int, default=8, help="chain mode pipeline pieces")
+    ap.add_argument("--mode", default="auto", choices=["auto", "p2p", "chain", "nccl", "allreduce"],
                     help="N>1 exchange: fused peer-memory kernel (p2p) or NCCL send/recv")
     return ap.parse_args()
 
@@ -278,7 +279,8 @@ def bench_multi(args, mname, N, cb):
     mode nccl: NCCL grouped send/recv push, fused kernel, NCCL all-gather-v pull."""
     import torch
     import torch.distributed as dist
-    from paper_1805_07891_b200.sharded import AllReduceBaseline, P2PShardedPHub, ShardedPHub
+    from paper_1805_07891_b200.sharded import (AllReduceBaseline, ChainShardedPHub,
+                                               P2PShardedPHub, ShardedPHub)
     from workloads import grad_stream, manifest
     from workloads.generate import values_torch
 
@@ -288,16 +290,23 @@ def bench_multi(args, mname, N, cb):
     dist.init_process_group("nccl", device_id=dev)
     rank, G = dist.get_rank(), dist.get_world_size()
     sizes = manifest(mname)
-    p2p = args.mode == "p2p"
+    if args.mode == "auto":      # fewest NVLink bytes: chain at G = 2, owner-sharded P2P above
+        args.mode = "chain" if G == 2 else "p2p"
+    chain = args.mode == "chain"
+    p2p = args.mode in ("p2p", "chain")
     ar = args.mode == "allreduce"
-    cls = {"p2p": P2PShardedPHub, "nccl": ShardedPHub, "allreduce": AllReduceBaseline}[args.mode]
     try:
-        sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
+        if chain:
+            sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces)
+        else:
+            cls = {"p2p": P2PShardedPHub, "nccl": ShardedPHub,
+                   "allreduce": AllReduceBaseline}[args.mode]
+            sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
     except Exception as e:  # noqa: BLE001 -- every rank raises together (see sharded.py)
         if not p2p:
             raise
         print(f"[bench] p2p exchange unavailable ({e}); using the NCCL exchange", file=sys.stderr)
-        args.mode, p2p = "nccl", False
+        args.mode, p2p, chain = "nccl", False, False
         sh = ShardedPHub(sizes, N, chunk_size_bytes=cb, device=local)
     hub, plan = sh.hub, sh.plan
     from paper_1805_07891_b200 import capi
@@ -330,6 +339,13 @@ def bench_multi(args, mname, N, cb):
     stream = torch.cuda.current_stream(dev)
 
     def one(i=None):
+        if chain:                      # the whole round is phases of fused kernels + barriers
+            if i is not None:
+                ev[i][0].record(stream)
+            sh.exchange()
+            if i is not None:
+                ev[i][1].record(stream)
+            return
         if ar:
             hosted = sh.hosted
             sh.sum.copy_(grads[hosted[0]])
@@ -376,6 +392,9 @@ def bench_multi(args, mname, N, cb):
             "k_ms": sum(a.elapsed_time(b) for a, b in ev) / args.steps,
             "owned": hub.owned_elements(), "out": plan.nvlink_bytes_out(),
             "in": plan.nvlink_bytes_in(), "launches": launches, "clocks": clocks.summary()}
+    if chain:   # one partial per link per round; the last rank stores w' into G-1 replicas
+        mine["out"] = 4 * Ep * ((G - 1) if rank == G - 1 else 1)
+        mine["in"] = 4 * Ep * ((1 if rank > 0 else 0) + (1 if rank < G - 1 else 0))
     allr = [None] * G
     dist.all_gather_object(allr, mine)
 
@@ -430,7 +449,10 @@ def bench_multi(args, mname, N, cb):
             "exchanges_per_s": round(N / t_step, 1),
             "config": {"workload": args.config, "keys": len(sizes), "E": E, "E_padded": Ep,
                        "workers": N, "workers_per_gpu": N // G, "chunk_bytes": cb,
-                       "mode": ("M3 (full exchange) p2p: one fused kernel per owner reads peer "
+                       "mode": (f"M3 (full exchange) chain: rank-ordered partial sums over "
+                                f"NVLink, last rank fused Nesterov + replica stores, pipelined "
+                                f"over {args.pieces} pieces") if chain else
+                               ("M3 (full exchange) p2p: one fused kernel per owner reads peer "
                                 "gradients + writes peer replicas over NVLink, NCCL barrier "
                                 "before/after") if p2p else
                                ("BASELINE (not exact, NEXT-3): local torch sum of hosted workers, "
@@ -448,8 +470,10 @@ def bench_multi(args, mname, N, cb):
                           "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                           "frac": round(nv_bytes / (k_ms / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
                           "traffic": None,
-                          "kernel": "fused exchange kernel (k_flat with peer loads/stores), "
-                                    "slowest owner", "kernel_ms": round(k_ms, 4),
+                          "kernel": ("chained exchange round (partial-sum + fused kernels, "
+                                     "incl. barriers)") if chain else
+                                    ("fused exchange kernel (k_flat with peer loads/stores), "
+                                     "slowest owner"), "kernel_ms": round(k_ms, 4),
                           "bytes_per_launch_max_dir": nv_bytes,
                           "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per "
                                          "direction"} if p2p else

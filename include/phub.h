@@ -237,6 +237,25 @@ phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
  * and after phub_aggregate_optimize); the library never spins on peers.
  * ------------------------------------------------------------------------- */
 
+/* Chained exchange (workers hosted in rank order): the
+ * worker-order partial sum of `count` (<= 64) padded-layout sources over
+ * [begin, end), stored into `dst` (padded layout; typically a peer-mapped
+ * buffer of the next rank):  dst[i] = ((+0 + src0[i]) + src1[i]) + ...
+ * Because the sum starts from +0 and adds in order, chaining partials rank
+ * by rank reproduces the global worker-order sum bit for bit (reading R3).
+ * All pointers 32-B aligned device memory; begin, end multiples of 8.
+ * Uses ctx's device; no receipts are involved. */
+phub_status phub_partial_sum(phub_ctx ctx, const float* const* srcs, int32_t count, float* dst,
+                             uint64_t begin, uint64_t end, void* stream);
+
+/* Range-wise aggregation of one iteration (pipelined exchange): requires all
+ * N x K pushes, whole-model / owned-range pushes under CONTIG ownership;
+ * runs the fused kernel on the owned elements of [begin, end).  Calls must
+ * cover the owned range in increasing, abutting order starting at its begin
+ * (begin == previous end); the call that reaches the owned range's end
+ * completes the iteration.  begin/end multiples of 8 (or the range bounds). */
+phub_status phub_aggregate_range(phub_ctx ctx, uint64_t begin, uint64_t end, void* stream);
+
 /* Every later phub_aggregate_optimize also stores w' of the owned range into
  * replicas[0..count) (padded layout, E_padded elements each; device pointers,
  * typically peer-mapped with phub_ipc_open).  count == 0 clears.  count <= 16.

@@ -69,6 +69,9 @@ _SIGS = {
                             C.c_void_p]),
     "phub_aggregate_optimize": (C.c_int, [phub_ctx, C.c_void_p]),
     "phub_aggregate_ready": (C.c_int, [phub_ctx, C.c_void_p, _u64p]),
+    "phub_aggregate_range": (C.c_int, [phub_ctx, C.c_uint64, C.c_uint64, C.c_void_p]),
+    "phub_partial_sum": (C.c_int, [phub_ctx, C.POINTER(C.c_void_p), C.c_int32, C.c_void_p,
+                                   C.c_uint64, C.c_uint64, C.c_void_p]),
     "phub_pull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
     "phub_pushpull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32,
                                 C.c_void_p, C.c_void_p]),
@@ -157,6 +160,16 @@ def phub_aggregate_ready(ctx, stream: int = 0) -> int:
     n = C.c_uint64()
     _check(_lib.phub_aggregate_ready(ctx, stream, C.byref(n)), "phub_aggregate_ready", ctx)
     return int(n.value)
+
+
+def phub_aggregate_range(ctx, begin: int, end: int, stream: int = 0):
+    _check(_lib.phub_aggregate_range(ctx, begin, end, stream), "phub_aggregate_range", ctx)
+
+
+def phub_partial_sum(ctx, srcs, dst: int, begin: int, end: int, stream: int = 0):
+    arr = (C.c_void_p * max(len(srcs), 1))(*srcs)
+    _check(_lib.phub_partial_sum(ctx, arr, len(srcs), dst, begin, end, stream),
+           "phub_partial_sum", ctx)
 
 
 def phub_pull(ctx, key: int, dst_ptr: int, n: int, stream: int = 0):

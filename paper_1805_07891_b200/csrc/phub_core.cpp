@@ -79,6 +79,7 @@ struct phub_ctx_s {
     std::vector<uintptr_t> base_uploaded;
     uintptr_t* d_base = nullptr;
     std::vector<float*> replicas;     // peer weight replicas written by the kernel
+    uint64_t range_cursor = UINT64_MAX;   // phub_aggregate_range progress (UINT64_MAX: none)
 
     // options + counters
     int kernel = PHUB_KERNEL_AUTO;
@@ -601,6 +602,8 @@ static void end_iteration(phub_ctx c) {
 phub_status phub_aggregate_ready(phub_ctx c, void* stream, uint64_t* keys_done) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
     if (c->failed) return PHUB_ERR_CUDA;
+    if (c->range_cursor != UINT64_MAX)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "iteration is being aggregated by ranges");
     if (!c->replicas.empty())
         return c->fail(PHUB_ERR_UNSUPPORTED, "streaming aggregation does not store replicas");
     DeviceGuard g(c->device);
@@ -625,6 +628,100 @@ phub_status phub_aggregate_ready(phub_ctx c, void* stream, uint64_t* keys_done) 
     c->done_count += n;
     if (keys_done) *keys_done = n;
     if (c->done_count == (uint64_t)c->K) end_iteration(c);
+    return PHUB_OK;
+}
+
+phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count, float* dst,
+                             uint64_t begin, uint64_t end, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    if (count < 1 || count > phub::kMaxWorkers || !srcs || !dst)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "need 1..%d sources and a destination",
+                       phub::kMaxWorkers);
+    if (end < begin || end > c->E_pad || begin % 8 || (end % 8 && end != c->E_pad))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "range must lie in [0, E_padded), 8-aligned");
+    if (reinterpret_cast<uintptr_t>(dst) % 32)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "dst must be 32-B aligned");
+    phub::FlatArgs a{};
+    for (int k = 0; k < count; ++k) {
+        if (!srcs[k] || reinterpret_cast<uintptr_t>(srcs[k]) % 32)
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "source %d NULL or not 32-B aligned", k);
+        a.g[k] = srcs[k];
+    }
+    a.nw = count;
+    a.begin = begin;
+    a.end = end;
+    DeviceGuard g(c->device);
+    c->launches = 0;
+    const uint64_t nvec = (end - begin) / 8;
+    const int grid = (int)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)c->flat_grid[1][0], (nvec + phub::kThreads - 1) / phub::kThreads));
+    cudaError_t e = phub::launch_prefix(a, dst, grid, static_cast<cudaStream_t>(stream),
+                                        &c->launches);
+    c->launches_total += (uint64_t)c->launches;
+    if (e != cudaSuccess) return c->cuda_fail(e, "partial-sum launch");
+    return PHUB_OK;
+}
+
+phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    if (c->got_count != (uint64_t)c->K * c->N)
+        return c->fail(PHUB_ERR_INCOMPLETE, "%llu of %llu (worker,key) pushes received (S:181)",
+                       (unsigned long long)c->got_count,
+                       (unsigned long long)((uint64_t)c->K * c->N));
+    if (!contig_mode(c) || c->done_count)
+        return c->fail(PHUB_ERR_UNSUPPORTED, "range aggregation needs CONTIG ownership and no "
+                       "streamed keys in this iteration");
+    const uint64_t ob = c->own_begin[c->rank], oe = c->own_end[c->rank];
+    const uint64_t cur = c->range_cursor == UINT64_MAX ? ob : c->range_cursor;
+    const uint64_t b = std::max(begin, ob), e_ = std::min(end, oe);
+    if (begin > cur || end < begin || (e_ > b && (b % 8 || (e_ % 8 && e_ != oe))))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "ranges must abut in increasing order, 8-aligned");
+    bool flat = c->ce % 8 == 0 && c->N <= phub::kMaxWorkers;
+    for (int w = 0; flat && w < c->N; ++w) {
+        const uintptr_t b0 = c->base[(size_t)w * c->K];
+        for (int k = 1; k < c->K && flat; ++k) flat = c->base[(size_t)w * c->K + k] == b0;
+        flat = flat && b0 % 32 == 0;
+    }
+    if (!flat)
+        return c->fail(PHUB_ERR_UNSUPPORTED, "range aggregation needs whole-model / owned-range "
+                       "pushes, 32-B aligned");
+    DeviceGuard g(c->device);
+    c->launches = 0;
+    cudaError_t e = cudaSuccess;
+    const uint64_t lo = std::max(b, cur);
+    if (e_ > lo) {
+        phub::FlatArgs a{};
+        for (int w = 0; w < c->N; ++w) a.g[w] = reinterpret_cast<const float*>(c->base[(size_t)w * c->K]);
+        a.w = c->d_w;
+        a.v = c->d_v;
+        a.agg = c->keep_agg ? c->d_agg : nullptr;
+        a.begin = lo;
+        a.end = e_;
+        a.lr = c->lr;
+        a.mu = c->mu;
+        a.rescale = c->rescale;
+        a.nw = c->N;
+        a.nrep = (int)c->replicas.size();
+        for (int r = 0; r < a.nrep; ++r) a.rep[r] = c->replicas[r];
+        const uint64_t nvec = (e_ - lo) / 8;
+        const uint64_t cover = (nvec + phub::kThreads - 1) / phub::kThreads;
+        int grid = c->grid_override ? c->grid_override
+                   : (c->flat_oneshot > 0 || (c->flat_oneshot < 0 && c->replicas.empty()))
+                         ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
+                         : c->flat_grid[1][c->keep_agg];
+        grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, cover));
+        e = phub::launch_flat(a, 8, c->cache, grid, static_cast<cudaStream_t>(stream),
+                              &c->launches);
+    }
+    c->launches_total += (uint64_t)c->launches;
+    if (e != cudaSuccess) return c->cuda_fail(e, "kernel launch");
+    c->range_cursor = std::max(cur, std::min(std::max(end, cur), oe));
+    if (c->range_cursor >= oe) {
+        c->range_cursor = UINT64_MAX;
+        end_iteration(c);
+    }
     return PHUB_OK;
 }
 
@@ -683,6 +780,8 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
     }
     const uint64_t b = contig_mode(c) ? c->own_begin[c->rank] : 0;
     const uint64_t eend = contig_mode(c) ? c->own_end[c->rank] : 0;
+    if (c->range_cursor != UINT64_MAX)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "iteration is being aggregated by ranges");
     if (variant == PHUB_KERNEL_FLAT || variant == PHUB_KERNEL_FLAT128 ||
         variant == PHUB_KERNEL_BULK) {
         phub::FlatArgs a{};

@@ -277,6 +277,40 @@ __global__ void __launch_bounds__(kThreads) k_tiles(const __grid_constant__ Tile
     }
 }
 
+// ---------------------------------------------- partial (prefix) sum only
+// One stage of the chained exchange: the worker-order prefix of this rank's
+// workers (the first source may be the incoming partial of the previous
+// rank), stored -- typically over NVLink -- into the next rank's buffer.
+template <int NW>
+__global__ void __launch_bounds__(kThreads) k_prefix(const __grid_constant__ FlatArgs a,
+                                                     float* __restrict__ dst) {
+    const uint64_t n = (a.end - a.begin) / 8;
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+        const int nw = NW > 0 ? NW : a.nw;
+        for (int k0 = 0; k0 < nw; k0 += 8) {
+            V8 gv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < nw) gv[k] = ld_grad(reinterpret_cast<const V8*>(a.g[k0 + k] + a.begin) + i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < nw) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+                }
+        }
+        V8 out;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) out.x[j] = acc[j];
+        reinterpret_cast<V8*>(dst + a.begin)[i] = out;
+    }
+    __threadfence_system();
+}
+
 // ------------------------------------------------ bulk-copy (TMA) staging
 // Variant with the loads taken off the register file: one producer thread per
 // CTA streams each tile's N gradient slices and the w, v slices into a
@@ -549,6 +583,20 @@ cudaError_t launch_tiles(const TileArgs& a, int grid, cudaStream_t s, int* launc
     if (a.ntiles == 0) return cudaSuccess;
     TileFn fn = a.agg ? pick_tiles_nw<true>(a.nw) : pick_tiles_nw<false>(a.nw);
     fn<<<grid, kThreads, 0, s>>>(a);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches) {
+    if (a.end <= a.begin) return cudaSuccess;
+    switch (a.nw) {
+        case 1: k_prefix<1><<<grid, kThreads, 0, s>>>(a, dst); break;
+        case 2: k_prefix<2><<<grid, kThreads, 0, s>>>(a, dst); break;
+        case 3: k_prefix<3><<<grid, kThreads, 0, s>>>(a, dst); break;
+        case 4: k_prefix<4><<<grid, kThreads, 0, s>>>(a, dst); break;
+        case 5: k_prefix<5><<<grid, kThreads, 0, s>>>(a, dst); break;
+        default: k_prefix<0><<<grid, kThreads, 0, s>>>(a, dst); break;
+    }
     ++*launches;
     return cudaGetLastError();
 }

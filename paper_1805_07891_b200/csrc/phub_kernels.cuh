@@ -57,6 +57,9 @@ struct WideArgs {                     // ablation: wide aggregation
 cudaError_t launch_flat(const FlatArgs& a, int vec, int cache, int grid, cudaStream_t s,
                         int* launches);
 cudaError_t launch_tiles(const TileArgs& a, int grid, cudaStream_t s, int* launches);
+// Worker-order partial sum (no optimizer): dst[i] = ((+0 + g0[i]) + g1[i]) + ...
+// over [a.begin, a.end); dst may be a peer-mapped pointer (chained exchange).
+cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches);
 // TMA-style staging: 1-D bulk async copies into a shared-memory ring (nw <= 8).
 cudaError_t launch_bulk(const FlatArgs& a, int grid, cudaStream_t s, int* launches);
 size_t bulk_smem_bytes(int nw);

@@ -339,3 +339,140 @@ class AllReduceBaseline:
 
     def close(self):
         self.hub.close()
+
+
+class ChainShardedPHub:
+    """Chained exchange, pipelined over pieces.
+
+    Workers are hosted in rank order, so the worker-order sum can be built
+    rank by rank: rank p adds its hosted workers to the partial sum it
+    received from rank p-1 (phub_partial_sum) and stores the result straight
+    into rank p+1's buffer over NVLink; the last rank finishes the sum, runs
+    the fused Nesterov kernel on the whole model (phub_aggregate_range) and
+    stores w' into every replica.  Because every partial starts from +0 and
+    adds in order, the result is bit-identical to the one-GPU sum (R3, R4).
+
+    Each link carries one model-size partial per round (4E bytes) instead of
+    N/G gradient slices per owner -- fewer NVLink bytes than the sharded
+    exchange when G is small (G = 2: 4E vs 10E/4... see DESIGN.md 8).  The
+    model is split into `pieces`; in phase j rank p works on piece j - p, and
+    a stream-ordered NCCL barrier separates phases, so the ranks' kernels
+    overlap like a pipeline (no kernel ever waits on a peer).
+    """
+
+    def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
+                 device=None, group=None, pieces=8):
+        import torch
+        import torch.distributed as dist
+        from .phub import PHub, _CudaArray
+        self.group = group
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.rank, self.world = rank, world
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        dev = self.device
+        self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, rank, world)
+        self.last = rank == world - 1
+        per = num_workers // world
+        if self.last:      # the finishing rank: incoming partial + its own workers
+            nw = per + (1 if world > 1 else 0)
+            self.hub = PHub(key_sizes, nw, chunk_size_bytes=chunk_size_bytes, lr=lr,
+                            momentum=momentum, rescale=1.0 / num_workers, device=dev)
+        else:              # a summing rank: its context is used for partial sums + its replica
+            self.hub = PHub(key_sizes, per, chunk_size_bytes=chunk_size_bytes, lr=lr,
+                            momentum=momentum, device=dev)
+        Ep = self.hub.E_padded
+        self._own = {w: capi.phub_alloc_shared(dev, 4 * Ep) for w in self.plan.hosted()}
+        self._grads = {w: torch.as_tensor(_CudaArray(p, Ep, self), device=f"cuda:{dev}")
+                       for w, p in self._own.items()}
+        for t in self._grads.values():
+            t.zero_()
+        self._pin = capi.phub_alloc_shared(dev, 4 * Ep) if rank > 0 else None
+        mine = (rank, capi.phub_ipc_get_handle(dev, self._pin) if self._pin else None,
+                capi.phub_ipc_get_handle(dev, self.hub.weights_ptr()))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        allh.sort(key=lambda x: x[0])
+        self._opened = []
+        self._next_in = None
+        if not self.last:
+            self._next_in = capi.phub_ipc_open(dev, allh[rank + 1][1])
+            self._opened.append(self._next_in)
+        else:
+            reps = []
+            for r, _pin, wh in allh:
+                if r != rank:
+                    reps.append(capi.phub_ipc_open(dev, wh))
+            self._opened += reps
+            capi.phub_set_replicas(self.hub.ctx, reps)
+        # piece boundaries: multiples of 64 elements (256 B)
+        k = max(1, int(pieces))
+        step = -(-Ep // k)
+        step = -(-step // 64) * 64
+        self.pieces = [(b, min(Ep, b + step)) for b in range(0, Ep, step)]
+        self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
+        self.replica = self.hub.weights()
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+    @property
+    def hosted(self):
+        return self.plan.hosted()
+
+    def gradients(self) -> dict:
+        return self._grads
+
+    def barrier(self):
+        import torch.distributed as dist
+        dist.all_reduce(self._flag, group=self.group)
+
+    def exchange(self):
+        Ep = self.hub.E_padded
+        hosted = self.hosted
+        self.barrier()                       # gradients of this round are in place everywhere
+        if self.last:
+            w0 = 0
+            if self.world > 1:
+                self.hub.push(0, self._pin, mode="borrow", n=Ep)
+                w0 = 1
+            for i, w in enumerate(hosted):
+                self.hub.push(w0 + i, self._own[w], mode="borrow", n=Ep)
+        srcs = ([self._pin] if self._pin else []) + [self._own[w] for w in hosted]
+        stream = self.hub._stream(None)
+        K = len(self.pieces)
+        for j in range(K + self.world - 1):
+            p = j - self.rank
+            if 0 <= p < K:
+                b, e = self.pieces[p]
+                if self.last:
+                    capi.phub_aggregate_range(self.hub.ctx, b, e, stream)
+                else:
+                    capi.phub_partial_sum(self.hub.ctx, srcs, self._next_in, b, e, stream)
+            self.barrier()                   # piece p is complete before the next rank reads it
+
+    def exchange_host(self, host_grads: dict, host_out: dict):
+        for w in self.hosted:
+            self._grads[w].copy_(host_grads[w], non_blocking=True)
+        self.exchange()
+        for w in self.hosted:
+            host_out[w].copy_(self.replica, non_blocking=True)
+
+    def weights(self):
+        return self.replica
+
+    def close(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        if self.last:
+            capi.phub_set_replicas(self.hub.ctx, [])
+        for p in self._opened:
+            capi.phub_ipc_close(self.device, p)
+        dist.barrier(group=self.group)
+        self._grads = {}
+        for p in self._own.values():
+            capi.phub_free_shared(self.device, p)
+        if self._pin:
+            capi.phub_free_shared(self.device, self._pin)
+        self._own = {}
+        self.hub.close()

@@ -15,7 +15,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
-from paper_1805_07891_b200.sharded import P2PShardedPHub, ShardedPHub  # noqa: E402
+from paper_1805_07891_b200.sharded import (  # noqa: E402
+    ChainShardedPHub, P2PShardedPHub, ShardedPHub)
 from workloads import grad_stream, manifest, values_np  # noqa: E402
 from workloads.generate import values_torch  # noqa: E402
 
@@ -31,19 +32,23 @@ def main():
     special = {"small": [3, 3, 9408, 64, 64, 4096, 20000, 1000, 7], "one": [5]}
     sizes = special[name] if name in special else manifest(name)
     E = sum(sizes)
-    cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
-    sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
+    if mode == "chain":
+        sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=3)
+    else:
+        cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
+        sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
+    fused = mode in ("p2p", "chain")
     w_ref, v_ref = values_np(1, 0, E, 20), values_np(2, 0, E, 25)
     sh.hub.load_state(w_ref, v_ref)
     idx = torch.as_tensor(sh.hub.padded_index(), device=dev)
     for r in range(rounds):
-        grads = sh.gradients() if mode == "p2p" else {}
+        grads = sh.gradients() if fused else {}
         for w in sh.hosted:
-            b = grads[w] if mode == "p2p" else torch.empty(sh.hub.E_padded, device=dev)
+            b = grads[w] if fused else torch.empty(sh.hub.E_padded, device=dev)
             b.fill_(float("nan"))
             b[idx] = values_torch(grad_stream(w) + 37 * r, 0, E, 25, dev)
             grads[w] = b
-        if mode == "p2p":
+        if fused:
             sh.exchange()
         else:
             sh.exchange(grads)

@@ -580,3 +580,56 @@ def test_copy_push_two_slots_pipelined():
     gw, gv, _ = hub.read_state()
     assert_bits_equal(gw, w, "w after 4 pipelined COPY rounds")
     assert_bits_equal(gv, v, "v after 4 pipelined COPY rounds")
+
+
+# ----------------------------------------------- chained-exchange building blocks
+def test_partial_sum_and_range_aggregate_chain_on_one_gpu():
+    """The chained exchange on one GPU: a partial sum of workers 0..2 (as a
+    previous rank would store it), then a context with N' = 1 + 3 workers
+    (the partial + workers 3..5, rescale 1/6) aggregated piece by piece --
+    bit-identical to the 6-worker oracle round."""
+    from paper_1805_07891_b200 import PHub, capi
+    sizes = manifest("resnet50")
+    E = sum(sizes)
+    w0, v0 = host_state(E, 8)
+    head = _hub(sizes, 3)
+    gd = device_grads(head, 6, 8)
+    for g in gd:
+        g.nan_to_num_(0.0)                  # padding must be finite for the flat partial sum
+    part = torch.empty(head.E_padded, device=DEV)
+    capi.phub_partial_sum(head.ctx, [g.data_ptr() for g in gd[:3]], part.data_ptr(), 0,
+                          head.E_padded, head._stream(None))
+    tail = PHub(sizes, 4, device=0, rescale=1.0 / 6)
+    tail.load_state(w0, v0)
+    tail.push(0, part)
+    for k in range(3):
+        tail.push(1 + k, gd[3 + k])
+    Ep = tail.E_padded
+    cuts = [0, 4096, 4096 * 9, Ep // 2 // 64 * 64, Ep]
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        assert tail.iteration == 0
+        capi.phub_aggregate_range(tail.ctx, b, e, tail._stream(None))
+    assert tail.iteration == 1
+    torch.cuda.synchronize()
+    w, v, _ = tail.read_state()
+    rw, rv, _ = oracle.round_(sizes, host_grads(E, 6, 8), w0, v0, 0.1, 0.9)
+    assert_bits_equal(w, rw, "chained w")
+    assert_bits_equal(v, rv, "chained v")
+    head.close()
+    tail.close()
+
+
+def test_range_aggregate_order_errors():
+    from paper_1805_07891_b200 import PhubError, capi
+    hub = _hub(SMALL, 2)
+    gd = device_grads(hub, 2)
+    for w, g in enumerate(gd):
+        hub.push(w, g)
+    with pytest.raises(PhubError):
+        capi.phub_aggregate_range(hub.ctx, 64, 128, 0)          # must start at the range begin
+    capi.phub_aggregate_range(hub.ctx, 0, 64, 0)
+    with pytest.raises(PhubError):
+        hub.aggregate_optimize()                                # iteration is being ranged
+    capi.phub_aggregate_range(hub.ctx, 64, hub.E_padded, 0)
+    assert hub.iteration == 1
+    hub.close()
