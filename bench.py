@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
-    ap.add_argument("--pieces", type=int, default=8, help="chain mode pipeline pieces")
+    ap.add_argument("--pieces", type=int, default=16, help="chain mode pipeline pieces")
+    ap.add_argument("--chain-sync", default="flags", choices=["flags", "barrier"])
     ap.add_argument("--mode", default="auto", choices=["auto", "p2p", "chain", "nccl", "allreduce"],
                     help="N>1 exchange: fused peer-memory kernel (p2p) or NCCL send/recv")
     return ap.parse_args()
@@ -297,7 +298,8 @@ def bench_multi(args, mname, N, cb):
     ar = args.mode == "allreduce"
     try:
         if chain:
-            sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces)
+            sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
+                                  sync=args.chain_sync)
         else:
             cls = {"p2p": P2PShardedPHub, "nccl": ShardedPHub,
                    "allreduce": AllReduceBaseline}[args.mode]
@@ -388,6 +390,8 @@ def bench_multi(args, mname, N, cb):
     dist.barrier()
     clocks.stop()
     launches = hub.kernel_launches - k0
+    if chain and sh.sync_timeouts():
+        raise RuntimeError("chained exchange: device-side waits timed out")
     mine = {"rank": rank, "ms": t0.elapsed_time(t1) / args.steps,
             "k_ms": sum(a.elapsed_time(b) for a, b in ev) / args.steps,
             "owned": hub.owned_elements(), "out": plan.nvlink_bytes_out(),
@@ -451,7 +455,7 @@ def bench_multi(args, mname, N, cb):
                        "workers": N, "workers_per_gpu": N // G, "chunk_bytes": cb,
                        "mode": (f"M3 (full exchange) chain: rank-ordered partial sums over "
                                 f"NVLink, last rank fused Nesterov + replica stores, pipelined "
-                                f"over {args.pieces} pieces") if chain else
+                                f"over {args.pieces} pieces ({args.chain_sync} sync)") if chain else
                                ("M3 (full exchange) p2p: one fused kernel per owner reads peer "
                                 "gradients + writes peer replicas over NVLink, NCCL barrier "
                                 "before/after") if p2p else

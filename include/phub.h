@@ -237,6 +237,21 @@ phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
  * and after phub_aggregate_optimize); the library never spins on peers.
  * ------------------------------------------------------------------------- */
 
+/* Device-side ordering between the stages of a chained exchange (one GPU per
+ * process).  `wait_flag` (nullable) is a uint32 in this GPU's memory that a
+ * previous stage raises; every CTA of the launch first waits until
+ * *wait_flag >= wait_value (system-scope acquire; bounded: after ~2 s it
+ * gives up, counts a timeout -- see phub_sync_timeouts -- and skips its
+ * work).  `signal_flag` (nullable, typically peer-mapped) is written with
+ * `signal_value` (system-scope release) once every CTA of the launch has
+ * finished its stores.  At most one signalling launch per context in flight. */
+typedef struct {
+    const uint32_t* wait_flag;
+    uint32_t wait_value;
+    uint32_t* signal_flag;
+    uint32_t signal_value;
+} phub_sync;
+
 /* Chained exchange (workers hosted in rank order): the
  * worker-order partial sum of `count` (<= 64) padded-layout sources over
  * [begin, end), stored into `dst` (padded layout; typically a peer-mapped
@@ -246,7 +261,7 @@ phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
  * All pointers 32-B aligned device memory; begin, end multiples of 8.
  * Uses ctx's device; no receipts are involved. */
 phub_status phub_partial_sum(phub_ctx ctx, const float* const* srcs, int32_t count, float* dst,
-                             uint64_t begin, uint64_t end, void* stream);
+                             uint64_t begin, uint64_t end, const phub_sync* sync, void* stream);
 
 /* Range-wise aggregation of one iteration (pipelined exchange): requires all
  * N x K pushes, whole-model / owned-range pushes under CONTIG ownership;
@@ -254,7 +269,11 @@ phub_status phub_partial_sum(phub_ctx ctx, const float* const* srcs, int32_t cou
  * cover the owned range in increasing, abutting order starting at its begin
  * (begin == previous end); the call that reaches the owned range's end
  * completes the iteration.  begin/end multiples of 8 (or the range bounds). */
-phub_status phub_aggregate_range(phub_ctx ctx, uint64_t begin, uint64_t end, void* stream);
+phub_status phub_aggregate_range(phub_ctx ctx, uint64_t begin, uint64_t end,
+                                 const phub_sync* sync, void* stream);
+
+/* Number of phub_sync waits that timed out on this context (synchronous). */
+phub_status phub_sync_timeouts(phub_ctx ctx, uint32_t* count);
 
 /* Every later phub_aggregate_optimize also stores w' of the owned range into
  * replicas[0..count) (padded layout, E_padded elements each; device pointers,

@@ -39,6 +39,11 @@ class phub_chunk(C.Structure):
                 ("length", C.c_uint64), ("owner", C.c_int32), ("reserved", C.c_int32)]
 
 
+class phub_sync(C.Structure):
+    _fields_ = [("wait_flag", C.c_void_p), ("wait_value", C.c_uint32),
+                ("signal_flag", C.c_void_p), ("signal_value", C.c_uint32)]
+
+
 class phub_config(C.Structure):
     _fields_ = [
         ("key_num_elements", C.POINTER(C.c_uint64)),
@@ -69,9 +74,11 @@ _SIGS = {
                             C.c_void_p]),
     "phub_aggregate_optimize": (C.c_int, [phub_ctx, C.c_void_p]),
     "phub_aggregate_ready": (C.c_int, [phub_ctx, C.c_void_p, _u64p]),
-    "phub_aggregate_range": (C.c_int, [phub_ctx, C.c_uint64, C.c_uint64, C.c_void_p]),
+    "phub_aggregate_range": (C.c_int, [phub_ctx, C.c_uint64, C.c_uint64, C.c_void_p,
+                                       C.c_void_p]),
     "phub_partial_sum": (C.c_int, [phub_ctx, C.POINTER(C.c_void_p), C.c_int32, C.c_void_p,
-                                   C.c_uint64, C.c_uint64, C.c_void_p]),
+                                   C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "phub_sync_timeouts": (C.c_int, [phub_ctx, C.POINTER(C.c_uint32)]),
     "phub_pull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
     "phub_pushpull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32,
                                 C.c_void_p, C.c_void_p]),
@@ -162,14 +169,34 @@ def phub_aggregate_ready(ctx, stream: int = 0) -> int:
     return int(n.value)
 
 
-def phub_aggregate_range(ctx, begin: int, end: int, stream: int = 0):
-    _check(_lib.phub_aggregate_range(ctx, begin, end, stream), "phub_aggregate_range", ctx)
+def _sync(wait=None, signal=None):
+    """phub_sync from (flag_ptr, value) pairs; None when neither is given."""
+    if wait is None and signal is None:
+        return None
+    s = phub_sync()
+    if wait is not None:
+        s.wait_flag, s.wait_value = wait
+    if signal is not None:
+        s.signal_flag, s.signal_value = signal
+    return C.byref(s)
 
 
-def phub_partial_sum(ctx, srcs, dst: int, begin: int, end: int, stream: int = 0):
+def phub_aggregate_range(ctx, begin: int, end: int, stream: int = 0, wait=None, signal=None):
+    _check(_lib.phub_aggregate_range(ctx, begin, end, _sync(wait, signal), stream),
+           "phub_aggregate_range", ctx)
+
+
+def phub_partial_sum(ctx, srcs, dst: int, begin: int, end: int, stream: int = 0, wait=None,
+                     signal=None):
     arr = (C.c_void_p * max(len(srcs), 1))(*srcs)
-    _check(_lib.phub_partial_sum(ctx, arr, len(srcs), dst, begin, end, stream),
-           "phub_partial_sum", ctx)
+    _check(_lib.phub_partial_sum(ctx, arr, len(srcs), dst, begin, end, _sync(wait, signal),
+                                 stream), "phub_partial_sum", ctx)
+
+
+def phub_sync_timeouts(ctx) -> int:
+    n = C.c_uint32()
+    _check(_lib.phub_sync_timeouts(ctx, C.byref(n)), "phub_sync_timeouts", ctx)
+    return int(n.value)
 
 
 def phub_pull(ctx, key: int, dst_ptr: int, n: int, stream: int = 0):

@@ -80,6 +80,7 @@ struct phub_ctx_s {
     uintptr_t* d_base = nullptr;
     std::vector<float*> replicas;     // peer weight replicas written by the kernel
     uint64_t range_cursor = UINT64_MAX;   // phub_aggregate_range progress (UINT64_MAX: none)
+    uint32_t* d_sync = nullptr;           // [0] CTA counter, [1] timeouts, [2] abandoned wait value
 
     // options + counters
     int kernel = PHUB_KERNEL_AUTO;
@@ -296,6 +297,7 @@ static void free_ctx(phub_ctx c) {
     cudaFree(c->d_recv);
     cudaFree(c->d_tiles);
     cudaFree(c->d_base);
+    cudaFree(c->d_sync);
     delete c;
 }
 
@@ -361,13 +363,15 @@ phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
         (e = cudaMalloc(&c->d_v, bytes)) != cudaSuccess ||
         (c->keep_agg && (e = cudaMalloc(&c->d_agg, bytes)) != cudaSuccess) ||
         (e = cudaMalloc(&c->d_base, sizeof(uintptr_t) * c->base.size())) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_sync, 3 * sizeof(uint32_t))) != cudaSuccess ||
         (c->n_tiles && (e = cudaMalloc(&c->d_tiles, sizeof(Tile) * c->n_tiles)) != cudaSuccess)) {
         cudaGetLastError();
         free_ctx(c);
         why = std::string("device arenas: ") + cudaGetErrorString(e);
         return PHUB_ERR_OUT_OF_MEMORY;
     }
-    bool ok = cudaMemset(c->d_w, 0, bytes) == cudaSuccess &&
+    bool ok = cudaMemset(c->d_sync, 0, 3 * sizeof(uint32_t)) == cudaSuccess &&
+              cudaMemset(c->d_w, 0, bytes) == cudaSuccess &&
               cudaMemset(c->d_v, 0, bytes) == cudaSuccess &&
               (!c->d_agg || cudaMemset(c->d_agg, 0, bytes) == cudaSuccess) &&
               (!c->n_tiles || cudaMemcpy(c->d_tiles, tiles.data(), sizeof(Tile) * c->n_tiles,
@@ -631,8 +635,26 @@ phub_status phub_aggregate_ready(phub_ctx c, void* stream, uint64_t* keys_done) 
     return PHUB_OK;
 }
 
+static void apply_sync(phub_ctx c, phub::FlatArgs& a, const phub_sync* sync) {
+    a.cta_counter = c->d_sync;
+    a.timeouts = c->d_sync + 1;
+    if (!sync) return;
+    a.wait_flag = sync->wait_flag;
+    a.wait_value = sync->wait_value;
+    a.signal_flag = sync->signal_flag;
+    a.signal_value = sync->signal_value;
+}
+
+phub_status phub_sync_timeouts(phub_ctx c, uint32_t* count) {
+    if (!c || !count) return PHUB_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaMemcpy(count, c->d_sync + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpy(timeouts)");
+    return PHUB_OK;
+}
+
 phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count, float* dst,
-                             uint64_t begin, uint64_t end, void* stream) {
+                             uint64_t begin, uint64_t end, const phub_sync* sync, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
     if (c->failed) return PHUB_ERR_CUDA;
     if (count < 1 || count > phub::kMaxWorkers || !srcs || !dst)
@@ -651,6 +673,7 @@ phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count
     a.nw = count;
     a.begin = begin;
     a.end = end;
+    apply_sync(c, a, sync);
     DeviceGuard g(c->device);
     c->launches = 0;
     const uint64_t nvec = (end - begin) / 8;
@@ -663,7 +686,8 @@ phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count
     return PHUB_OK;
 }
 
-phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end, void* stream) {
+phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
+                                 const phub_sync* sync, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
     if (c->failed) return PHUB_ERR_CUDA;
     if (c->got_count != (uint64_t)c->K * c->N)
@@ -691,8 +715,9 @@ phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end, void*
     c->launches = 0;
     cudaError_t e = cudaSuccess;
     const uint64_t lo = std::max(b, cur);
-    if (e_ > lo) {
+    if (e_ > lo || (sync && sync->signal_flag)) {
         phub::FlatArgs a{};
+        apply_sync(c, a, sync);
         for (int w = 0; w < c->N; ++w) a.g[w] = reinterpret_cast<const float*>(c->base[(size_t)w * c->K]);
         a.w = c->d_w;
         a.v = c->d_v;

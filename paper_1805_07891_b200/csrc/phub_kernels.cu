@@ -115,6 +115,66 @@ __device__ __forceinline__ void st_stream(V4* p, const V4& r) {
                  :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]) : "memory");
 }
 
+// ----------------------------------------------- stage ordering (chain)
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Every CTA waits for the previous stage's flag (bounded); returns false when
+// the wait expired (the CTA then skips its work; the timeout is counted).
+__device__ __forceinline__ bool stage_wait(const FlatArgs& a) {
+    if (!a.wait_flag) return true;
+    __shared__ int ok;
+    if (threadIdx.x == 0) {
+        // timeouts[0]: expired waits; timeouts[1]: highest wait value given up on,
+        // so once one CTA gives up, the rest of the grid does not wait again
+        volatile uint32_t* abandoned = a.timeouts + 1;
+        const uint64_t t0 = globaltimer_ns();
+        int good = 1;
+        while (ld_acquire_sys(a.wait_flag) < a.wait_value) {
+            if (*abandoned >= a.wait_value) {
+                good = 0;
+                break;
+            }
+            if (globaltimer_ns() - t0 > 2000000000ull) {
+                atomicAdd(a.timeouts, 1u);
+                atomicMax(a.timeouts + 1, a.wait_value);
+                good = 0;
+                break;
+            }
+            __nanosleep(64);
+        }
+        ok = good;
+    }
+    __syncthreads();
+    return ok != 0;
+}
+
+// After all CTAs' stores: the last CTA to finish raises the next stage's flag.
+__device__ __forceinline__ void stage_signal(const FlatArgs& a) {
+    if (!a.signal_flag) return;
+    __threadfence_system();                       // this thread's (peer) stores are visible
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t done = atomicAdd(a.cta_counter, 1u);
+        if (done == gridDim.x - 1) {
+            *a.cta_counter = 0;
+            __threadfence_system();
+            st_release_sys(a.signal_flag, a.signal_value);
+        }
+    }
+}
+
 // ------------------------------------------------------------- arithmetic
 // Nesterov step on one element, each op rounded separately (R5).
 __device__ __forceinline__ void nag(float s, float& w, float& v, float lr, float mu,
@@ -207,7 +267,8 @@ __device__ __forceinline__ void flat_loop(const FlatArgs& a) {
 
 template <int NW, int VEC, int CACHE, bool AGG>
 __global__ void __launch_bounds__(kThreads) k_flat(const __grid_constant__ FlatArgs a) {
-    flat_loop<NW, VEC, CACHE, AGG>(a);
+    if (stage_wait(a)) flat_loop<NW, VEC, CACHE, AGG>(a);
+    stage_signal(a);
 }
 
 template <int MINB>
@@ -284,7 +345,8 @@ __global__ void __launch_bounds__(kThreads) k_tiles(const __grid_constant__ Tile
 template <int NW>
 __global__ void __launch_bounds__(kThreads) k_prefix(const __grid_constant__ FlatArgs a,
                                                      float* __restrict__ dst) {
-    const uint64_t n = (a.end - a.begin) / 8;
+    const bool go = stage_wait(a);
+    const uint64_t n = go ? (a.end - a.begin) / 8 : 0;
     const uint64_t stride = (uint64_t)gridDim.x * kThreads;
     for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
         float acc[8];
@@ -309,6 +371,7 @@ __global__ void __launch_bounds__(kThreads) k_prefix(const __grid_constant__ Fla
         reinterpret_cast<V8*>(dst + a.begin)[i] = out;
     }
     __threadfence_system();
+    stage_signal(a);
 }
 
 // ------------------------------------------------ bulk-copy (TMA) staging
@@ -573,7 +636,7 @@ int flat_blocks_per_sm(int vec, int nw, bool agg, int cache) {
 
 cudaError_t launch_flat(const FlatArgs& a, int vec, int cache, int grid, cudaStream_t s,
                         int* launches) {
-    if (a.end <= a.begin) return cudaSuccess;
+    if (a.end <= a.begin && !a.signal_flag) return cudaSuccess;
     pick_flat(vec, a.nw, a.agg != nullptr, cache)<<<grid, kThreads, 0, s>>>(a);
     ++*launches;
     return cudaGetLastError();
@@ -588,7 +651,7 @@ cudaError_t launch_tiles(const TileArgs& a, int grid, cudaStream_t s, int* launc
 }
 
 cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches) {
-    if (a.end <= a.begin) return cudaSuccess;
+    if (a.end <= a.begin && !a.signal_flag) return cudaSuccess;
     switch (a.nw) {
         case 1: k_prefix<1><<<grid, kThreads, 0, s>>>(a, dst); break;
         case 2: k_prefix<2><<<grid, kThreads, 0, s>>>(a, dst); break;

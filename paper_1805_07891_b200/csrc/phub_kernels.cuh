@@ -29,6 +29,13 @@ struct FlatArgs {
     int nrep;                         // extra replicas (peer-mapped) that also receive w'
     float* rep[kMaxReplicas];
     uint64_t seg;                     // 0: grid-stride; else CTA-contiguous segments (vectors)
+    // optional device-side stage ordering (chained exchange)
+    const uint32_t* wait_flag;
+    uint32_t wait_value;
+    uint32_t* signal_flag;
+    uint32_t signal_value;
+    uint32_t* cta_counter;            // local counter: last CTA raises signal_flag
+    uint32_t* timeouts;               // local counter of expired waits
 };
 
 struct TileArgs {

@@ -361,13 +361,17 @@ class ChainShardedPHub:
     """
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, pieces=8):
+                 device=None, group=None, pieces=8, sync="flags"):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
         self.group = group
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         self.rank, self.world = rank, world
+        if sync not in ("flags", "barrier"):
+            raise ValueError("sync must be 'flags' or 'barrier'")
+        self.sync = sync
+        self._epoch = 0
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
         self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, rank, world)
@@ -387,28 +391,35 @@ class ChainShardedPHub:
         for t in self._grads.values():
             t.zero_()
         self._pin = capi.phub_alloc_shared(dev, 4 * Ep) if rank > 0 else None
-        mine = (rank, capi.phub_ipc_get_handle(dev, self._pin) if self._pin else None,
-                capi.phub_ipc_get_handle(dev, self.hub.weights_ptr()))
-        allh = [None] * world
-        dist.all_gather_object(allh, mine, group=group)
-        allh.sort(key=lambda x: x[0])
-        self._opened = []
-        self._next_in = None
-        if not self.last:
-            self._next_in = capi.phub_ipc_open(dev, allh[rank + 1][1])
-            self._opened.append(self._next_in)
-        else:
-            reps = []
-            for r, _pin, wh in allh:
-                if r != rank:
-                    reps.append(capi.phub_ipc_open(dev, wh))
-            self._opened += reps
-            capi.phub_set_replicas(self.hub.ctx, reps)
         # piece boundaries: multiples of 64 elements (256 B)
         k = max(1, int(pieces))
         step = -(-Ep // k)
         step = -(-step // 64) * 64
         self.pieces = [(b, min(Ep, b + step)) for b in range(0, Ep, step)]
+        # one uint32 "piece ready" flag per piece, raised by the previous rank
+        self._flags = capi.phub_alloc_shared(dev, 4 * len(self.pieces)) if rank > 0 else None
+        if self._flags:
+            torch.as_tensor(_CudaArray(self._flags, len(self.pieces), self),
+                            device=f"cuda:{dev}").zero_()
+        mine = (rank, capi.phub_ipc_get_handle(dev, self._pin) if self._pin else None,
+                capi.phub_ipc_get_handle(dev, self.hub.weights_ptr()),
+                capi.phub_ipc_get_handle(dev, self._flags) if self._flags else None)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        allh.sort(key=lambda x: x[0])
+        self._opened = []
+        self._next_in = self._next_flags = None
+        if not self.last:
+            self._next_in = capi.phub_ipc_open(dev, allh[rank + 1][1])
+            self._next_flags = capi.phub_ipc_open(dev, allh[rank + 1][3])
+            self._opened += [self._next_in, self._next_flags]
+        else:
+            reps = []
+            for r, _pin, wh, _fl in allh:
+                if r != rank:
+                    reps.append(capi.phub_ipc_open(dev, wh))
+            self._opened += reps
+            capi.phub_set_replicas(self.hub.ctx, reps)
         self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
         self.replica = self.hub.weights()
         torch.cuda.synchronize(dev)
@@ -439,6 +450,20 @@ class ChainShardedPHub:
         srcs = ([self._pin] if self._pin else []) + [self._own[w] for w in hosted]
         stream = self.hub._stream(None)
         K = len(self.pieces)
+        if self.sync == "flags":
+            # all pieces enqueued at once; each launch waits (on the device) for the
+            # previous rank's "piece ready" flag and raises the next rank's
+            self._epoch += 1
+            ep = self._epoch
+            for p, (b, e) in enumerate(self.pieces):
+                wait = (self._flags + 4 * p, ep) if self._flags else None
+                if self.last:
+                    capi.phub_aggregate_range(self.hub.ctx, b, e, stream, wait=wait)
+                else:
+                    capi.phub_partial_sum(self.hub.ctx, srcs, self._next_in, b, e, stream,
+                                          wait=wait, signal=(self._next_flags + 4 * p, ep))
+            self.barrier()                   # replicas complete; buffers free for the next round
+            return
         for j in range(K + self.world - 1):
             p = j - self.rank
             if 0 <= p < K:
@@ -455,6 +480,9 @@ class ChainShardedPHub:
         self.exchange()
         for w in self.hosted:
             host_out[w].copy_(self.replica, non_blocking=True)
+
+    def sync_timeouts(self) -> int:
+        return capi.phub_sync_timeouts(self.hub.ctx)
 
     def weights(self):
         return self.replica
@@ -474,5 +502,7 @@ class ChainShardedPHub:
             capi.phub_free_shared(self.device, p)
         if self._pin:
             capi.phub_free_shared(self.device, self._pin)
+        if self._flags:
+            capi.phub_free_shared(self.device, self._flags)
         self._own = {}
         self.hub.close()

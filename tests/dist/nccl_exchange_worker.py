@@ -32,12 +32,13 @@ def main():
     special = {"small": [3, 3, 9408, 64, 64, 4096, 20000, 1000, 7], "one": [5]}
     sizes = special[name] if name in special else manifest(name)
     E = sum(sizes)
-    if mode == "chain":
-        sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=3)
+    if mode.startswith("chain"):
+        sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=3,
+                              sync="barrier" if mode == "chain_barrier" else "flags")
     else:
         cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
         sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
-    fused = mode in ("p2p", "chain")
+    fused = mode in ("p2p", "chain", "chain_barrier")
     w_ref, v_ref = values_np(1, 0, E, 20), values_np(2, 0, E, 25)
     sh.hub.load_state(w_ref, v_ref)
     idx = torch.as_tensor(sh.hub.padded_index(), device=dev)
@@ -57,6 +58,8 @@ def main():
     torch.cuda.synchronize()
     got = sh.weights()[idx].cpu().numpy()
     ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
+    if mode.startswith("chain") and sh.sync_timeouts() != 0:
+        ok = False
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)

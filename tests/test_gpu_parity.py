@@ -633,3 +633,39 @@ def test_range_aggregate_order_errors():
     capi.phub_aggregate_range(hub.ctx, 64, hub.E_padded, 0)
     assert hub.iteration == 1
     hub.close()
+
+
+def test_stage_flags_signal_and_bounded_wait():
+    """phub_sync: a partial sum raises a flag that a range aggregate waits on;
+    a wait on a flag nobody raises gives up (bounded) and is counted."""
+    from paper_1805_07891_b200 import PHub, capi
+    sizes = manifest("tiny")
+    E = sum(sizes)
+    head = _hub(sizes, 2)
+    gd = [g.nan_to_num_(0.0) for g in device_grads(head, 4, 9)]
+    flags = torch.zeros(4, dtype=torch.int32, device=DEV)
+    part = torch.empty(head.E_padded, device=DEV)
+    st = head._stream(None)
+    capi.phub_partial_sum(head.ctx, [g.data_ptr() for g in gd[:2]], part.data_ptr(), 0,
+                          head.E_padded, st, signal=(flags.data_ptr(), 7))
+    tail = PHub(sizes, 3, device=0, rescale=0.25)
+    w0, v0 = host_state(E, 9)
+    tail.load_state(w0, v0)
+    tail.push(0, part)
+    tail.push(1, gd[2])
+    tail.push(2, gd[3])
+    capi.phub_aggregate_range(tail.ctx, 0, tail.E_padded, st, wait=(flags.data_ptr(), 7))
+    torch.cuda.synchronize()
+    assert int(flags[0].item()) == 7
+    assert capi.phub_sync_timeouts(tail.ctx) == 0
+    w, _, _ = tail.read_state()
+    rw, _, _ = oracle.round_(sizes, host_grads(E, 4, 9), w0, v0, 0.1, 0.9)
+    assert_bits_equal(w, rw, "flag-ordered chain on one GPU")
+    # a flag that is never raised: the wait expires (~2 s), the work is skipped
+    for k in range(3):
+        tail.push(k, gd[k])
+    capi.phub_aggregate_range(tail.ctx, 0, tail.E_padded, st, wait=(flags.data_ptr() + 4, 1))
+    torch.cuda.synchronize()
+    assert capi.phub_sync_timeouts(tail.ctx) >= 1
+    head.close()
+    tail.close()
