@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
-    ap.add_argument("--pieces", type=int, default=16, help="chain mode pipeline pieces")
+    ap.add_argument("--pieces", type=int, default=8, help="chain mode pipeline pieces")
     ap.add_argument("--chain-sync", default="flags", choices=["flags", "barrier"])
     ap.add_argument("--mode", default="auto", choices=["auto", "p2p", "chain", "nccl", "allreduce"],
                     help="N>1 exchange: fused peer-memory kernel (p2p) or NCCL send/recv")
