@@ -141,6 +141,16 @@ phub_status phub_destroy(phub_ctx ctx);
 phub_status phub_push(phub_ctx ctx, int32_t worker, int32_t key, const float* grad,
                       uint64_t n, int32_t mode, void* stream);
 
+/* Batched push: `count` pushes in one call (per-key framework pushes, e.g.
+ * one per layer as a backward pass produces them -- P:638).  Entry j
+ * is phub_push(ctx, workers[j], keys[j], grads[j], lens[j], mode, stream).
+ * Validated all-or-nothing: on any error nothing is recorded (no receipts,
+ * no copies) and *failed_index (nullable) names the offending entry. */
+phub_status phub_push_batch(phub_ctx ctx, int32_t count, const int32_t* workers,
+                            const int32_t* keys, const float* const* grads,
+                            const uint64_t* lens, int32_t mode, void* stream,
+                            int32_t* failed_index);
+
 /* Aggregate + optimize every owned chunk: for each element i
  *   s  = (((+0.0f + g_0[i]) + g_1[i]) + ...) + g_{N-1}[i]   (worker-id order)
  *   g  = s * rescale
@@ -301,7 +311,7 @@ phub_status phub_ipc_close(int32_t device, void* dev_ptr);
 enum {
     PHUB_OPT_KERNEL = 1,      /* PHUB_KERNEL_*                                           */
     PHUB_OPT_GRID = 2,        /* CTAs for the flat kernels, 0 = auto (SMs x occupancy)   */
-    PHUB_OPT_TILE_ELEMS = 3,  /* max elements per CTA tile in the chunk-tile kernel      */
+    PHUB_OPT_TILE_ELEMS = 3,  /* max elements per CTA tile in the chunk-tile kernel (1024) */
     PHUB_OPT_CACHE = 4,       /* PHUB_CACHE_*: L2 policy of the pulled weights   */
     PHUB_OPT_FLAT_SEG = 5,    /* flat kernels: 0 = grid-stride, else CTA-contiguous      */
                               /* segments of this many vectors                           */

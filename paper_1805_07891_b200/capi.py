@@ -73,6 +73,9 @@ _SIGS = {
     "phub_push": (C.c_int, [phub_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32,
                             C.c_void_p]),
     "phub_aggregate_optimize": (C.c_int, [phub_ctx, C.c_void_p]),
+    "phub_push_batch": (C.c_int, [phub_ctx, C.c_int32, C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int32), C.POINTER(C.c_void_p), _u64p, C.c_int32,
+                                  C.c_void_p, C.POINTER(C.c_int32)]),
     "phub_aggregate_ready": (C.c_int, [phub_ctx, C.c_void_p, _u64p]),
     "phub_aggregate_range": (C.c_int, [phub_ctx, C.c_uint64, C.c_uint64, C.c_void_p,
                                        C.c_void_p]),
@@ -157,6 +160,19 @@ def phub_destroy(ctx):
 
 def phub_push(ctx, worker: int, key: int, grad_ptr: int, n: int, mode: int, stream: int = 0):
     _check(_lib.phub_push(ctx, worker, key, grad_ptr, n, mode, stream), "phub_push", ctx)
+
+
+def phub_push_batch(ctx, workers, keys, ptrs, lens, mode: int, stream: int = 0) -> None:
+    n = len(workers)
+    wa = (C.c_int32 * max(n, 1))(*workers)
+    ka = (C.c_int32 * max(n, 1))(*keys)
+    pa = (C.c_void_p * max(n, 1))(*ptrs)
+    la = (C.c_uint64 * max(n, 1))(*lens)
+    bad = C.c_int32(-1)
+    st = _lib.phub_push_batch(ctx, n, wa, ka, pa, la, mode, stream, C.byref(bad))
+    if st != PHUB_OK:
+        d = _lib.phub_last_error(ctx)
+        raise PhubError(st, f"phub_push_batch[{bad.value}]", d.decode() if d else "")
 
 
 def phub_aggregate_optimize(ctx, stream: int = 0):

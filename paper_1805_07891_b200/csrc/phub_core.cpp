@@ -62,7 +62,7 @@ struct phub_ctx_s {
     uint64_t n_tiles = 0;
     Tile* d_tiles = nullptr;
     std::vector<uint64_t> key_tile_begin, key_tile_end;   // owned tiles of key k, in order
-    uint32_t tile_elems = 8192;
+    uint32_t tile_elems = 1024;       // measured best (profiles/r01_tune: tiles1024)
 
     // arenas
     float* d_w = nullptr;
@@ -650,6 +650,55 @@ phub_status phub_sync_timeouts(phub_ctx c, uint32_t* count) {
     DeviceGuard g(c->device);
     cudaError_t e = cudaMemcpy(count, c->d_sync + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpy(timeouts)");
+    return PHUB_OK;
+}
+
+phub_status phub_push_batch(phub_ctx c, int32_t count, const int32_t* workers,
+                            const int32_t* keys, const float* const* grads,
+                            const uint64_t* lens, int32_t mode, void* stream,
+                            int32_t* failed_index) {
+    if (failed_index) *failed_index = -1;
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    if (count < 0 || (count && (!workers || !keys || !grads || !lens)))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "batch arrays are NULL");
+    // all-or-nothing: validate every entry (including duplicates inside the
+    // batch) against a scratch copy of the receipts before recording anything
+    std::vector<uint8_t> got = c->got;
+    for (int32_t j = 0; j < count; ++j) {
+        const int32_t w = workers[j], k = keys[j];
+        phub_status st = PHUB_OK;
+        if (w < 0 || w >= c->N) st = PHUB_ERR_BAD_WORKER;
+        else if (k != PHUB_ALL_KEYS && k != PHUB_OWNED_RANGE && (k < 0 || k >= c->K))
+            st = PHUB_ERR_BAD_KEY;
+        else {
+            const int k0 = k < 0 ? 0 : k, k1 = k < 0 ? c->K : k + 1;
+            for (int kk = k0; kk < k1 && st == PHUB_OK; ++kk) {
+                if (got[(size_t)kk * c->N + w]) st = PHUB_ERR_DUPLICATE_PUSH;
+                got[(size_t)kk * c->N + w] = 1;
+            }
+        }
+        if (st != PHUB_OK) {
+            if (failed_index) *failed_index = j;
+            return c->fail(st, "batch entry %d (worker %d, key %d) rejected", j, w, k);
+        }
+    }
+    // lengths / pointers / modes are checked by phub_push itself; the first
+    // failure there is reported, and the pushes before it are rolled back
+    std::vector<uint8_t> got_before = c->got;
+    const uint64_t count_before = c->got_count;
+    std::vector<uintptr_t> base_before = c->base;
+    for (int32_t j = 0; j < count; ++j) {
+        phub_status st = phub_push(c, workers[j], keys[j], grads[j], lens[j], mode, stream);
+        if (st != PHUB_OK) {
+            if (c->failed) return st;
+            c->got = got_before;
+            c->got_count = count_before;
+            c->base = base_before;
+            if (failed_index) *failed_index = j;
+            return st;
+        }
+    }
     return PHUB_OK;
 }
 

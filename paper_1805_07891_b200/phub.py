@@ -106,6 +106,17 @@ class PHub:
         p, cnt = _ptr_len(grad, n)
         capi.phub_push(self.ctx, int(worker), int(key), p, cnt, _MODES[mode], self._stream(stream))
 
+    def push_batch(self, entries, mode="borrow", stream=None):
+        """entries: iterable of (worker, key, buffer) -- one C call, all-or-nothing."""
+        ws, ks, ps, ls = [], [], [], []
+        for w, k, buf in entries:
+            p, n = _ptr_len(buf)
+            ws.append(int(w))
+            ks.append(int(k))
+            ps.append(p)
+            ls.append(n)
+        capi.phub_push_batch(self.ctx, ws, ks, ps, ls, _MODES[mode], self._stream(stream))
+
     def aggregate_optimize(self, stream=None):
         capi.phub_aggregate_optimize(self.ctx, self._stream(stream))
 

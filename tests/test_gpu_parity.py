@@ -388,7 +388,7 @@ def _sample_indices(sizes, chunk_bytes, rng, n_random=20000):
 
 @pytest.mark.parametrize("name,N,cb", [
     ("resnet50", 8, 32768), ("alexnet", 8, 32768), ("vgg19", 8, 32768),
-    ("resnet269", 8, 32768), ("resnet269", 8, 4096), ("resnet269", 8, 1 << 20),
+    *[("resnet269", 8, 4096 << i) for i in range(9)],        # BJ configs[4] sweep
 ])
 def test_full_size_sampled(name, N, cb):
     from workloads.generate import values_torch
@@ -669,3 +669,52 @@ def test_stage_flags_signal_and_bounded_wait():
     assert capi.phub_sync_timeouts(tail.ctx) >= 1
     head.close()
     tail.close()
+
+
+def test_push_batch_per_key_and_all_or_nothing():
+    from paper_1805_07891_b200 import PhubError, capi
+    sizes = SMALL
+    N = 3
+    hub = _hub(sizes, N, keep_aggregate=True)
+    w0, v0 = host_state(hub.E, 11)
+    hub.load_state(w0, v0)
+    hg = host_grads(hub.E, N, 11)
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    keys = [[torch.tensor(hg[w][starts[k]:starts[k + 1]], device=DEV) for k in range(len(sizes))]
+            for w in range(N)]
+    # a batch with a duplicate inside it is rejected whole
+    with pytest.raises(PhubError) as e:
+        hub.push_batch([(0, 0, keys[0][0]), (1, 0, keys[1][0]), (0, 0, keys[0][0])])
+    assert capi.STATUS_NAMES[e.value.status] == "PHUB_ERR_DUPLICATE_PUSH"
+    # a bad length late in the batch rolls back the earlier entries
+    with pytest.raises(PhubError):
+        hub.push_batch([(0, 0, keys[0][0]), (0, 1, keys[0][2])])
+    entries = [(w, k, keys[w][k]) for k in reversed(range(len(sizes))) for w in range(N)]
+    hub.push_batch(entries)                                 # nothing was recorded before
+    hub.aggregate_optimize()
+    w, v, s = hub.read_state()
+    rw, rv, rs = oracle.round_(sizes, hg, w0, v0, 0.1, 0.9)
+    assert_bits_equal(s, rs, "batch s")
+    assert_bits_equal(w, rw, "batch w")
+
+
+def test_two_contexts_multi_tenant():
+    """Two jobs with separate key namespaces share one GPU."""
+    a = _hub(manifest("tiny"), 4)
+    b = _hub(SMALL, 3, lr=0.05, momentum=0.5)
+    wa, va = host_state(a.E, 12)
+    wb, vb = host_state(b.E, 13)
+    a.load_state(wa, va)
+    b.load_state(wb, vb)
+    ga, gb = device_grads(a, 4, 12), device_grads(b, 3, 13)
+    for r in range(2):
+        for i in range(4):
+            a.push(i, ga[i])
+            if i < 3:
+                b.push(i, gb[i])
+        b.aggregate_optimize()
+        a.aggregate_optimize()
+        wa, va, _ = oracle.round_(manifest("tiny"), host_grads(a.E, 4, 12), wa, va, 0.1, 0.9)
+        wb, vb, _ = oracle.round_(SMALL, host_grads(b.E, 3, 13), wb, vb, 0.05, 0.5)
+    assert_bits_equal(a.read_state()[0], wa, "tenant a")
+    assert_bits_equal(b.read_state()[0], wb, "tenant b")
