@@ -409,19 +409,48 @@ def bench_multi(args, mname, N, cb):
             host_g[w].copy_(grads[w])
         host_o = {w: torch.empty(Ep, dtype=torch.float32, pin_memory=True) for w in sh.hosted}
 
-        def e2e_step():
-            if p2p:
-                sh.exchange_host(host_g, host_o)
-            else:
-                sh.exchange_host(host_g, grads, host_o)
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        total = args.e2e_steps + 1
+        ev_x = [torch.cuda.Event() for _ in range(total)]
+        ev_in = [torch.cuda.Event() for _ in range(total)]
+        ev_out = [torch.cuda.Event() for _ in range(total)]
 
-        e2e_step()
+        def e2e_round(k):
+            """fused modes: H2D of round k (slot k % 2) on s_in overlaps the D2H of
+            round k-1 on s_out; the exchange waits for both."""
+            if not p2p:
+                sh.exchange_host(host_g, grads, host_o)
+                return
+            slot = k % 2
+            if k >= 2:
+                s_in.wait_event(ev_x[k - 2])            # slot free: exchange k-2 is done
+            g = sh.gradients(slot)
+            with torch.cuda.stream(s_in):
+                for w in sh.hosted:
+                    g[w].copy_(host_g[w], non_blocking=True)
+            ev_in[k].record(s_in)
+            stream.wait_event(ev_in[k])
+            if k >= 1:
+                stream.wait_event(ev_out[k - 1])        # previous pulls have read w
+            sh.exchange(slot)
+            ev_x[k].record(stream)
+            s_out.wait_event(ev_x[k])
+            with torch.cuda.stream(s_out):
+                for w in sh.hosted:
+                    host_o[w].copy_(sh.replica, non_blocking=True)
+            ev_out[k].record(s_out)
+
+        e2e_round(0)
         torch.cuda.synchronize()
         dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for _ in range(args.e2e_steps):
-            e2e_step()
+        s_in.wait_event(a)
+        s_out.wait_event(a)
+        for k in range(1, total):
+            e2e_round(k)
+        if p2p:
+            stream.wait_event(ev_out[total - 1])
         b.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / args.e2e_steps], device=dev)
@@ -430,8 +459,10 @@ def bench_multi(args, mname, N, cb):
         e2e = {"value": round(N * 4 * E / te / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": N * 4 * Ep, "d2h_bytes_per_step": N * 4 * Ep,
                "steps": args.e2e_steps, "ms_per_step": round(te * 1e3, 3),
-               "path": f"{type(sh).__name__}.exchange_host: H2D of hosted grads -> exchange "
-                       f"({args.mode}) -> D2H of the replica per hosted worker"}
+               "path": f"{type(sh).__name__}: H2D of hosted grads -> exchange ({args.mode}) -> "
+                       f"D2H of the replica per hosted worker" +
+                       (" ; rounds pipelined (2 gradient slots, H2D of k+1 || D2H of k)"
+                        if p2p else "")}
     if rank == 0:
         ms_step = max(r["ms"] for r in allr)
         k_ms = max(r["k_ms"] for r in allr)

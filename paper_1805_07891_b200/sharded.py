@@ -193,7 +193,7 @@ class P2PShardedPHub:
     """
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 rescale=0.0, device=None, group=None):
+                 rescale=0.0, device=None, group=None, nslots=2):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -206,12 +206,16 @@ class P2PShardedPHub:
                         num_owners=world, owner_rank=rank, owner_policy="contig")
         Ep = self.hub.E_padded
         dev = self.device
-        self._own = {w: capi.phub_alloc_shared(dev, 4 * Ep) for w in self.plan.hosted()}
-        self._grads = {w: torch.as_tensor(_CudaArray(p, Ep, self), device=f"cuda:{dev}")
-                       for w, p in self._own.items()}
+        # gradient buffers per (slot, worker): two slots let round k+1's gradients
+        # be written while round k's exchange still reads slot k % 2
+        self.nslots = int(nslots)
+        self._own = {(sl, w): capi.phub_alloc_shared(dev, 4 * Ep)
+                     for sl in range(self.nslots) for w in self.plan.hosted()}
+        self._grads = {key: torch.as_tensor(_CudaArray(p, Ep, self), device=f"cuda:{dev}")
+                       for key, p in self._own.items()}
         for t in self._grads.values():
             t.zero_()
-        mine = (rank, {w: capi.phub_ipc_get_handle(dev, p) for w, p in self._own.items()},
+        mine = (rank, {key: capi.phub_ipc_get_handle(dev, p) for key, p in self._own.items()},
                 capi.phub_ipc_get_handle(dev, self.hub.weights_ptr()))
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
@@ -221,8 +225,8 @@ class P2PShardedPHub:
             for r, hs, wh in sorted(allh, key=lambda x: x[0]):
                 if r == rank:
                     continue
-                for w, h in hs.items():
-                    self._peer_grad[w] = capi.phub_ipc_open(dev, h)
+                for key, h in hs.items():
+                    self._peer_grad[key] = capi.phub_ipc_open(dev, h)
                 self._peer_w.append(capi.phub_ipc_open(dev, wh))
             capi.phub_set_replicas(self.hub.ctx, self._peer_w)
         except capi.PhubError as e:
@@ -250,30 +254,32 @@ class P2PShardedPHub:
     def hosted(self):
         return self.plan.hosted()
 
-    def gradients(self) -> dict:
+    def gradients(self, slot: int = 0) -> dict:
         """Device buffers (padded layout) the hosted workers write their gradients into."""
-        return self._grads
+        return {w: self._grads[(slot, w)] for w in self.hosted}
 
     def barrier(self):
         import torch.distributed as dist
         dist.all_reduce(self._flag, group=self.group)
 
-    def push(self):
+    def push(self, slot: int = 0):
         Ep = self.hub.E_padded
         for w in range(self.plan.num_workers):
-            ptr = self._own[w] if w in self._own else self._peer_grad[w]
+            key = (slot, w)
+            ptr = self._own[key] if key in self._own else self._peer_grad[key]
             self.hub.push(w, ptr, key=capi.PHUB_ALL_KEYS, mode="borrow", n=Ep)
 
-    def exchange(self):
+    def exchange(self, slot: int = 0):
         self.barrier()                  # every rank's gradients of this round are in place
-        self.push()                     # zero-copy: local and peer-mapped pointers
+        self.push(slot)                 # zero-copy: local and peer-mapped pointers
         self.hub.aggregate_optimize()   # NVLink loads + NAG + NVLink replica stores
         self.barrier()                  # every owner's stores into this replica are done
 
-    def exchange_host(self, host_grads: dict, host_out: dict):
+    def exchange_host(self, host_grads: dict, host_out: dict, slot: int = 0):
+        g = self.gradients(slot)
         for w in self.hosted:
-            self._grads[w].copy_(host_grads[w], non_blocking=True)
-        self.exchange()
+            g[w].copy_(host_grads[w], non_blocking=True)
+        self.exchange(slot)
         for w in self.hosted:
             host_out[w].copy_(self.replica, non_blocking=True)
 
@@ -361,7 +367,7 @@ class ChainShardedPHub:
     """
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, pieces=8, sync="flags"):
+                 device=None, group=None, pieces=8, sync="flags", nslots=2):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -385,9 +391,11 @@ class ChainShardedPHub:
             self.hub = PHub(key_sizes, per, chunk_size_bytes=chunk_size_bytes, lr=lr,
                             momentum=momentum, device=dev)
         Ep = self.hub.E_padded
-        self._own = {w: capi.phub_alloc_shared(dev, 4 * Ep) for w in self.plan.hosted()}
-        self._grads = {w: torch.as_tensor(_CudaArray(p, Ep, self), device=f"cuda:{dev}")
-                       for w, p in self._own.items()}
+        self.nslots = int(nslots)
+        self._own = {(sl, w): capi.phub_alloc_shared(dev, 4 * Ep)
+                     for sl in range(self.nslots) for w in self.plan.hosted()}
+        self._grads = {key: torch.as_tensor(_CudaArray(p, Ep, self), device=f"cuda:{dev}")
+                       for key, p in self._own.items()}
         for t in self._grads.values():
             t.zero_()
         self._pin = capi.phub_alloc_shared(dev, 4 * Ep) if rank > 0 else None
@@ -429,14 +437,14 @@ class ChainShardedPHub:
     def hosted(self):
         return self.plan.hosted()
 
-    def gradients(self) -> dict:
-        return self._grads
+    def gradients(self, slot: int = 0) -> dict:
+        return {w: self._grads[(slot, w)] for w in self.hosted}
 
     def barrier(self):
         import torch.distributed as dist
         dist.all_reduce(self._flag, group=self.group)
 
-    def exchange(self):
+    def exchange(self, slot: int = 0):
         Ep = self.hub.E_padded
         hosted = self.hosted
         self.barrier()                       # gradients of this round are in place everywhere
@@ -446,8 +454,8 @@ class ChainShardedPHub:
                 self.hub.push(0, self._pin, mode="borrow", n=Ep)
                 w0 = 1
             for i, w in enumerate(hosted):
-                self.hub.push(w0 + i, self._own[w], mode="borrow", n=Ep)
-        srcs = ([self._pin] if self._pin else []) + [self._own[w] for w in hosted]
+                self.hub.push(w0 + i, self._own[(slot, w)], mode="borrow", n=Ep)
+        srcs = ([self._pin] if self._pin else []) + [self._own[(slot, w)] for w in hosted]
         stream = self.hub._stream(None)
         K = len(self.pieces)
         if self.sync == "flags":
@@ -474,10 +482,11 @@ class ChainShardedPHub:
                     capi.phub_partial_sum(self.hub.ctx, srcs, self._next_in, b, e, stream)
             self.barrier()                   # piece p is complete before the next rank reads it
 
-    def exchange_host(self, host_grads: dict, host_out: dict):
+    def exchange_host(self, host_grads: dict, host_out: dict, slot: int = 0):
+        g = self.gradients(slot)
         for w in self.hosted:
-            self._grads[w].copy_(host_grads[w], non_blocking=True)
-        self.exchange()
+            g[w].copy_(host_grads[w], non_blocking=True)
+        self.exchange(slot)
         for w in self.hosted:
             host_out[w].copy_(self.replica, non_blocking=True)
 
