@@ -576,9 +576,10 @@ def bench_single(args, mname, N, cb):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
 
+    batch = [(w, capi.PHUB_ALL_KEYS, grads[w]) for w in range(N)]
+
     def step():
-        for w in range(N):
-            hub.push(w, grads[w])            # zero-copy BORROW: host bookkeeping only
+        hub.push_batch(batch)                 # N zero-copy BORROW pushes: host bookkeeping only
         hub.aggregate_optimize()              # one fused kernel on `stream`
 
     for _ in range(args.warmup):
@@ -593,8 +594,7 @@ def bench_single(args, mname, N, cb):
     torch.cuda.synchronize()
     t_start.record(stream)
     for i in range(args.steps):
-        for w in range(N):
-            hub.push(w, grads[w])
+        hub.push_batch(batch)
         ev[i][0].record(stream)
         hub.aggregate_optimize()
         ev[i][1].record(stream)

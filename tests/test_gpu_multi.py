@@ -33,9 +33,12 @@ def _port():
 def test_sharded_exchange_bit_exact(G, name, N, cb, rounds, mode):
     if _ngpus() < G:
         pytest.skip(f"needs {G} GPUs, have {_ngpus()}")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
-           "--master-addr=127.0.0.1", f"--master-port={_port()}", WORKER, name, str(N), str(cb),
-           str(rounds), mode]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    for _attempt in range(3):          # a just-freed port can be taken before torchrun binds it
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={G}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+               WORKER, name, str(N), str(cb), str(rounds), mode]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(": ok") == G

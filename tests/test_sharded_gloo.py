@@ -22,11 +22,14 @@ def _free_port():
     (4, "one", 4, 32768),            # one chunk: three owners own nothing
 ])
 def test_gloo_exchange(world, name, N, cb):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
-           f"--master-port={_free_port()}", WORKER, name, str(N), str(cb)]
     env = dict(os.environ, OMP_NUM_THREADS="1")
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    for _attempt in range(3):          # a just-freed port can be taken before torchrun binds it
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", WORKER, name, str(N), str(cb)]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(" ok: ") == world
 
