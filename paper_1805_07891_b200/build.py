@@ -65,5 +65,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+EXAMPLE_SRC = os.path.join(ROOT, "examples", "phub_c_example.c")
+EXAMPLE_BIN = os.path.join(ROOT, "build", "phub_c_example")
+
+
+def build_example() -> str:
+    """Compile the plain-C client of the ABI (examples/phub_c_example.c)."""
+    os.makedirs(os.path.dirname(EXAMPLE_BIN), exist_ok=True)
+    cuda = os.path.dirname(os.path.dirname(nvcc())) if os.path.isabs(nvcc()) else "/usr/local/cuda"
+    cmd = ["gcc", "-std=c11", "-Wall", "-O2", "-I", INCLUDE, "-I", os.path.join(cuda, "include"),
+           EXAMPLE_SRC, "-L", PKG, "-lphub", "-L", os.path.join(cuda, "lib64"), "-lcudart",
+           f"-Wl,-rpath,{PKG}", f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", EXAMPLE_BIN]
+    subprocess.check_call(cmd)
+    return EXAMPLE_BIN
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)

@@ -31,3 +31,12 @@ def test_bench_json_contract_tiny():
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["clocks"]["sm_mhz"] is None or d["clocks"]["sm_mhz"] > 0
+
+
+def test_c_example_runs():
+    import runpy
+    b = runpy.run_path(os.path.join(ROOT, "paper_1805_07891_b200", "build.py"))
+    exe = b["build_example"]()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 mismatches" in r.stdout

@@ -116,3 +116,14 @@ def test_plan_sweep_matches_oracle(cb):
     for f in ("vkey_id", "key_id", "offset", "length"):
         assert np.array_equal(np.array(lib[f]).astype(np.uint64), ref[f].astype(np.uint64))
     assert np.array_equal(np.array(lib["owner"]), oracle.owners_lpt(ref["length"], 4))
+
+
+def test_c_example_builds_against_the_abi():
+    """A plain-C program (no Python, no torch) compiles and links against
+    include/phub.h + libphub.so; its run is a GPU test."""
+    import runpy
+    b = runpy.run_path(os.path.join(ROOT, "paper_1805_07891_b200", "build.py"))
+    exe = b["build_example"]()
+    assert os.path.exists(exe)
+    out = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "libphub.so" in out
