@@ -397,8 +397,8 @@ def bench_multi(args, mname, N, cb):
             "owned": hub.owned_elements(), "out": plan.nvlink_bytes_out(),
             "in": plan.nvlink_bytes_in(), "launches": launches, "clocks": clocks.summary()}
     if chain:   # one partial per link per round; the last rank stores w' into G-1 replicas
-        mine["out"] = 4 * Ep * ((G - 1) if rank == G - 1 else 1)
-        mine["in"] = 4 * Ep * ((1 if rank > 0 else 0) + (1 if rank < G - 1 else 0))
+        from paper_1805_07891_b200.sharded import chain_nvlink_bytes
+        mine["out"], mine["in"] = chain_nvlink_bytes(Ep, G, rank)
     allr = [None] * G
     dist.all_gather_object(allr, mine)
 

@@ -347,6 +347,23 @@ class AllReduceBaseline:
         self.hub.close()
 
 
+def chain_pieces(E_padded: int, pieces: int):
+    """Pipeline pieces of the chained exchange: <= `pieces` abutting ranges
+    covering [0, E_padded), boundaries on 64-element (256 B) multiples."""
+    k = max(1, int(pieces))
+    step = -(-E_padded // k)
+    step = -(-step // 64) * 64
+    return [(b, min(E_padded, b + step)) for b in range(0, E_padded, step)]
+
+
+def chain_nvlink_bytes(E_padded: int, world: int, rank: int):
+    """(out, in) NVLink bytes of one chained round for `rank`: one partial per
+    link, and the last rank's w' stores into the other replicas."""
+    out = 4 * E_padded * ((world - 1) if rank == world - 1 else 1)
+    inn = 4 * E_padded * ((1 if rank > 0 else 0) + (1 if rank < world - 1 else 0))
+    return out, inn
+
+
 class ChainShardedPHub:
     """Chained exchange, pipelined over pieces.
 
@@ -399,11 +416,7 @@ class ChainShardedPHub:
         for t in self._grads.values():
             t.zero_()
         self._pin = capi.phub_alloc_shared(dev, 4 * Ep) if rank > 0 else None
-        # piece boundaries: multiples of 64 elements (256 B)
-        k = max(1, int(pieces))
-        step = -(-Ep // k)
-        step = -(-step // 64) * 64
-        self.pieces = [(b, min(Ep, b + step)) for b in range(0, Ep, step)]
+        self.pieces = chain_pieces(Ep, pieces)
         # one uint32 "piece ready" flag per piece, raised by the previous rank
         self._flags = capi.phub_alloc_shared(dev, 4 * len(self.pieces)) if rank > 0 else None
         if self._flags:

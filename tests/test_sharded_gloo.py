@@ -49,3 +49,20 @@ def test_plan_bytes_and_hosting():
         # per-GPU bytes out = 32E(G-1)/G^2 + 4E(G-1)/G (+ padding)
         expect = 32 * E * (G - 1) / G ** 2 + 4 * E * (G - 1) / G
         assert abs(max(p.nvlink_bytes_out() for p in plans) / expect - 1) < 2e-3
+
+
+def test_chain_pieces_and_bytes():
+    from paper_1805_07891_b200.sharded import ExchangePlan, chain_nvlink_bytes, chain_pieces
+    for Ep, k in ((32, 3), (143667264, 8), (288768, 16), (64, 64), (143667264, 1)):
+        p = chain_pieces(Ep, k)
+        assert p[0][0] == 0 and p[-1][1] == Ep and len(p) <= k
+        assert all(a[1] == b[0] for a, b in zip(p, p[1:]))
+        assert all(b % 64 == 0 for b, _ in p)
+    # the chain moves fewer NVLink bytes than the owner-sharded exchange at G = 2 only
+    from workloads import manifest
+    m = manifest("vgg19")
+    for G in (2, 4, 8):
+        plans = [ExchangePlan.build(m, 8, 32768, r, G) for r in range(G)]
+        sharded = max(max(p.nvlink_bytes_out(), p.nvlink_bytes_in()) for p in plans)
+        chain = max(max(chain_nvlink_bytes(plans[0].E_padded, G, r)) for r in range(G))
+        assert (chain < sharded) == (G == 2)
