@@ -718,3 +718,59 @@ def test_two_contexts_multi_tenant():
         wb, vb, _ = oracle.round_(SMALL, host_grads(b.E, 3, 13), wb, vb, 0.05, 0.5)
     assert_bits_equal(a.read_state()[0], wa, "tenant a")
     assert_bits_equal(b.read_state()[0], wb, "tenant b")
+
+
+# ------------------------------------------------------------ randomized
+@pytest.mark.parametrize("seed", range(24))
+def test_randomized_configs(seed):
+    """Random manifests (incl. 1-3 element keys), chunk sizes, worker counts,
+    kernels and push modes (whole-model / per-key / COPY / BORROW mixed per
+    worker), two rounds -- always bit-exact against the oracle."""
+    from paper_1805_07891_b200 import capi
+    rng = np.random.default_rng(1000 + seed)
+    K = int(rng.integers(1, 12))
+    sizes = [int(x) for x in rng.choice([1, 2, 3, 5, 31, 32, 33, 1000, 4096, 9999, 40000], K)]
+    cb = int(rng.choice([4, 8, 16, 100, 1024, 4096, 32768, 65536]))
+    N = int(rng.integers(1, 13))
+    kern = int(rng.choice([capi.PHUB_KERNEL_AUTO, capi.PHUB_KERNEL_TILES]))
+    lr = float(rng.choice([0.1, 0.01, 0.0]))
+    mu = float(rng.choice([0.9, 0.0, 0.5]))
+    hub = _hub(sizes, N, chunk_size_bytes=cb, keep_aggregate=True, lr=lr, momentum=mu)
+    E = hub.E
+    w, v = host_state(E, 20 + seed)
+    hub.load_state(w, v)
+    hub.set_option(capi.PHUB_OPT_KERNEL, kern)
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    pidx = hub.padded_index()
+    keep = []
+    for r in range(2):
+        hg = host_grads(E, N, 40 + seed * 3 + r)
+        for wk in range(N):
+            how = int(rng.integers(0, 4))
+            if how == 0:                                   # whole model, device, BORROW
+                t = torch.full((hub.E_padded,), float("nan"), device=DEV)
+                t[torch.as_tensor(pidx, device=DEV)] = torch.as_tensor(hg[wk], device=DEV)
+                keep.append(t)
+                hub.push(wk, t)
+            elif how == 1:                                 # whole model, host, COPY
+                h = np.full(hub.E_padded, np.nan, np.float32)
+                h[pidx] = hg[wk]
+                hub.push(wk, h, mode="copy")
+            elif how == 2:                                 # per key, device, BORROW
+                for k in rng.permutation(K):
+                    t = torch.as_tensor(np.ascontiguousarray(hg[wk][starts[k]:starts[k + 1]]),
+                                        device=DEV)
+                    keep.append(t)
+                    hub.push(wk, t, key=int(k))
+            else:                                          # per key, host, COPY
+                for k in rng.permutation(K):
+                    hub.push(wk, np.ascontiguousarray(hg[wk][starts[k]:starts[k + 1]]),
+                             key=int(k), mode="copy")
+        hub.aggregate_optimize()
+        torch.cuda.synchronize()
+        keep.clear()
+        w, v, s = oracle.round_(sizes, hg, w, v, lr, mu, chunk_bytes=cb)
+    gw, gv, gs = hub.read_state()
+    assert_bits_equal(gs, s, f"seed {seed} s")
+    assert_bits_equal(gv, v, f"seed {seed} v")
+    assert_bits_equal(gw, w, f"seed {seed} w")

@@ -187,3 +187,24 @@ def test_elems_matches_round():
     assert np.array_equal(bits(we), bits(w[idx]))
     assert np.array_equal(bits(ve), bits(v[idx]))
     assert np.array_equal(bits(se), bits(s[idx]))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_manifests_two_oracles_agree(seed):
+    """Random manifests / chunk sizes / worker counts / hyper-parameters: the
+    C oracle and the independent numpy oracle agree bit for bit, and the
+    result does not depend on the chunk size."""
+    rng = np.random.default_rng(500 + seed)
+    K = int(rng.integers(1, 9))
+    sizes = [int(x) for x in rng.choice([1, 2, 3, 7, 32, 33, 500, 4096, 9999], K)]
+    N = int(rng.integers(1, 10))
+    cb = int(rng.choice([4, 12, 64, 4096, 32768]))
+    lr = float(rng.choice([0.1, 0.37, 0.0]))
+    mu = float(rng.choice([0.9, 0.0, 0.5]))
+    grads, w0, v0 = _inputs(sizes, N, seed=seed + 100)
+    a = oracle.round_(sizes, grads, w0, v0, lr, mu, chunk_bytes=cb)
+    b = ref.round_(sizes, grads, w0, v0, lr, mu, chunk_bytes=cb)
+    c = oracle.round_(sizes, grads, w0, v0, lr, mu, chunk_bytes=32768)
+    for x, y, z in zip(a, b, c):
+        assert np.array_equal(bits(x), bits(y))
+        assert np.array_equal(bits(x), bits(z))
