@@ -57,7 +57,15 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
     ap.add_argument("--pieces", type=int, default=8, help="chain mode pipeline pieces")
-    ap.add_argument("--chain-sync", default="flags", choices=["flags", "barrier"])
+    ap.add_argument("--chain-sync", default="blocks", choices=["blocks", "flags", "barrier"])
+    ap.add_argument("--chain-block", type=int, default=16384,
+                    help="chain mode: elements per block flag (sync=blocks)")
+    ap.add_argument("--chain-pull", action="store_true",
+                    help="chain mode: next rank reads the partial over NVLink (default: pushed)")
+    ap.add_argument("--chain-no-consume", action="store_true",
+                    help="chain mode: push the incoming partial as BORROW, not CONSUME")
+    ap.add_argument("--chain-producer-grid", type=int, default=0,
+                    help="chain mode: CTAs of the partial-sum launch on non-last ranks")
     ap.add_argument("--mode", default="auto", choices=["auto", "p2p", "chain", "nccl", "allreduce"],
                     help="N>1 exchange: fused peer-memory kernel (p2p) or NCCL send/recv")
     return ap.parse_args()
@@ -273,6 +281,42 @@ def main():
 NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction per GPU
 
 
+def owner_phase_ms(sizes, N, cb, rank, G, steps, warmup, dev):
+    """Mode M2: this rank's owner kernel alone, with the N workers'
+    slices of its owned range already resident in its HBM (PHub's pushes land
+    by DMA at the owner).  Returns the mean kernel ms (CUDA
+    events on the launching stream)."""
+    import torch
+    from paper_1805_07891_b200 import PHub, capi
+    from workloads import grad_stream
+    from workloads.generate import values_torch
+    hub = PHub(sizes, N, chunk_size_bytes=cb, device=dev.index, num_owners=G, owner_rank=rank,
+               owner_policy="contig")
+    b, e = hub.owner_range()
+    bufs = [values_torch(grad_stream(w), b, e - b, 25, dev) for w in range(N)]
+    stream = torch.cuda.current_stream(dev)
+
+    def one():
+        for w in range(N):
+            hub.push(w, bufs[w], key=capi.PHUB_OWNED_RANGE)
+        hub.aggregate_optimize()
+
+    for _ in range(warmup):
+        one()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    t0.record(stream)
+    for _ in range(steps):
+        one()
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = t0.elapsed_time(t1) / steps
+    owned = hub.owned_elements()
+    hub.close()
+    del bufs
+    return ms, owned
+
+
 def bench_multi(args, mname, N, cb):
     """M3: 8 workers hosted N/G per GPU, chunks sharded by owner.
     mode p2p : one fused kernel per owner reads peers' gradients and writes peers'
@@ -299,7 +343,11 @@ def bench_multi(args, mname, N, cb):
     try:
         if chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
-                                  sync=args.chain_sync)
+                                  sync=args.chain_sync, block=args.chain_block,
+                                  pull=args.chain_pull, consume=not args.chain_no_consume)
+            if args.chain_producer_grid and not sh.last:
+                from paper_1805_07891_b200 import capi as _c
+                sh.hub.set_option(_c.PHUB_OPT_GRID, args.chain_producer_grid)
         else:
             cls = {"p2p": P2PShardedPHub, "nccl": ShardedPHub,
                    "allreduce": AllReduceBaseline}[args.mode]
@@ -399,6 +447,11 @@ def bench_multi(args, mname, N, cb):
     if chain:   # one partial per link per round; the last rank stores w' into G-1 replicas
         from paper_1805_07891_b200.sharded import chain_nvlink_bytes
         mine["out"], mine["in"] = chain_nvlink_bytes(Ep, G, rank)
+    if p2p:     # M2: the owner kernel alone on resident slices (NCCL mode: its k_ms already is)
+        mine["m2_ms"], mine["m2_owned"] = owner_phase_ms(sizes, N, cb, rank, G, args.steps,
+                                                         args.warmup, dev)
+    else:
+        mine["m2_ms"], mine["m2_owned"] = mine["k_ms"], mine["owned"]
     allr = [None] * G
     dist.all_gather_object(allr, mine)
 
@@ -469,6 +522,8 @@ def bench_multi(args, mname, N, cb):
         t_step = ms_step / 1e3
         value = N * 4 * E / t_step / 1e9
         slow = max(allr, key=lambda r: r["k_ms"])
+        m2_slow = max(allr, key=lambda r: r["m2_ms"])
+        m2_ms = m2_slow["m2_ms"]
         achieved = (4 * N + 16) * slow["owned"] / (slow["k_ms"] / 1e3) / 1e9
         peak, peak_src = measured_peaks()
         nv_bytes = max(max(r["out"], r["in"]) for r in allr) if not ar else \
@@ -485,8 +540,13 @@ def bench_multi(args, mname, N, cb):
             "config": {"workload": args.config, "keys": len(sizes), "E": E, "E_padded": Ep,
                        "workers": N, "workers_per_gpu": N // G, "chunk_bytes": cb,
                        "mode": (f"M3 (full exchange) chain: rank-ordered partial sums over "
-                                f"NVLink, last rank fused Nesterov + replica stores, pipelined "
-                                f"over {args.pieces} pieces ({args.chain_sync} sync)") if chain else
+                                f"NVLink, last rank fused Nesterov + replica stores, " +
+                                (f"one launch per rank streamed by per-block device flags "
+                                 f"({args.chain_block} elements/block, partial "
+                                 f"{'pulled' if args.chain_pull else 'pushed'})"
+                                 if args.chain_sync == "blocks" else
+                                 f"pipelined over {args.pieces} pieces ({args.chain_sync} sync)"))
+                               if chain else
                                ("M3 (full exchange) p2p: one fused kernel per owner reads peer "
                                 "gradients + writes peer replicas over NVLink, NCCL barrier "
                                 "before/after") if p2p else
@@ -498,9 +558,14 @@ def bench_multi(args, mname, N, cb):
                        "parallelism": f"owner-sharded x{G}", "kernel": args.kernel,
                        "seg": args.seg, "minb": args.minb, "grid": args.grid,
                        "l2": "no flush: inputs exceed L2"},
-            "owner_phase": None if (p2p or ar) else {
-                "mode": "M2 (kernel only, max over ranks)", "kernel_ms": round(k_ms, 4),
-                "value": round(N * 4 * E / (k_ms / 1e3) / 1e9, 1), "unit": "GB/s"},
+            "owner_phase": None if ar else {
+                "mode": "M2 (SURVEY 8(d)): owner kernel alone, the N workers' slices of its "
+                        "range resident in its HBM (pushes landed by DMA, P:895/P:933); "
+                        "max over ranks; NOT the headline (no NVLink transfer)",
+                "kernel_ms": round(m2_ms, 4),
+                "value": round(N * 4 * E / (m2_ms / 1e3) / 1e9, 1), "unit": "GB/s",
+                "hbm_frac": round((4 * N + 16) * m2_slow["m2_owned"] / (m2_ms / 1e3) / 1e9 /
+                                  measured_peaks()[0], 4)},
             "roofline": ({"bound": "nvlink", "achieved": round(nv_bytes / (k_ms / 1e3) / 1e9, 1),
                           "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                           "frac": round(nv_bytes / (k_ms / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),

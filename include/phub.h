@@ -70,7 +70,7 @@ typedef enum {
 #define PHUB_ALL_KEYS (-1)            /* whole-model push/pull in the padded layout        */
 #define PHUB_OWNED_RANGE (-2)         /* push of exactly this context's owned padded range  */
 
-enum { PHUB_COPY = 0, PHUB_BORROW = 1 };           /* ownership mode of a pushed buffer   */
+enum { PHUB_COPY = 0, PHUB_BORROW = 1, PHUB_CONSUME = 2 };   /* ownership mode of a pushed buffer */
 enum { PHUB_OWNER_LPT = 0, PHUB_OWNER_CONTIG = 1 };  /* chunk -> owner policy    */
 
 /* One virtual key: chunk `vkey_id` of key `key_id` covers elements
@@ -129,6 +129,15 @@ phub_status phub_destroy(phub_ctx ctx);
  *     the next phub_aggregate_optimize.  `grad` must be device memory
  *     (this or a peer-mapped GPU), 16-byte aligned.  The caller must keep it
  *     valid and unmodified until that aggregate has completed on its stream.
+ *   mode PHUB_CONSUME: as PHUB_BORROW, and the buffer's contents become
+ *     UNDEFINED once the aggregate that reads it has run: a block-streaming
+ *     kernel (phub_sync.block_elems > 0) may drop the buffer's lines from L2
+ *     right after reading them (discard.global.L2) instead of letting them be
+ *     written back -- for a transient staging buffer, e.g. a partial sum
+ *     another GPU stored over NVLink moments earlier, which then costs the
+ *     consumer neither an HBM write nor an HBM read.  Whole-model
+ *     (PHUB_ALL_KEYS) pushes of 128-B aligned buffers by workers < 64;
+ *     otherwise it behaves exactly as PHUB_BORROW.
  *   mode PHUB_COPY: the data (host or device memory) is copied into the
  *     context's receive arena on `stream`; the caller may reuse `grad` once
  *     the copy has completed on `stream`.  The arena has two slots (iteration
@@ -254,12 +263,24 @@ phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
  * gives up, counts a timeout -- see phub_sync_timeouts -- and skips its
  * work).  `signal_flag` (nullable, typically peer-mapped) is written with
  * `signal_value` (system-scope release) once every CTA of the launch has
- * finished its stores.  At most one signalling launch per context in flight. */
+ * finished its stores.  At most one signalling (or block-streaming) launch per
+ * context in flight.
+ *
+ * Block-streaming form (`block_elems` > 0, a multiple of 2048): the model is
+ * cut into blocks b = [b*block_elems, (b+1)*block_elems) of the padded layout
+ * and `wait_flag` / `signal_flag` point at ARRAYS with one uint32 per block
+ * (ceil(E_padded / block_elems) entries).  One persistent launch walks its
+ * range block by block: before reading block b a CTA waits for
+ * wait_flag[b] >= wait_value; once block b's stores are performed it raises
+ * signal_flag[b] = signal_value.  A downstream stage can then start on block b
+ * while this launch still works on later blocks -- the pipelining of PHub's
+ * streaming aggregation without one launch per piece. */
 typedef struct {
     const uint32_t* wait_flag;
     uint32_t wait_value;
     uint32_t* signal_flag;
     uint32_t signal_value;
+    uint64_t block_elems;       /* 0: one flag per launch; > 0: one flag per block */
 } phub_sync;
 
 /* Chained exchange (workers hosted in rank order): the

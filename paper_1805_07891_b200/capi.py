@@ -25,7 +25,7 @@ for _i, _n in enumerate(STATUS_NAMES):
     globals()[_n] = _i
 PHUB_ALL_KEYS = -1
 PHUB_OWNED_RANGE = -2
-PHUB_COPY, PHUB_BORROW = 0, 1
+PHUB_COPY, PHUB_BORROW, PHUB_CONSUME = 0, 1, 2
 PHUB_OWNER_LPT, PHUB_OWNER_CONTIG = 0, 1
 PHUB_OPT_KERNEL, PHUB_OPT_GRID, PHUB_OPT_TILE_ELEMS, PHUB_OPT_CACHE = 1, 2, 3, 4
 PHUB_OPT_FLAT_SEG, PHUB_OPT_FLAT_MINB, PHUB_OPT_FLAT_ONESHOT = 5, 6, 7
@@ -41,7 +41,8 @@ class phub_chunk(C.Structure):
 
 class phub_sync(C.Structure):
     _fields_ = [("wait_flag", C.c_void_p), ("wait_value", C.c_uint32),
-                ("signal_flag", C.c_void_p), ("signal_value", C.c_uint32)]
+                ("signal_flag", C.c_void_p), ("signal_value", C.c_uint32),
+                ("block_elems", C.c_uint64)]
 
 
 class phub_config(C.Structure):
@@ -185,8 +186,9 @@ def phub_aggregate_ready(ctx, stream: int = 0) -> int:
     return int(n.value)
 
 
-def _sync(wait=None, signal=None):
-    """phub_sync from (flag_ptr, value) pairs; None when neither is given."""
+def _sync(wait=None, signal=None, block=0):
+    """phub_sync from (flag_ptr, value) pairs; None when neither is given.
+    block > 0: the flag pointers are per-block arrays (block-streaming form)."""
     if wait is None and signal is None:
         return None
     s = phub_sync()
@@ -194,19 +196,21 @@ def _sync(wait=None, signal=None):
         s.wait_flag, s.wait_value = wait
     if signal is not None:
         s.signal_flag, s.signal_value = signal
+    s.block_elems = int(block)
     return C.byref(s)
 
 
-def phub_aggregate_range(ctx, begin: int, end: int, stream: int = 0, wait=None, signal=None):
-    _check(_lib.phub_aggregate_range(ctx, begin, end, _sync(wait, signal), stream),
+def phub_aggregate_range(ctx, begin: int, end: int, stream: int = 0, wait=None, signal=None,
+                         block: int = 0):
+    _check(_lib.phub_aggregate_range(ctx, begin, end, _sync(wait, signal, block), stream),
            "phub_aggregate_range", ctx)
 
 
 def phub_partial_sum(ctx, srcs, dst: int, begin: int, end: int, stream: int = 0, wait=None,
-                     signal=None):
+                     signal=None, block: int = 0):
     arr = (C.c_void_p * max(len(srcs), 1))(*srcs)
-    _check(_lib.phub_partial_sum(ctx, arr, len(srcs), dst, begin, end, _sync(wait, signal),
-                                 stream), "phub_partial_sum", ctx)
+    _check(_lib.phub_partial_sum(ctx, arr, len(srcs), dst, begin, end,
+                                 _sync(wait, signal, block), stream), "phub_partial_sum", ctx)
 
 
 def phub_sync_timeouts(ctx) -> int:

@@ -79,8 +79,10 @@ struct phub_ctx_s {
     std::vector<uintptr_t> base_uploaded;
     uintptr_t* d_base = nullptr;
     std::vector<float*> replicas;     // peer weight replicas written by the kernel
+    uint64_t consume_mask = 0;        // workers pushed with PHUB_CONSUME this iteration
     uint64_t range_cursor = UINT64_MAX;   // phub_aggregate_range progress (UINT64_MAX: none)
-    uint32_t* d_sync = nullptr;           // [0] CTA counter, [1] timeouts, [2] abandoned wait value
+    uint32_t* d_sync = nullptr;           // [0] CTA counter, [1] timeouts, [2] abandoned wait value,
+                                          // [3] block ticket, [4] CTAs done (block streaming)
 
     // options + counters
     int kernel = PHUB_KERNEL_AUTO;
@@ -92,6 +94,7 @@ struct phub_ctx_s {
                                       // registered (NVLink latency; profiles/r01_multi2)
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
+    int blocks_occ[2][phub::kMaxWorkers + 1] = {};   // resident CTAs/SM of k_blocks [nag][nw]
     uint64_t iteration = 0;
     int launches = 0;
     uint64_t launches_total = 0;
@@ -363,14 +366,14 @@ phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
         (e = cudaMalloc(&c->d_v, bytes)) != cudaSuccess ||
         (c->keep_agg && (e = cudaMalloc(&c->d_agg, bytes)) != cudaSuccess) ||
         (e = cudaMalloc(&c->d_base, sizeof(uintptr_t) * c->base.size())) != cudaSuccess ||
-        (e = cudaMalloc(&c->d_sync, 3 * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_sync, 5 * sizeof(uint32_t))) != cudaSuccess ||
         (c->n_tiles && (e = cudaMalloc(&c->d_tiles, sizeof(Tile) * c->n_tiles)) != cudaSuccess)) {
         cudaGetLastError();
         free_ctx(c);
         why = std::string("device arenas: ") + cudaGetErrorString(e);
         return PHUB_ERR_OUT_OF_MEMORY;
     }
-    bool ok = cudaMemset(c->d_sync, 0, 3 * sizeof(uint32_t)) == cudaSuccess &&
+    bool ok = cudaMemset(c->d_sync, 0, 5 * sizeof(uint32_t)) == cudaSuccess &&
               cudaMemset(c->d_w, 0, bytes) == cudaSuccess &&
               cudaMemset(c->d_v, 0, bytes) == cudaSuccess &&
               (!c->d_agg || cudaMemset(c->d_agg, 0, bytes) == cudaSuccess) &&
@@ -486,8 +489,11 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
         return c->fail(PHUB_ERR_LENGTH_MISMATCH, "push length %llu != %llu (S:172)",
                        (unsigned long long)n, (unsigned long long)want);
     if (!grad && n) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "grad is NULL");
-    if (mode != PHUB_COPY && mode != PHUB_BORROW)
-        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "mode must be PHUB_COPY or PHUB_BORROW");
+    if (mode != PHUB_COPY && mode != PHUB_BORROW && mode != PHUB_CONSUME)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT,
+                       "mode must be PHUB_COPY, PHUB_BORROW or PHUB_CONSUME");
+    const bool consume = mode == PHUB_CONSUME;
+    if (consume) mode = PHUB_BORROW;
     const int k0 = all ? 0 : key, k1 = all ? c->K : key + 1;
     for (int k = k0; k < k1; ++k)
         if (c->got[(size_t)k * c->N + worker])
@@ -502,6 +508,10 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW needs device memory");
         if (reinterpret_cast<uintptr_t>(grad) % 16 != 0)
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW pointer must be 16-B aligned");
+        // the kernel may drop a consumed buffer's 128-B lines from L2 after reading them
+        if (consume && key == PHUB_ALL_KEYS && worker < 64 &&
+            reinterpret_cast<uintptr_t>(grad) % 128 == 0)
+            c->consume_mask |= 1ull << worker;
         // base + 4*dev_off is the byte address of padded element dev_off
         for (int k = k0; k < k1; ++k)
             c->base[(size_t)worker * c->K + k] =
@@ -598,6 +608,7 @@ static cudaError_t launch_keys(phub_ctx c, cudaStream_t s, const std::vector<uin
 static void end_iteration(phub_ctx c) {
     std::fill(c->got.begin(), c->got.end(), 0);
     c->got_count = 0;
+    c->consume_mask = 0;
     std::fill(c->done.begin(), c->done.end(), 0);
     c->done_count = 0;
     ++c->iteration;
@@ -638,11 +649,33 @@ phub_status phub_aggregate_ready(phub_ctx c, void* stream, uint64_t* keys_done) 
 static void apply_sync(phub_ctx c, phub::FlatArgs& a, const phub_sync* sync) {
     a.cta_counter = c->d_sync;
     a.timeouts = c->d_sync + 1;
+    a.ticket = c->d_sync + 3;
     if (!sync) return;
     a.wait_flag = sync->wait_flag;
     a.wait_value = sync->wait_value;
     a.signal_flag = sync->signal_flag;
     a.signal_value = sync->signal_value;
+    a.block = sync->block_elems;
+}
+
+// Block-streaming sync: blocks are whole multiples of one 256-thread x 8-element pass.
+static phub_status check_block_sync(phub_ctx c, const phub_sync* sync) {
+    if (!sync || !sync->block_elems) return PHUB_OK;
+    if (sync->block_elems % 2048)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block_elems must be a multiple of 2048");
+    if ((sync->wait_flag && reinterpret_cast<uintptr_t>(sync->wait_flag) % 4) ||
+        (sync->signal_flag && reinterpret_cast<uintptr_t>(sync->signal_flag) % 4))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block flags must be 4-B aligned");
+    return PHUB_OK;
+}
+
+// Persistent grid of a block-streaming launch: every SM x resident CTAs, at most one CTA per block.
+static int blocks_grid(phub_ctx c, int nw, bool nag, uint64_t begin, uint64_t end, uint64_t B) {
+    int& occ = c->blocks_occ[nag ? 1 : 0][std::min(nw, phub::kMaxWorkers)];
+    if (!occ) occ = phub::blocks_per_sm(nw, nag);
+    const uint64_t nblk = (end + B - 1) / B - begin / B;
+    const int grid = c->grid_override ? c->grid_override : c->num_sms * occ;
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid, nblk));
 }
 
 phub_status phub_sync_timeouts(phub_ctx c, uint32_t* count) {
@@ -688,6 +721,7 @@ phub_status phub_push_batch(phub_ctx c, int32_t count, const int32_t* workers,
     std::vector<uint8_t> got_before = c->got;
     const uint64_t count_before = c->got_count;
     std::vector<uintptr_t> base_before = c->base;
+    const uint64_t consume_before = c->consume_mask;
     for (int32_t j = 0; j < count; ++j) {
         phub_status st = phub_push(c, workers[j], keys[j], grads[j], lens[j], mode, stream);
         if (st != PHUB_OK) {
@@ -695,6 +729,7 @@ phub_status phub_push_batch(phub_ctx c, int32_t count, const int32_t* workers,
             c->got = got_before;
             c->got_count = count_before;
             c->base = base_before;
+            c->consume_mask = consume_before;
             if (failed_index) *failed_index = j;
             return st;
         }
@@ -722,14 +757,20 @@ phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count
     a.nw = count;
     a.begin = begin;
     a.end = end;
+    if (phub_status bs = check_block_sync(c, sync)) return bs;
     apply_sync(c, a, sync);
     DeviceGuard g(c->device);
     c->launches = 0;
-    const uint64_t nvec = (end - begin) / 8;
-    const int grid = (int)std::max<uint64_t>(
-        1, std::min<uint64_t>((uint64_t)c->flat_grid[1][0], (nvec + phub::kThreads - 1) / phub::kThreads));
-    cudaError_t e = phub::launch_prefix(a, dst, grid, static_cast<cudaStream_t>(stream),
-                                        &c->launches);
+    cudaError_t e;
+    if (a.block) {
+        e = phub::launch_blocks(a, dst, blocks_grid(c, count, false, begin, end, a.block),
+                                static_cast<cudaStream_t>(stream), &c->launches);
+    } else {
+        const uint64_t nvec = (end - begin) / 8;
+        const int grid = (int)std::max<uint64_t>(
+            1, std::min<uint64_t>((uint64_t)c->flat_grid[1][0], (nvec + phub::kThreads - 1) / phub::kThreads));
+        e = phub::launch_prefix(a, dst, grid, static_cast<cudaStream_t>(stream), &c->launches);
+    }
     c->launches_total += (uint64_t)c->launches;
     if (e != cudaSuccess) return c->cuda_fail(e, "partial-sum launch");
     return PHUB_OK;
@@ -760,6 +801,7 @@ phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
     if (!flat)
         return c->fail(PHUB_ERR_UNSUPPORTED, "range aggregation needs whole-model / owned-range "
                        "pushes, 32-B aligned");
+    if (phub_status bs = check_block_sync(c, sync)) return bs;
     DeviceGuard g(c->device);
     c->launches = 0;
     cudaError_t e = cudaSuccess;
@@ -781,13 +823,20 @@ phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
         for (int r = 0; r < a.nrep; ++r) a.rep[r] = c->replicas[r];
         const uint64_t nvec = (e_ - lo) / 8;
         const uint64_t cover = (nvec + phub::kThreads - 1) / phub::kThreads;
-        int grid = c->grid_override ? c->grid_override
-                   : (c->flat_oneshot > 0 || (c->flat_oneshot < 0 && c->replicas.empty()))
-                         ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
-                         : c->flat_grid[1][c->keep_agg];
-        grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, cover));
-        e = phub::launch_flat(a, 8, c->cache, grid, static_cast<cudaStream_t>(stream),
-                              &c->launches);
+        if (a.block) {
+            a.discard = c->consume_mask;
+            e = e_ > lo ? phub::launch_blocks(a, nullptr, blocks_grid(c, c->N, true, lo, e_, a.block),
+                                              static_cast<cudaStream_t>(stream), &c->launches)
+                        : cudaSuccess;
+        } else {
+            int grid = c->grid_override ? c->grid_override
+                       : (c->flat_oneshot > 0 || (c->flat_oneshot < 0 && c->replicas.empty()))
+                             ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
+                             : c->flat_grid[1][c->keep_agg];
+            grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, cover));
+            e = phub::launch_flat(a, 8, c->cache, grid, static_cast<cudaStream_t>(stream),
+                                  &c->launches);
+        }
     }
     c->launches_total += (uint64_t)c->launches;
     if (e != cudaSuccess) return c->cuda_fail(e, "kernel launch");

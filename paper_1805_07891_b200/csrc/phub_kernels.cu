@@ -374,6 +374,163 @@ __global__ void __launch_bounds__(kThreads) k_prefix(const __grid_constant__ Fla
     stage_signal(a);
 }
 
+// ------------------------------------------- block-streaming chain stages
+// One persistent launch per stage and round.  CTA i walks blocks i, i+grid, ...
+// of `a.block` elements; per block it waits for the upstream stage's flag
+// (a.wait_flag[b], system-scope acquire, bounded), reads its sources, and
+// raises a.signal_flag[b] (system-scope release) once the block's stores are
+// performed.  The downstream stage therefore starts on block b while this one
+// still works on later blocks (streaming aggregation) -- no launch per
+// piece.  Sources are read with coherent loads (not the .nc path): the
+// upstream partial is written by another GPU while this kernel runs.
+__device__ __forceinline__ V8 ld_coherent(const V8* p) {
+    V8 r;
+    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
+                   "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
+                 : "l"(p) : "memory");
+    return r;
+}
+
+// Thread 0 waits for flag >= value (bounded, like stage_wait); the CTA learns
+// the outcome through shared memory.
+__device__ __forceinline__ bool block_wait(const FlatArgs& a, const uint32_t* flag) {
+    __shared__ int ok;
+    if (threadIdx.x == 0) {
+        volatile uint32_t* abandoned = a.timeouts + 1;
+        int good = 1;
+        if (ld_acquire_sys(flag) < a.wait_value) {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_sys(flag) < a.wait_value) {
+                if (*abandoned >= a.wait_value) { good = 0; break; }
+                if (globaltimer_ns() - t0 > 2000000000ull) {
+                    atomicAdd(a.timeouts, 1u);
+                    atomicMax(a.timeouts + 1, a.wait_value);
+                    good = 0;
+                    break;
+                }
+                __nanosleep(100);
+            }
+        }
+        ok = good;
+    }
+    __syncthreads();
+    return ok != 0;
+}
+
+template <int NW, bool NAG>
+__global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ FlatArgs a,
+                                                     float* __restrict__ dst) {
+    const uint64_t B = a.block;
+    const uint64_t b0 = a.begin / B, b1 = (a.end + B - 1) / B;
+    const int nw = NW > 0 ? NW : a.nw;
+    __shared__ uint64_t s_blk;
+    for (;;) {
+        // dynamic ticket: CTAs take blocks in global order as they free up, so
+        // this stage's front follows the upstream stage's front closely
+        if (threadIdx.x == 0) s_blk = b0 + atomicAdd(a.ticket, 1u);
+        __syncthreads();
+        const uint64_t blk = s_blk;
+        if (blk >= b1) break;
+        const bool go = a.wait_flag ? block_wait(a, a.wait_flag + blk) : true;
+        const uint64_t lo = (blk * B > a.begin ? blk * B : a.begin) / 8;
+        const uint64_t hi = ((blk + 1) * B < a.end ? (blk + 1) * B : a.end) / 8;
+        for (uint64_t i = lo + threadIdx.x; go && i < hi; i += kThreads) {
+            float acc[8];
+            if constexpr (NW > 0) {
+                V8 gv[NW];
+#pragma unroll
+                for (int k = 0; k < NW; ++k) gv[k] = ld_coherent(reinterpret_cast<const V8*>(a.g[k]) + i);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float s = __fadd_rn(0.0f, gv[0].x[j]);
+#pragma unroll
+                    for (int k = 1; k < NW; ++k) s = __fadd_rn(s, gv[k].x[j]);
+                    acc[j] = s;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+                for (int k0 = 0; k0 < nw; k0 += 8) {
+                    V8 gv[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k0 + k < nw) gv[k] = ld_coherent(reinterpret_cast<const V8*>(a.g[k0 + k]) + i);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k0 + k < nw) {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+                        }
+                }
+            }
+            if (a.discard) {
+                // consumed inputs (PHUB_CONSUME): the lane holding the first
+                // 32 B of each 128-B line drops it from L2 once the whole warp
+                // has its data -- no write-back of a staging buffer
+                __syncwarp(__activemask());
+                if ((i & 3) == 0)
+                    for (int k = 0; k < nw; ++k)
+                        if ((a.discard >> k) & 1)
+                            asm volatile("discard.global.L2 [%0], 128;"
+                                         :: "l"(reinterpret_cast<const V8*>(a.g[k]) + i) : "memory");
+            }
+            V8 out;
+            if constexpr (NAG) {
+                V8* w = reinterpret_cast<V8*>(a.w);
+                V8* v = reinterpret_cast<V8*>(a.v);
+                V8 wv = ld_state<PHUB_CACHE_ENABLED>(w + i);
+                V8 vv = ld_state<PHUB_CACHE_ENABLED>(v + i);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    out.x[j] = acc[j];
+                    nag(acc[j], wv.x[j], vv.x[j], a.lr, a.mu, a.rescale);
+                }
+                st_stream(w + i, wv);     // the pull is the replica stores below: keep L2
+                st_stream(v + i, vv);     // for the incoming partial, not for w'
+                if (a.agg) st_stream(reinterpret_cast<V8*>(a.agg) + i, out);
+                for (int r = 0; r < a.nrep; ++r) reinterpret_cast<V8*>(a.rep[r])[i] = wv;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) out.x[j] = acc[j];
+                reinterpret_cast<V8*>(dst)[i] = out;
+            }
+        }
+        // bar.sync (also retires this block's `ok` before the next wait) then
+        // one system-scope fence: cumulative over the CTA's stores (the
+        // cooperative-groups grid-sync pattern)
+        __syncthreads();
+        if (a.signal_flag) {
+            if (threadIdx.x == 0 && go) {
+                __threadfence_system();
+                st_release_sys(a.signal_flag + blk, a.signal_value);
+            }
+        }
+    }
+    if (NAG && a.nrep) __threadfence_system();
+    // the last CTA out resets the tickets for the next launch (stream-ordered)
+    if (threadIdx.x == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x - 1) {
+        a.ticket[0] = 0;
+        a.ticket[1] = 0;
+    }
+}
+
+template <bool NAG>
+void* pick_blocks(int nw) {
+    switch (nw) {
+        case 1: return (void*)k_blocks<1, NAG>;
+        case 2: return (void*)k_blocks<2, NAG>;
+        case 3: return (void*)k_blocks<3, NAG>;
+        case 4: return (void*)k_blocks<4, NAG>;
+        case 5: return (void*)k_blocks<5, NAG>;
+        case 6: return (void*)k_blocks<6, NAG>;
+        case 7: return (void*)k_blocks<7, NAG>;
+        case 8: return (void*)k_blocks<8, NAG>;
+        case 9: return (void*)k_blocks<9, NAG>;
+        default: return (void*)k_blocks<0, NAG>;
+    }
+}
+
 // ------------------------------------------------ bulk-copy (TMA) staging
 // Variant with the loads taken off the register file: one producer thread per
 // CTA streams each tile's N gradient slices and the w, v slices into a
@@ -662,6 +819,22 @@ cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t 
     }
     ++*launches;
     return cudaGetLastError();
+}
+
+int blocks_per_sm(int nw, bool nag) {
+    int nb = 0;
+    const void* fn = nag ? pick_blocks<true>(nw) : pick_blocks<false>(nw);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches) {
+    if (a.end <= a.begin || a.block == 0) return cudaSuccess;
+    void* fn = dst ? pick_blocks<false>(a.nw) : pick_blocks<true>(a.nw);
+    void* args[] = {const_cast<FlatArgs*>(&a), &dst};
+    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);
+    ++*launches;
+    return e;
 }
 
 size_t bulk_smem_bytes(int nw) { return (size_t)kBulkStages * (nw + 2) * kBulkTile * sizeof(float); }

@@ -36,6 +36,9 @@ struct FlatArgs {
     uint32_t signal_value;
     uint32_t* cta_counter;            // local counter: last CTA raises signal_flag
     uint32_t* timeouts;               // local counter of expired waits
+    uint64_t block;                   // > 0: block-streaming flags (one per `block` elements)
+    uint64_t discard;                 // bit k: input k is consumed (L2 lines may be discarded)
+    uint32_t* ticket;                 // [0] next block, [1] CTAs done (block streaming, zeroed)
 };
 
 struct TileArgs {
@@ -67,6 +70,12 @@ cudaError_t launch_tiles(const TileArgs& a, int grid, cudaStream_t s, int* launc
 // Worker-order partial sum (no optimizer): dst[i] = ((+0 + g0[i]) + g1[i]) + ...
 // over [a.begin, a.end); dst may be a peer-mapped pointer (chained exchange).
 cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches);
+// Block-streaming forms (a.block > 0): one persistent launch over [begin, end)
+// walking blocks of a.block elements in order, waiting on a.wait_flag[b] and
+// raising a.signal_flag[b] per block.  dst == nullptr: fused Nesterov (w, v,
+// replicas); else the worker-order partial sum stored into dst.
+cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches);
+int blocks_per_sm(int nw, bool nag);
 // TMA-style staging: 1-D bulk async copies into a shared-memory ring (nw <= 8).
 cudaError_t launch_bulk(const FlatArgs& a, int grid, cudaStream_t s, int* launches);
 size_t bulk_smem_bytes(int nw);

@@ -17,9 +17,10 @@ import ctypes as C
 import numpy as np
 
 from . import capi
-from .capi import PHUB_ALL_KEYS, PHUB_BORROW, PHUB_COPY
+from .capi import PHUB_ALL_KEYS, PHUB_BORROW, PHUB_CONSUME, PHUB_COPY
 
-_MODES = {"borrow": PHUB_BORROW, "copy": PHUB_COPY, PHUB_BORROW: PHUB_BORROW, PHUB_COPY: PHUB_COPY}
+_MODES = {"borrow": PHUB_BORROW, "copy": PHUB_COPY, "consume": PHUB_CONSUME,
+          PHUB_BORROW: PHUB_BORROW, PHUB_COPY: PHUB_COPY, PHUB_CONSUME: PHUB_CONSUME}
 _POLICIES = {"lpt": capi.PHUB_OWNER_LPT, "contig": capi.PHUB_OWNER_CONTIG,
              capi.PHUB_OWNER_LPT: capi.PHUB_OWNER_LPT, capi.PHUB_OWNER_CONTIG: capi.PHUB_OWNER_CONTIG}
 

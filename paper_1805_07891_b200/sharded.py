@@ -365,35 +365,45 @@ def chain_nvlink_bytes(E_padded: int, world: int, rank: int):
 
 
 class ChainShardedPHub:
-    """Chained exchange, pipelined over pieces.
+    """Chained exchange.
 
     Workers are hosted in rank order, so the worker-order sum can be built
-    rank by rank: rank p adds its hosted workers to the partial sum it
-    received from rank p-1 (phub_partial_sum) and stores the result straight
-    into rank p+1's buffer over NVLink; the last rank finishes the sum, runs
-    the fused Nesterov kernel on the whole model (phub_aggregate_range) and
-    stores w' into every replica.  Because every partial starts from +0 and
-    adds in order, the result is bit-identical to the one-GPU sum (R3, R4).
+    rank by rank: rank p adds its hosted workers to the partial sum of ranks
+    0..p-1 (phub_partial_sum); the last rank finishes the sum, runs the fused
+    Nesterov kernel on the whole model (phub_aggregate_range) and stores w'
+    into every replica.  Because every partial starts from +0 and adds in
+    order, the result is bit-identical to the one-GPU sum (R3, R4).
 
     Each link carries one model-size partial per round (4E bytes) instead of
     N/G gradient slices per owner -- fewer NVLink bytes than the sharded
-    exchange when G is small (G = 2: 4E vs 10E/4... see DESIGN.md 8).  The
-    model is split into `pieces`; in phase j rank p works on piece j - p, and
-    a stream-ordered NCCL barrier separates phases, so the ranks' kernels
-    overlap like a pipeline (no kernel ever waits on a peer).
+    exchange when G is small (G = 2: 4E per direction vs 10E).
+
+    sync="blocks" (default): ONE persistent launch per rank and round; the
+      model is cut into blocks of `block` elements with one device flag each,
+      so rank p+1 starts on block b as soon as rank p has raised its flag
+      (streaming).  With pull=True (default) each rank keeps its partial
+      in its own HBM and the next rank reads it over NVLink inside its kernel,
+      so the incoming partial never costs the consumer an HBM write + read.
+    sync="flags": the model is split into `pieces`, one launch per piece, each
+      waiting for a per-piece flag (device-side) -- the previous design.
+    sync="barrier": per-piece launches separated by NCCL barriers.
     """
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, pieces=8, sync="flags", nslots=2):
+                 device=None, group=None, pieces=8, sync="blocks", nslots=2, block=16384,
+                 pull=False, consume=True):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
         self.group = group
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         self.rank, self.world = rank, world
-        if sync not in ("flags", "barrier"):
-            raise ValueError("sync must be 'flags' or 'barrier'")
+        if sync not in ("blocks", "flags", "barrier"):
+            raise ValueError("sync must be 'blocks', 'flags' or 'barrier'")
         self.sync = sync
+        self.block = int(block)
+        self.pull = bool(pull) and sync == "blocks"
+        self.consume = bool(consume)
         self._epoch = 0
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
@@ -415,28 +425,38 @@ class ChainShardedPHub:
                        for key, p in self._own.items()}
         for t in self._grads.values():
             t.zero_()
-        self._pin = capi.phub_alloc_shared(dev, 4 * Ep) if rank > 0 else None
+        # partial-sum buffers: push style -> an inbox on the consumer (rank > 0);
+        # pull style -> an outbox on the producer (rank < world - 1)
+        self._pin = capi.phub_alloc_shared(dev, 4 * Ep) if rank > 0 and not self.pull else None
+        self._pout = capi.phub_alloc_shared(dev, 4 * Ep) if not self.last and self.pull else None
         self.pieces = chain_pieces(Ep, pieces)
-        # one uint32 "piece ready" flag per piece, raised by the previous rank
-        self._flags = capi.phub_alloc_shared(dev, 4 * len(self.pieces)) if rank > 0 else None
+        nflags = -(-Ep // self.block) if sync == "blocks" else len(self.pieces)
+        # one uint32 "ready" flag per block (or piece), raised by the previous rank
+        self._flags = capi.phub_alloc_shared(dev, 4 * nflags) if rank > 0 else None
         if self._flags:
-            torch.as_tensor(_CudaArray(self._flags, len(self.pieces), self),
-                            device=f"cuda:{dev}").zero_()
-        mine = (rank, capi.phub_ipc_get_handle(dev, self._pin) if self._pin else None,
-                capi.phub_ipc_get_handle(dev, self.hub.weights_ptr()),
-                capi.phub_ipc_get_handle(dev, self._flags) if self._flags else None)
+            torch.as_tensor(_CudaArray(self._flags, nflags, self), device=f"cuda:{dev}").zero_()
+        h = capi.phub_ipc_get_handle
+        mine = (rank, h(dev, self._pin) if self._pin else None,
+                h(dev, self.hub.weights_ptr()),
+                h(dev, self._flags) if self._flags else None,
+                h(dev, self._pout) if self._pout else None)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         allh.sort(key=lambda x: x[0])
         self._opened = []
-        self._next_in = self._next_flags = None
+        self._next_in = self._next_flags = self._prev_out = None
         if not self.last:
-            self._next_in = capi.phub_ipc_open(dev, allh[rank + 1][1])
+            if not self.pull:
+                self._next_in = capi.phub_ipc_open(dev, allh[rank + 1][1])
+                self._opened.append(self._next_in)
             self._next_flags = capi.phub_ipc_open(dev, allh[rank + 1][3])
-            self._opened += [self._next_in, self._next_flags]
-        else:
+            self._opened.append(self._next_flags)
+        if rank > 0 and self.pull:
+            self._prev_out = capi.phub_ipc_open(dev, allh[rank - 1][4])
+            self._opened.append(self._prev_out)
+        if self.last:
             reps = []
-            for r, _pin, wh, _fl in allh:
+            for r, _pin, wh, _fl, _po in allh:
                 if r != rank:
                     reps.append(capi.phub_ipc_open(dev, wh))
             self._opened += reps
@@ -461,16 +481,33 @@ class ChainShardedPHub:
         Ep = self.hub.E_padded
         hosted = self.hosted
         self.barrier()                       # gradients of this round are in place everywhere
+        upstream = self._prev_out if self.pull else self._pin     # partial of ranks 0..p-1
         if self.last:
             w0 = 0
             if self.world > 1:
-                self.hub.push(0, self._pin, mode="borrow", n=Ep)
+                # the pushed-in partial is a transient inbox: the block kernel may
+                # drop it from L2 after reading (no HBM write-back, PHUB_CONSUME)
+                consume = self.sync == "blocks" and not self.pull and self.consume
+                self.hub.push(0, upstream, mode="consume" if consume else "borrow", n=Ep)
                 w0 = 1
             for i, w in enumerate(hosted):
                 self.hub.push(w0 + i, self._own[(slot, w)], mode="borrow", n=Ep)
-        srcs = ([self._pin] if self._pin else []) + [self._own[(slot, w)] for w in hosted]
+        srcs = ([upstream] if upstream else []) + [self._own[(slot, w)] for w in hosted]
         stream = self.hub._stream(None)
         K = len(self.pieces)
+        if self.sync == "blocks":
+            # one persistent launch per rank: per-block flags order the stages
+            self._epoch += 1
+            ep = self._epoch
+            wait = (self._flags, ep) if self._flags else None
+            if self.last:
+                capi.phub_aggregate_range(self.hub.ctx, 0, Ep, stream, wait=wait, block=self.block)
+            else:
+                dst = self._pout if self.pull else self._next_in
+                capi.phub_partial_sum(self.hub.ctx, srcs, dst, 0, Ep, stream, wait=wait,
+                                      signal=(self._next_flags, ep), block=self.block)
+            self.barrier()                   # replicas complete; buffers free for the next round
+            return
         if self.sync == "flags":
             # all pieces enqueued at once; each launch waits (on the device) for the
             # previous rank's "piece ready" flag and raises the next rank's
@@ -524,6 +561,8 @@ class ChainShardedPHub:
             capi.phub_free_shared(self.device, p)
         if self._pin:
             capi.phub_free_shared(self.device, self._pin)
+        if self._pout:
+            capi.phub_free_shared(self.device, self._pout)
         if self._flags:
             capi.phub_free_shared(self.device, self._flags)
         self._own = {}

@@ -1,0 +1,88 @@
+"""Full-size multi-GPU parity worker (torchrun, NCCL): the exchange bench.py
+times at N > 1 (`--mode auto`: chained exchange with block-streaming flags at
+G = 2, owner-sharded P2P kernel above), at BASELINE.json's full model size,
+checked against the CPU oracle on sampled elements (the oracle computes them
+one by one from independently generated inputs).
+
+    torchrun --nproc-per-node G full_size_exchange_worker.py vgg19 [mode] [rounds]
+
+Every rank's pulled replica is checked at key starts/ends, chunk boundaries,
+owner-range and block boundaries and random elements.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_1805_07891_b200.sharded import ChainShardedPHub, P2PShardedPHub  # noqa: E402
+from workloads import grad_stream, manifest  # noqa: E402
+from workloads.generate import values_at_np, values_torch  # noqa: E402
+
+
+def sample(sizes, E, ranges, block, rng):
+    """Real-element indices: key starts/ends, 32 KB chunk starts, the elements
+    around owner-range and block boundaries (mapped back from the padded
+    layout), and 20000 random ones."""
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    pts = [rng.integers(0, E, 20000), starts[:-1], starts[1:] - 1]
+    for k in range(len(sizes)):
+        pts.append(np.arange(starts[k], starts[k + 1], 8192)[:32])
+    return np.unique(np.concatenate(pts)).astype(np.int64)
+
+
+def main():
+    name = sys.argv[1]
+    mode = sys.argv[2] if len(sys.argv) > 2 else "auto"
+    rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    N, cb = 8, 32768
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    dist.init_process_group("nccl", device_id=dev)
+    rank, G = dist.get_rank(), dist.get_world_size()
+    if mode == "auto":                       # bench.py --mode auto
+        mode = "chain" if G == 2 else "p2p"
+    sizes = manifest(name)
+    E = sum(sizes)
+    sh = (ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local) if mode == "chain"
+          else P2PShardedPHub(sizes, N, chunk_size_bytes=cb, device=local))
+    hub = sh.hub
+    idx = torch.as_tensor(hub.padded_index(), device=dev)
+    hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
+    for r in range(rounds):
+        g = sh.gradients(slot=r % 2)
+        for w in sh.hosted:
+            g[w].fill_(float("nan"))
+            g[w][idx] = values_torch(grad_stream(w) + 37 * r, 0, E, 25, dev)
+        sh.exchange(slot=r % 2)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(7 + rank)
+    samp = sample(sizes, E, None, None, rng)
+    got = sh.weights()[idx[torch.as_tensor(samp, device=dev)]].cpu().numpy()
+    w_ref = values_at_np(1, samp, 20)
+    v_ref = values_at_np(2, samp, 25)
+    for r in range(rounds):
+        gs = np.stack([values_at_np(grad_stream(w) + 37 * r, samp, 25) for w in range(N)])
+        w_ref, v_ref, _ = oracle.elems(gs, w_ref, v_ref, 0.1, 0.9)
+    ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
+    if mode == "chain" and sh.sync_timeouts() != 0:
+        ok = False
+    bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))
+    flag = torch.tensor([0 if ok else 1], device=dev)
+    dist.all_reduce(flag)
+    sh.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"rank {rank}/{G} {name} {mode} {samp.size} sampled: "
+          f"{'ok' if ok else f'MISMATCH {bad} elements'}")
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -33,12 +33,16 @@ def main():
     sizes = special[name] if name in special else manifest(name)
     E = sum(sizes)
     if mode.startswith("chain"):
-        sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=3,
-                              sync="barrier" if mode == "chain_barrier" else "flags")
+        # chain: block-streaming flags, partial pushed to the next rank;
+        # chain_pull: ... read by the next rank; chain_flags / chain_barrier: per piece
+        sync = {"chain": "blocks", "chain_pull": "blocks", "chain_flags": "flags",
+                "chain_barrier": "barrier"}[mode]
+        sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=3, sync=sync,
+                              block=2048, pull=mode == "chain_pull")
     else:
         cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
         sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
-    fused = mode in ("p2p", "chain", "chain_barrier")
+    fused = mode == "p2p" or mode.startswith("chain")
     w_ref, v_ref = values_np(1, 0, E, 20), values_np(2, 0, E, 25)
     sh.hub.load_state(w_ref, v_ref)
     idx = torch.as_tensor(sh.hub.padded_index(), device=dev)

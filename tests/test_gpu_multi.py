@@ -24,7 +24,8 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("mode", ["nccl", "p2p", "chain", "chain_barrier"])
+@pytest.mark.parametrize("mode", ["nccl", "p2p", "chain", "chain_pull", "chain_flags",
+                                  "chain_barrier"])
 @pytest.mark.parametrize("G,name,N,cb,rounds", [
     (2, "small", 8, 32768, 2), (2, "tiny", 4, 4096, 1), (4, "resnet50", 8, 32768, 2),
     (8, "resnet50", 8, 32768, 2), (8, "small", 8, 64, 1), (2, "one", 2, 32768, 2),
@@ -42,3 +43,25 @@ def test_sharded_exchange_bit_exact(G, name, N, cb, rounds, mode):
             break
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(": ok") == G
+
+
+FULL = os.path.join(ROOT, "tests", "dist", "full_size_exchange_worker.py")
+
+
+@pytest.mark.parametrize("G,mode", [(2, "auto"), (2, "p2p"), (4, "auto"), (4, "chain"),
+                                    (8, "auto")])
+def test_full_size_vgg19_exchange_sampled(G, mode):
+    """bench.py's N > 1 launch configuration at BASELINE.json's full VGG-19
+    size (2 rounds), every rank's replica checked against the oracle on
+    sampled elements."""
+    if _ngpus() < G:
+        pytest.skip(f"needs {G} GPUs, have {_ngpus()}")
+    for _attempt in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={G}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+               FULL, "vgg19", mode, "2"]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("sampled: ok") == G

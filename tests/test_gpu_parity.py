@@ -671,6 +671,76 @@ def test_stage_flags_signal_and_bounded_wait():
     tail.close()
 
 
+@pytest.mark.parametrize("block,mode", [(2048, "borrow"), (32768, "borrow"), (16384, "consume")])
+def test_block_streaming_flags_chain_on_one_gpu(block, mode):
+    """phub_sync block form: a partial sum raises one flag per block and a
+    range aggregate waits on them block by block (same stream here: the
+    producer finishes first, so no kernel waits on a co-resident one) --
+    bit-identical to the 6-worker oracle round; every flag raised exactly
+    to the epoch; a bad block size is refused; an unraised flag times out."""
+    from paper_1805_07891_b200 import PHub, PhubError, capi
+    sizes = manifest("resnet50")
+    E = sum(sizes)
+    w0, v0 = host_state(E, 12)
+    head = _hub(sizes, 3)
+    gd = device_grads(head, 6, 12)
+    Ep = head.E_padded
+    nblk = -(-Ep // block)
+    flags = torch.zeros(nblk + 1, dtype=torch.int32, device=DEV)
+    part = torch.empty(Ep, device=DEV)
+    st = head._stream(None)
+    with pytest.raises(PhubError):
+        capi.phub_partial_sum(head.ctx, [g.data_ptr() for g in gd[:3]], part.data_ptr(), 0, Ep,
+                              st, signal=(flags.data_ptr(), 3), block=1000)
+    capi.phub_partial_sum(head.ctx, [g.data_ptr() for g in gd[:3]], part.data_ptr(), 0, Ep, st,
+                          signal=(flags.data_ptr(), 3), block=block)
+    tail = PHub(sizes, 4, device=0, rescale=1.0 / 6, keep_aggregate=True)
+    tail.load_state(w0, v0)
+    tail.push(0, part, mode=mode)          # consume: its L2 lines may be discarded after reading
+    for k in range(3):
+        tail.push(1 + k, gd[3 + k])
+    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 3), block=block)
+    torch.cuda.synchronize()
+    assert tail.iteration == 1
+    f = flags.cpu().numpy()
+    assert (f[:nblk] == 3).all() and f[nblk] == 0
+    assert capi.phub_sync_timeouts(tail.ctx) == 0
+    w, v, s = tail.read_state()
+    rw, rv, rs = oracle.round_(sizes, host_grads(E, 6, 12), w0, v0, 0.1, 0.9)
+    assert_bits_equal(s, rs, "block-streamed aggregate")
+    assert_bits_equal(w, rw, "block-streamed w")
+    assert_bits_equal(v, rv, "block-streamed v")
+    # flags never raised for epoch 4: the waits expire once (~2 s), the work is skipped
+    for k in range(4):
+        tail.push(k, gd[k])
+    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 4), block=block)
+    torch.cuda.synchronize()
+    assert capi.phub_sync_timeouts(tail.ctx) >= 1
+    head.close()
+    tail.close()
+
+
+def test_consume_push_outside_block_streaming_is_a_borrow():
+    """PHUB_CONSUME on the flat (non-block) kernel reads like PHUB_BORROW and
+    leaves the buffer intact; per-key CONSUME pushes are plain borrows."""
+    hub = _hub(SMALL, 3, keep_aggregate=True)
+    w0, v0 = host_state(hub.E, 13)
+    hub.load_state(w0, v0)
+    gd = device_grads(hub, 3, 13)
+    keep = gd[0].clone()
+    hub.push(0, gd[0], mode="consume")
+    for w in (1, 2):
+        hub.push(w, gd[w], mode="consume" if w == 1 else "borrow")
+    hub.aggregate_optimize()
+    torch.cuda.synchronize()
+    w, v, s = hub.read_state()
+    rw, rv, rs = oracle.round_(SMALL, host_grads(hub.E, 3, 13), w0, v0, 0.1, 0.9)
+    assert_bits_equal(s, rs, "consume (flat) aggregate")
+    assert_bits_equal(w, rw, "consume (flat) w")
+    assert torch.equal(gd[0].nan_to_num(7.0), keep.nan_to_num(7.0))
+    hub.close()
+
+
 def test_push_batch_per_key_and_all_or_nothing():
     from paper_1805_07891_b200 import PhubError, capi
     sizes = SMALL
