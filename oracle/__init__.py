@@ -67,6 +67,12 @@ def _load():
             lib.oracle_elems.argtypes = [C.c_uint64, C.c_int32, f32p, f32p, f32p, C.c_void_p,
                                          C.c_float, C.c_float, C.c_float]
             lib.oracle_elems.restype = None
+            lib.oracle_hier_round.argtypes = [u64p, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                                              C.POINTER(C.c_void_p), f32p, f32p, C.c_void_p,
+                                              C.c_float, C.c_float, C.c_float]
+            lib.oracle_hier_elems.argtypes = [C.c_uint64, C.c_int32, C.c_int32, f32p, f32p, f32p,
+                                              C.c_void_p, C.c_float, C.c_float, C.c_float]
+            lib.oracle_hier_elems.restype = None
             lib.oracle_max_threads.restype = C.c_int
             _lib = lib
     return _lib
@@ -170,6 +176,42 @@ def elems(g, w, v, lr: float, mu: float, rescale: float = 0.0):
     v2 = np.array(v, dtype=np.float32, copy=True)
     s = np.zeros(m, np.float32)
     _load().oracle_elems(m, N, g.reshape(-1), w2, v2, s.ctypes.data, lr, mu, rescale)
+    return w2, v2, s
+
+
+def hier_round(key_sizes, rack_grads, w, v, lr: float, mu: float, rescale: float = 0.0,
+               chunk_bytes: int = 32768):
+    """Hierarchical reduction round (reading R17).
+
+    rack_grads: R sequences of P float32 arrays of E elements (worker k of rack
+    r).  Returns (w', v', s) with s = ((+0 + S_0) + S_1) + ... + S_{R-1} and
+    S_r the worker-order sum of rack r.
+    """
+    n = _u64(key_sizes)
+    E = int(n.sum())
+    R, P = len(rack_grads), len(rack_grads[0])
+    gs = [np.ascontiguousarray(g, dtype=np.float32) for rack in rack_grads for g in rack]
+    if any(len(rack) != P for rack in rack_grads) or any(g.shape != (E,) for g in gs):
+        raise OracleError("every rack needs P gradients of E elements")
+    ptrs = (C.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
+    w2 = np.array(w, dtype=np.float32, copy=True)
+    v2 = np.array(v, dtype=np.float32, copy=True)
+    agg = np.zeros(E, np.float32)
+    r = _load().oracle_hier_round(n, len(n), chunk_bytes, R, P, ptrs, w2, v2, agg.ctypes.data,
+                                  lr, mu, rescale)
+    if r != 0:
+        raise OracleError(f"oracle_hier_round -> {r}")
+    return w2, v2, agg
+
+
+def hier_elems(g, w, v, lr: float, mu: float, rescale: float = 0.0):
+    """hier_round's arithmetic on gathered elements: g is (R, P, m)."""
+    g = np.ascontiguousarray(g, dtype=np.float32)
+    R, P, m = g.shape
+    w2 = np.array(w, dtype=np.float32, copy=True)
+    v2 = np.array(v, dtype=np.float32, copy=True)
+    s = np.zeros(m, np.float32)
+    _load().oracle_hier_elems(m, R, P, g.reshape(-1), w2, v2, s.ctypes.data, lr, mu, rescale)
     return w2, v2, s
 
 

@@ -37,6 +37,13 @@
  *                         bound, chunk-size / order invariance.
  *   oracle_elems          the same per-element arithmetic on gathered
  *                         elements (for sampled full-size parity).
+ *   oracle_hier_round     P:746-763 (rack deployment, hierarchical reduction:
+ *   oracle_hier_elems     per-rack aggregation, cross-rack aggregation, then
+ *                         the optimizer), P:1008 (cross-rack accumulation one
+ *                         rack after another).  Pinned: R = 1 and one worker
+ *                         per rack reduce to oracle_round; dyadic inputs ==
+ *                         exact float64 sum; a hand-computed case where the
+ *                         two-level order differs from the flat one.
  *
  * The Nesterov recurrence is not printed in the paper (P:783 only names
  * "Nesterov's accelerated gradient method"); this oracle implements SPEC's
@@ -256,6 +263,88 @@ void oracle_elems(uint64_t count, int32_t N, const float* g, float* w, float* v,
     for (uint64_t i = 0; i < count; ++i) {
         float merge = 0.0f;
         for (int32_t wk = 0; wk < N; ++wk) merge = merge + g[(uint64_t)wk * count + i];
+        float gg = merge * rescale;
+        float t1 = mu * v[i];
+        float vn = t1 + gg;
+        float t2 = mu * vn;
+        float t3 = gg + t2;
+        float t4 = lr * t3;
+        w[i] = w[i] - t4;
+        v[i] = vn;
+        if (agg) agg[i] = merge;
+    }
+}
+
+/* ------------------------------------------- hierarchical reduction (NEXT-4) */
+/* PHub's rack deployment: "each PBox centrally aggregates gradient
+ * updates from workers in the same rack; then, the PBox nodes start
+ * cross-rack aggregation and compute globally aggregated gradients; finally,
+ * each per-rack PBox runs an optimizer on this gradient".  The
+ * paper's own emulation of the cross-rack step sends "N chunk-size messages
+ * sequentially, each performing one additional aggregation", i.e. the
+ * racks' aggregates are accumulated one rack after another (reading R17):
+ *   rack r:   S_r = ((+0 + g_{rP}) + g_{rP+1}) + ... + g_{rP+P-1}
+ *   global:   s   = ((+0 + S_0) + S_1) + ... + S_{R-1}
+ *   then the same optimizer as oracle_chunk, rescale default 1/(R*P).
+ * grads[r*P + k] is worker k of rack r.  Same layout/outputs as oracle_round. */
+int oracle_hier_round(const uint64_t* n, int32_t K, uint64_t chunk_bytes, int32_t R, int32_t P,
+                      const float* const* grads, float* w, float* v, float* agg,
+                      float lr, float mu, float rescale)
+{
+    if (R < 1 || P < 1 || grads == NULL || w == NULL || v == NULL) return ORACLE_ERR_ARG;
+    int64_t count = oracle_chunk_count(n, K, chunk_bytes);
+    if (count < 0) return (int)count;
+    uint64_t ce = chunk_bytes / 4;
+    if (rescale == 0.0f) rescale = 1.0f / (float)(R * P);
+    float* merge = (float*)malloc(sizeof(float) * (size_t)ce);
+    float* rack = (float*)malloc(sizeof(float) * (size_t)ce);
+    if (!merge || !rack) { free(merge); free(rack); return ORACLE_ERR_ARG; }
+    uint64_t acc = 0;
+    for (int32_t k = 0; k < K; ++k) {
+        for (uint64_t off = 0; off < n[k]; off += ce) {          /* one chunk (vkey) */
+            const uint64_t base = acc + off;
+            const uint64_t len = (n[k] - off < ce) ? (n[k] - off) : ce;
+            for (uint64_t j = 0; j < len; ++j) merge[j] = 0.0f;
+            for (int32_t r = 0; r < R; ++r) {                      /* step 1: per rack */
+                for (uint64_t j = 0; j < len; ++j) rack[j] = 0.0f;
+                for (int32_t wk = 0; wk < P; ++wk) {
+                    const float* g = grads[r * P + wk] + base;
+                    for (uint64_t j = 0; j < len; ++j) rack[j] = rack[j] + g[j];
+                }
+                for (uint64_t j = 0; j < len; ++j) merge[j] = merge[j] + rack[j];  /* step 2 */
+            }
+            for (uint64_t j = 0; j < len; ++j) {                   /* step 3: optimizer */
+                float g = merge[j] * rescale;
+                float t1 = mu * v[base + j];
+                float vn = t1 + g;
+                float t2 = mu * vn;
+                float t3 = g + t2;
+                float t4 = lr * t3;
+                float wn = w[base + j] - t4;
+                v[base + j] = vn;
+                w[base + j] = wn;
+                if (agg) agg[base + j] = merge[j];
+            }
+        }
+        acc += n[k];
+    }
+    free(merge);
+    free(rack);
+    return 0;
+}
+
+/* oracle_hier_round's arithmetic on gathered elements: g[(r*P + k)*count + i]. */
+void oracle_hier_elems(uint64_t count, int32_t R, int32_t P, const float* g, float* w, float* v,
+                       float* agg, float lr, float mu, float rescale)
+{
+    if (rescale == 0.0f) rescale = 1.0f / (float)(R * P);
+    for (uint64_t i = 0; i < count; ++i) {
+        float merge = 0.0f;
+        for (int32_t r = 0; r < R; ++r) {
+            float rack = 0.0f;
+            for (int32_t wk = 0; wk < P; ++wk) rack = rack + g[(uint64_t)(r * P + wk) * count + i];
+            merge = merge + rack;
+        }
         float gg = merge * rescale;
         float t1 = mu * v[i];
         float vn = t1 + gg;
