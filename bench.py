@@ -9,9 +9,11 @@ One step = one full parameter-exchange round of the 8-worker job: every
 worker's push, the fused tall aggregation + Nesterov update of every chunk,
 and the pull.  N = 1: all 8 workers' gradients are resident in HBM and pushed
 zero-copy (mode M1).  N > 1: one process per GPU, 8/N workers per
-GPU, chunks sharded by owner; push = NCCL grouped send/recv of each worker's
-slices to their owners, pull = NCCL all-gather of the owners' updated ranges
-(mode M3).  Total work is fixed as N grows ("scaling": "strong").
+GPU, chunks sharded by owner (mode M3); `--mode auto` runs the block-streamed
+chained exchange at N = 2 and the owner-sharded peer-memory kernel above
+(DESIGN.md 8.2); NCCL send/recv and an NCCL all-reduce baseline are options.
+Total work is fixed as N grows ("scaling": "strong").  `--mode hier` is the
+hierarchical reduction (one 8-worker rack per GPU, weak scaling, NEXT-4).
 
 metric: aggregated gradient GB/s = 8 * 4E / t_step (plus exchanges/s = 8 / t_step).
 Prints ONE JSON line (rank 0).
@@ -60,14 +62,20 @@ def parse():
     ap.add_argument("--chain-sync", default="blocks", choices=["blocks", "flags", "barrier"])
     ap.add_argument("--chain-block", type=int, default=16384,
                     help="chain mode: elements per block flag (sync=blocks)")
+    ap.add_argument("--hier-block", type=int, default=32768,
+                    help="hier mode: elements per block flag")
     ap.add_argument("--chain-pull", action="store_true",
                     help="chain mode: next rank reads the partial over NVLink (default: pushed)")
     ap.add_argument("--chain-no-consume", action="store_true",
                     help="chain mode: push the incoming partial as BORROW, not CONSUME")
     ap.add_argument("--chain-producer-grid", type=int, default=0,
                     help="chain mode: CTAs of the partial-sum launch on non-last ranks")
-    ap.add_argument("--mode", default="auto", choices=["auto", "p2p", "chain", "nccl", "allreduce"],
-                    help="N>1 exchange: fused peer-memory kernel (p2p) or NCCL send/recv")
+    ap.add_argument("--mode", default="auto",
+                    choices=["auto", "p2p", "chain", "nccl", "allreduce", "hier"],
+                    help="N>1 exchange of the 8-worker job: chained (chain) or owner-sharded "
+                         "(p2p) peer-memory kernels, NCCL send/recv (nccl), NCCL all-reduce "
+                         "baseline (allreduce); hier: hierarchical reduction, one 8-worker "
+                         "rack per GPU (SURVEY NEXT-4, weak scaling)")
     return ap.parse_args()
 
 
@@ -324,7 +332,7 @@ def bench_multi(args, mname, N, cb):
     mode nccl: NCCL grouped send/recv push, fused kernel, NCCL all-gather-v pull."""
     import torch
     import torch.distributed as dist
-    from paper_1805_07891_b200.sharded import (AllReduceBaseline, ChainShardedPHub,
+    from paper_1805_07891_b200.sharded import (AllReduceBaseline, ChainShardedPHub, HierPHub,
                                                P2PShardedPHub, ShardedPHub)
     from workloads import grad_stream, manifest
     from workloads.generate import values_torch
@@ -337,11 +345,16 @@ def bench_multi(args, mname, N, cb):
     sizes = manifest(mname)
     if args.mode == "auto":      # fewest NVLink bytes: chain at G = 2, owner-sharded P2P above
         args.mode = "chain" if G == 2 else "p2p"
-    chain = args.mode == "chain"
-    p2p = args.mode in ("p2p", "chain")
+    hier = args.mode == "hier"
+    chain = args.mode in ("chain", "hier")      # the whole round is one exchange() call
+    p2p = args.mode in ("p2p", "chain", "hier")
     ar = args.mode == "allreduce"
+    NT = N * G if hier else N                   # workers in the job
     try:
-        if chain:
+        if hier:
+            sh = HierPHub(sizes, workers_per_rack=N, chunk_size_bytes=cb, device=local,
+                          block=args.hier_block)
+        elif chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
                                   sync=args.chain_sync, block=args.chain_block,
                                   pull=args.chain_pull, consume=not args.chain_no_consume)
@@ -358,7 +371,7 @@ def bench_multi(args, mname, N, cb):
         print(f"[bench] p2p exchange unavailable ({e}); using the NCCL exchange", file=sys.stderr)
         args.mode, p2p, chain = "nccl", False, False
         sh = ShardedPHub(sizes, N, chunk_size_bytes=cb, device=local)
-    hub, plan = sh.hub, sh.plan
+    hub, plan = sh.hub, getattr(sh, "plan", None)
     from paper_1805_07891_b200 import capi
     if args.grid:
         hub.set_option(capi.PHUB_OPT_GRID, args.grid)
@@ -382,7 +395,7 @@ def bench_multi(args, mname, N, cb):
     grads = sh.gradients() if p2p else {}
     for w in sh.hosted:
         b = grads[w] if p2p else torch.zeros(Ep, dtype=torch.float32, device=dev)
-        b[idx] = values_torch(grad_stream(w), 0, E, 25, dev)
+        b[idx] = values_torch(grad_stream(rank * N + w if hier else w), 0, E, 25, dev)
         grads[w] = b
     del idx
     torch.cuda.synchronize()
@@ -442,13 +455,18 @@ def bench_multi(args, mname, N, cb):
         raise RuntimeError("chained exchange: device-side waits timed out")
     mine = {"rank": rank, "ms": t0.elapsed_time(t1) / args.steps,
             "k_ms": sum(a.elapsed_time(b) for a, b in ev) / args.steps,
-            "owned": hub.owned_elements(), "out": plan.nvlink_bytes_out(),
-            "in": plan.nvlink_bytes_in(), "launches": launches, "clocks": clocks.summary()}
-    if chain:   # one partial per link per round; the last rank stores w' into G-1 replicas
+            "owned": hub.owned_elements(), "launches": launches, "clocks": clocks.summary()}
+    if plan is not None:
+        mine["out"], mine["in"] = plan.nvlink_bytes_out(), plan.nvlink_bytes_in()
+    if hier:    # rack aggregate of every other owner's range out, w' of the own range to G-1
+        ob, oe = hub.owner_range()
+        mine["out"] = 4 * (Ep - (oe - ob)) + 4 * (oe - ob) * (G - 1)
+        mine["in"] = 4 * (oe - ob) * (G - 1) + 4 * (Ep - (oe - ob))
+    elif chain:  # one partial per link per round; the last rank stores w' into G-1 replicas
         from paper_1805_07891_b200.sharded import chain_nvlink_bytes
         mine["out"], mine["in"] = chain_nvlink_bytes(Ep, G, rank)
     if p2p:     # M2: the owner kernel alone on resident slices (NCCL mode: its k_ms already is)
-        mine["m2_ms"], mine["m2_owned"] = owner_phase_ms(sizes, N, cb, rank, G, args.steps,
+        mine["m2_ms"], mine["m2_owned"] = owner_phase_ms(sizes, NT, cb, rank, G, args.steps,
                                                          args.warmup, dev)
     else:
         mine["m2_ms"], mine["m2_owned"] = mine["k_ms"], mine["owned"]
@@ -509,8 +527,8 @@ def bench_multi(args, mname, N, cb):
         t = torch.tensor([a.elapsed_time(b) / args.e2e_steps], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item()) / 1e3
-        e2e = {"value": round(N * 4 * E / te / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": N * 4 * Ep, "d2h_bytes_per_step": N * 4 * Ep,
+        e2e = {"value": round(NT * 4 * E / te / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": NT * 4 * Ep, "d2h_bytes_per_step": NT * 4 * Ep,
                "steps": args.e2e_steps, "ms_per_step": round(te * 1e3, 3),
                "path": f"{type(sh).__name__}: H2D of hosted grads -> exchange ({args.mode}) -> "
                        f"D2H of the replica per hosted worker" +
@@ -520,11 +538,11 @@ def bench_multi(args, mname, N, cb):
         ms_step = max(r["ms"] for r in allr)
         k_ms = max(r["k_ms"] for r in allr)
         t_step = ms_step / 1e3
-        value = N * 4 * E / t_step / 1e9
+        value = NT * 4 * E / t_step / 1e9
         slow = max(allr, key=lambda r: r["k_ms"])
         m2_slow = max(allr, key=lambda r: r["m2_ms"])
         m2_ms = m2_slow["m2_ms"]
-        achieved = (4 * N + 16) * slow["owned"] / (slow["k_ms"] / 1e3) / 1e9
+        achieved = (4 * NT + 16) * slow["owned"] / (slow["k_ms"] / 1e3) / 1e9
         peak, peak_src = measured_peaks()
         nv_bytes = max(max(r["out"], r["in"]) for r in allr) if not ar else \
             int(2 * (G - 1) / G * 4 * Ep)              # ring all-reduce bytes per direction
@@ -534,12 +552,17 @@ def bench_multi(args, mname, N, cb):
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": G,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": round(value / PAPER_GBS, 2), "dtype": "f32", "data": "synthetic",
-            "exchanges_per_s": round(N / t_step, 1),
+            "higher_is_better": True, "scaling": "weak" if hier else "strong",
+            "vs_baseline": None if hier else round(value / PAPER_GBS, 2), "dtype": "f32",
+            "data": "synthetic", "exchanges_per_s": round(NT / t_step, 1),
             "config": {"workload": args.config, "keys": len(sizes), "E": E, "E_padded": Ep,
-                       "workers": N, "workers_per_gpu": N // G, "chunk_bytes": cb,
-                       "mode": (f"M3 (full exchange) chain: rank-ordered partial sums over "
+                       "workers": NT, "workers_per_gpu": NT // G, "chunk_bytes": cb,
+                       "mode": (f"NEXT-4 hierarchical reduction (P:746-763): one rack of {N} "
+                                f"workers per GPU ({NT} in all), rack aggregate -> cross-rack "
+                                f"aggregation in rack order over NVLink -> Nesterov on owner "
+                                f"ranges + w' into every rack's replica; one launch per GPU, "
+                                f"{args.hier_block}-element blocks") if hier else
+                               (f"M3 (full exchange) chain: rank-ordered partial sums over "
                                 f"NVLink, last rank fused Nesterov + replica stores, " +
                                 (f"one launch per rank streamed by per-block device flags "
                                  f"({args.chain_block} elements/block, partial "
@@ -563,14 +586,16 @@ def bench_multi(args, mname, N, cb):
                         "range resident in its HBM (pushes landed by DMA, P:895/P:933); "
                         "max over ranks; NOT the headline (no NVLink transfer)",
                 "kernel_ms": round(m2_ms, 4),
-                "value": round(N * 4 * E / (m2_ms / 1e3) / 1e9, 1), "unit": "GB/s",
-                "hbm_frac": round((4 * N + 16) * m2_slow["m2_owned"] / (m2_ms / 1e3) / 1e9 /
+                "value": round(NT * 4 * E / (m2_ms / 1e3) / 1e9, 1), "unit": "GB/s",
+                "hbm_frac": round((4 * NT + 16) * m2_slow["m2_owned"] / (m2_ms / 1e3) / 1e9 /
                                   measured_peaks()[0], 4)},
             "roofline": ({"bound": "nvlink", "achieved": round(nv_bytes / (k_ms / 1e3) / 1e9, 1),
                           "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                           "frac": round(nv_bytes / (k_ms / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
                           "traffic": None,
-                          "kernel": ("chained exchange round (partial-sum + fused kernels, "
+                          "kernel": ("hierarchical exchange round (k_hier, incl. the "
+                                     "end barrier)") if hier else
+                                    ("chained exchange round (partial-sum + fused kernels, "
                                      "incl. barriers)") if chain else
                                     ("fused exchange kernel (k_flat with peer loads/stores), "
                                      "slowest owner"), "kernel_ms": round(k_ms, 4),

@@ -314,6 +314,48 @@ phub_status phub_sync_timeouts(phub_ctx ctx, uint32_t* count);
  * at aggregate time. */
 phub_status phub_set_replicas(phub_ctx ctx, float* const* replicas, int32_t count);
 
+/* Hierarchical reduction across racks: each
+ * GPU (context) is one rack's PBox whose N local workers pushed their whole
+ * model (PHUB_ALL_KEYS, BORROW, 32-B aligned) this iteration; the context has
+ * CONTIG ownership over G = num_racks owners and owner_rank = this rack.
+ * One launch performs the paper's three steps for the whole model:
+ *   1. per rack:   S_rack = ((+0 + g_0) + g_1) + ... + g_{N-1}  (local workers)
+ *   2. cross rack: every other rack's S over this owner's range arrives in
+ *                  this owner's inbox (their launches store it over NVLink);
+ *                  s = ((+0 + S_0) + S_1) + ... + S_{G-1}  in rack order, the
+ *                  rack-by-rack accumulation of the paper's emulation (P:1008,
+ *                  reading R17)
+ *   3. optimizer:  Nesterov on the owned range with g = s * rescale (set
+ *                  rescale = 1/(G*N) for the mean over all workers), w'
+ *                  stored locally and into every replica registered with
+ *                  phub_set_replicas (the per-rack broadcast).
+ * while its own step-1 sums for the OTHER owners' ranges are stored into their
+ * inboxes.  Work is cut into blocks of `block_elems` (multiple of 2048) of each
+ * owner range; per block and source rack a uint32 flag (system-scope release /
+ * acquire, value `epoch`) orders arrival.  Bounded waits as phub_sync.
+ *   inbox[q]       device pointer such that inbox[q] + x is this owner's
+ *                  receive slot for rack q's element x (x in the owned padded
+ *                  range); inbox[rack] unused.  Two slots alternated by the
+ *                  caller per epoch parity (a rack may run one round ahead).
+ *   peer_inbox[o]  peer-mapped: owner o's receive slot for THIS rack, same
+ *                  addressing over o's range; [rack] unused.
+ *   flags          this owner's flags, ceil(owned / block_elems) x num_racks
+ *                  uint32, zero before the first epoch; never reset.
+ *   peer_flags[o]  peer-mapped flags of owner o.
+ *   epoch          1, 2, 3, ... (strictly increasing per round).
+ * Completes the iteration.  The caller orders rounds so every replica write
+ * of round k is complete before its replica is read (e.g. a barrier after). */
+typedef struct {
+    int32_t num_racks;
+    uint64_t block_elems;
+    const float* const* inbox;
+    float* const* peer_inbox;
+    const uint32_t* flags;
+    uint32_t* const* peer_flags;
+    uint32_t epoch;
+} phub_hier;
+phub_status phub_hier_exchange(phub_ctx ctx, const phub_hier* h, void* stream);
+
 /* Shared device allocations that can be exported to peer processes.
  * phub_alloc_shared: cudaMalloc of `bytes` on `device` (whole allocation, so an
  * IPC handle maps exactly this buffer).  phub_free_shared releases it. */

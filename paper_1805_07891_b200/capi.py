@@ -45,6 +45,13 @@ class phub_sync(C.Structure):
                 ("block_elems", C.c_uint64)]
 
 
+class phub_hier(C.Structure):
+    _fields_ = [("num_racks", C.c_int32), ("block_elems", C.c_uint64),
+                ("inbox", C.POINTER(C.c_void_p)), ("peer_inbox", C.POINTER(C.c_void_p)),
+                ("flags", C.c_void_p), ("peer_flags", C.POINTER(C.c_void_p)),
+                ("epoch", C.c_uint32)]
+
+
 class phub_config(C.Structure):
     _fields_ = [
         ("key_num_elements", C.POINTER(C.c_uint64)),
@@ -102,6 +109,7 @@ _SIGS = {
     "phub_kernel_launches": (C.c_int, [phub_ctx, _u64p]),
     "phub_set_option": (C.c_int, [phub_ctx, C.c_int32, C.c_int64]),
     "phub_set_replicas": (C.c_int, [phub_ctx, C.POINTER(C.c_void_p), C.c_int32]),
+    "phub_hier_exchange": (C.c_int, [phub_ctx, C.c_void_p, C.c_void_p]),
     "phub_alloc_shared": (C.c_int, [C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)]),
     "phub_free_shared": (C.c_int, [C.c_int32, C.c_void_p]),
     "phub_ipc_get_handle": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p]),
@@ -318,6 +326,18 @@ def phub_set_option(ctx, option: int, value: int):
 def phub_set_replicas(ctx, ptrs):
     arr = (C.c_void_p * max(len(ptrs), 1))(*ptrs)
     _check(_lib.phub_set_replicas(ctx, arr, len(ptrs)), "phub_set_replicas", ctx)
+
+
+def phub_hier_exchange(ctx, num_racks: int, block: int, inbox, peer_inbox, flags: int,
+                       peer_flags, epoch: int, stream: int = 0):
+    """Hierarchical reduction round (phub.h phub_hier_exchange); pointer lists
+    have num_racks entries (this rack's entry ignored, may be 0)."""
+    R = int(num_racks)
+    def arr(xs):
+        return (C.c_void_p * max(R, 1))(*[int(x or 0) for x in xs]) if xs else None
+    ib, pib, pf = arr(inbox), arr(peer_inbox), arr(peer_flags)     # alive across the call
+    h = phub_hier(R, int(block), ib, pib, flags or None, pf, int(epoch))
+    _check(_lib.phub_hier_exchange(ctx, C.byref(h), stream), "phub_hier_exchange", ctx)
 
 
 def phub_alloc_shared(device: int, nbytes: int) -> int:

@@ -95,6 +95,7 @@ struct phub_ctx_s {
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     int blocks_occ[2][phub::kMaxWorkers + 1] = {};   // resident CTAs/SM of k_blocks [nag][nw]
+    int hier_occ = 0;                                  // resident CTAs/SM of k_hier
     uint64_t iteration = 0;
     int launches = 0;
     uint64_t launches_total = 0;
@@ -1113,6 +1114,75 @@ phub_status phub_set_replicas(phub_ctx c, float* const* replicas, int32_t count)
     if (count && !contig_mode(c))
         return c->fail(PHUB_ERR_UNSUPPORTED, "replicas need CONTIG ownership");
     c->replicas.assign(replicas, replicas + count);
+    return PHUB_OK;
+}
+
+phub_status phub_hier_exchange(phub_ctx c, const phub_hier* h, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (c->failed) return PHUB_ERR_CUDA;
+    if (!h || h->num_racks != c->G || h->num_racks > phub::kMaxRacks)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "num_racks must equal the context's owners (<= %d)",
+                       phub::kMaxRacks);
+    if (!contig_mode(c) || c->ce % 8 || c->N > phub::kMaxWorkers)
+        return c->fail(PHUB_ERR_UNSUPPORTED, "hierarchical exchange needs CONTIG ownership, "
+                       "chunks of a multiple of 32 B and <= %d local workers", phub::kMaxWorkers);
+    if (!h->block_elems || h->block_elems % 2048)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block_elems must be a positive multiple of 2048");
+    if (h->epoch == 0) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "epoch must be >= 1");
+    const int R = h->num_racks, me = c->rank;
+    if (R > 1 && (!h->inbox || !h->peer_inbox || !h->flags || !h->peer_flags))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "inbox / flag pointers required for > 1 rack");
+    for (int q = 0; R > 1 && q < R; ++q)
+        if (q != me && (!h->inbox[q] || !h->peer_inbox[q] || !h->peer_flags[q]))
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "rack %d: inbox / peer pointers missing", q);
+    if (c->got_count != (uint64_t)c->K * c->N)
+        return c->fail(PHUB_ERR_INCOMPLETE, "%llu of %llu (worker,key) pushes received (S:181)",
+                       (unsigned long long)c->got_count,
+                       (unsigned long long)((uint64_t)c->K * c->N));
+    if (c->range_cursor != UINT64_MAX || c->done_count)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "iteration is being aggregated otherwise");
+    phub::HierArgs a{};
+    for (int w = 0; w < c->N; ++w) {
+        const uintptr_t b0 = c->base[(size_t)w * c->K];
+        for (int k = 1; k < c->K; ++k)
+            if (c->base[(size_t)w * c->K + k] != b0 || b0 % 32)
+                return c->fail(PHUB_ERR_UNSUPPORTED, "worker %d: whole-model 32-B aligned push "
+                               "required", w);
+        a.g[w] = reinterpret_cast<const float*>(b0);
+    }
+    a.nw = c->N;
+    a.R = R;
+    a.rack = me;
+    a.w = c->d_w;
+    a.v = c->d_v;
+    a.agg = c->keep_agg ? c->d_agg : nullptr;
+    a.lr = c->lr;
+    a.mu = c->mu;
+    a.rescale = c->rescale;
+    a.nrep = (int)c->replicas.size();
+    for (int r = 0; r < a.nrep; ++r) a.rep[r] = c->replicas[r];
+    for (int o = 0; o < R; ++o) {
+        a.own_begin[o] = c->own_begin[o];
+        a.own_end[o] = c->own_end[o];
+        if (o != me && R > 1) {
+            a.inbox[o] = h->inbox[o];
+            a.peer_inbox[o] = h->peer_inbox[o];
+            a.peer_flags[o] = h->peer_flags[o];
+        }
+    }
+    a.block = h->block_elems;
+    a.flags = R > 1 ? h->flags : nullptr;
+    a.epoch = h->epoch;
+    a.ticket = c->d_sync + 3;
+    a.timeouts = c->d_sync + 1;
+    DeviceGuard g(c->device);
+    c->launches = 0;
+    if (!c->hier_occ) c->hier_occ = phub::hier_blocks_per_sm(c->N);
+    const int grid = c->grid_override ? c->grid_override : c->num_sms * c->hier_occ;
+    cudaError_t e = phub::launch_hier(a, grid, static_cast<cudaStream_t>(stream), &c->launches);
+    c->launches_total += (uint64_t)c->launches;
+    if (e != cudaSuccess) return c->cuda_fail(e, "hierarchical exchange launch");
+    end_iteration(c);
     return PHUB_OK;
 }
 

@@ -531,6 +531,178 @@ void* pick_blocks(int nw) {
     }
 }
 
+// ------------------------------------------- hierarchical reduction (NEXT-4)
+// PHub's rack deployment: each GPU is one rack's PBox holding its
+// P workers' gradients.  One persistent launch per rack and round walks a
+// ticket-ordered item list; for block index j the items are
+//   produce(o, j), o != rack:  S_rack = worker-order sum of the local workers
+//                              over owner o's block j, stored straight into o's
+//                              inbox over NVLink, then o's flag [j][rack] raised;
+//   consume(j):                once every other rack's flag for block j is up,
+//                              s = ((+0 + S_0) + S_1) + ... + S_{R-1} in rack
+//                              order (own S computed here), Nesterov, w' stored
+//                              locally and into every peer replica.
+// Deadlock-free: produce items never wait, and tickets are taken in item order,
+// so every produce item a waiting consume item needs has already been taken by
+// a running CTA on its rack.
+template <int NW>
+__device__ __forceinline__ void local_sum(const HierArgs& a, uint64_t i, float acc[8]) {
+    const int nw = NW > 0 ? NW : a.nw;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    if constexpr (NW > 0) {
+        V8 gv[NW];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) gv[k] = ld_grad(reinterpret_cast<const V8*>(a.g[k]) + i);
+#pragma unroll
+        for (int k = 0; k < NW; ++k)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+    } else {
+        for (int k0 = 0; k0 < nw; k0 += 8) {
+            V8 gv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < nw) gv[k] = ld_grad(reinterpret_cast<const V8*>(a.g[k0 + k]) + i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < nw) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+                }
+        }
+    }
+}
+
+// acc += inbox[q] for q in [q0, q1), in rack order (loads batched 4 at a time)
+__device__ __forceinline__ void add_racks(const HierArgs& a, uint64_t i, int q0, int q1,
+                                          float acc[8]) {
+    for (int b = q0; b < q1; b += 4) {
+        V8 rv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (b + k < q1) rv[k] = ld_coherent(reinterpret_cast<const V8*>(a.inbox[b + k]) + i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (b + k < q1) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], rv[k].x[j]);
+            }
+    }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kThreads, 2) k_hier(const __grid_constant__ HierArgs a) {
+    const uint64_t B = a.block;
+    const int R = a.R;
+    uint64_t J = 0;                                    // blocks of the largest owner range
+    for (int o = 0; o < R; ++o) {
+        const uint64_t n = (a.own_end[o] - a.own_begin[o] + B - 1) / B;
+        J = n > J ? n : J;
+    }
+    const uint64_t items = J * (uint64_t)R;
+    __shared__ uint64_t s_item;
+    __shared__ int ok;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(a.ticket, 1u);
+        __syncthreads();
+        const uint64_t t = s_item;
+        if (t >= items) break;
+        const uint64_t j = t / R;
+        const int k = (int)(t % R);
+        if (k < R - 1) {                               // ---- produce(o, j)
+            const int o = (a.rack + 1 + k) % R;
+            const uint64_t lo = a.own_begin[o] + j * B;
+            const uint64_t hi = lo + B < a.own_end[o] ? lo + B : a.own_end[o];
+            if (lo < hi) {
+                V8* dst = reinterpret_cast<V8*>(a.peer_inbox[o]);
+                for (uint64_t i = lo / 8 + threadIdx.x; i < hi / 8; i += kThreads) {
+                    float acc[8];
+                    local_sum<NW>(a, i, acc);
+                    V8 out;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) out.x[e] = acc[e];
+                    dst[i] = out;
+                }
+                __syncthreads();                       // bar.sync + one fence (cumulative)
+                if (threadIdx.x == 0) {
+                    __threadfence_system();
+                    st_release_sys(a.peer_flags[o] + j * R + a.rack, a.epoch);
+                }
+            }
+        } else {                                       // ---- consume(j)
+            const uint64_t lo = a.own_begin[a.rack] + j * B;
+            const uint64_t hi = lo + B < a.own_end[a.rack] ? lo + B : a.own_end[a.rack];
+            if (lo < hi) {
+                if (threadIdx.x == 0) {
+                    int good = 1;
+                    volatile uint32_t* abandoned = a.timeouts + 1;
+                    const uint64_t t0 = globaltimer_ns();
+                    for (int q = 0; q < R && good; ++q) {
+                        if (q == a.rack) continue;
+                        const uint32_t* f = a.flags + j * R + q;
+                        while (ld_acquire_sys(f) < a.epoch) {
+                            if (*abandoned >= a.epoch) { good = 0; break; }
+                            if (globaltimer_ns() - t0 > 2000000000ull) {
+                                atomicAdd(a.timeouts, 1u);
+                                atomicMax(a.timeouts + 1, a.epoch);
+                                good = 0;
+                                break;
+                            }
+                            __nanosleep(100);
+                        }
+                    }
+                    ok = good;
+                }
+                __syncthreads();
+                if (ok) {
+                    V8* w = reinterpret_cast<V8*>(a.w);
+                    V8* v = reinterpret_cast<V8*>(a.v);
+                    for (uint64_t i = lo / 8 + threadIdx.x; i < hi / 8; i += kThreads) {
+                        float acc[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+                        add_racks(a, i, 0, a.rack, acc);             // S_0 .. S_{rack-1}
+                        float own[8];
+                        local_sum<NW>(a, i, own);                  // S_rack, from +0
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], own[e]);
+                        add_racks(a, i, a.rack + 1, R, acc);       // S_{rack+1} .. S_{R-1}
+                        V8 wv = ld_state<PHUB_CACHE_ENABLED>(w + i);
+                        V8 vv = ld_state<PHUB_CACHE_ENABLED>(v + i);
+                        V8 sv;
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            sv.x[e] = acc[e];
+                            nag(acc[e], wv.x[e], vv.x[e], a.lr, a.mu, a.rescale);
+                        }
+                        st_stream(w + i, wv);
+                        st_stream(v + i, vv);
+                        if (a.agg) st_stream(reinterpret_cast<V8*>(a.agg) + i, sv);
+                        for (int r = 0; r < a.nrep; ++r) reinterpret_cast<V8*>(a.rep[r])[i] = wv;
+                    }
+                }
+            }
+        }
+        __syncthreads();                               // s_item / ok retire before the next item
+    }
+    if (a.nrep) __threadfence_system();
+    if (threadIdx.x == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x - 1) {
+        a.ticket[0] = 0;
+        a.ticket[1] = 0;
+    }
+}
+
+void* pick_hier(int nw) {
+    switch (nw) {
+        case 1: return (void*)k_hier<1>;
+        case 2: return (void*)k_hier<2>;
+        case 4: return (void*)k_hier<4>;
+        case 8: return (void*)k_hier<8>;
+        default: return (void*)k_hier<0>;
+    }
+}
+
 // ------------------------------------------------ bulk-copy (TMA) staging
 // Variant with the loads taken off the register file: one producer thread per
 // CTA streams each tile's N gradient slices and the w, v slices into a
@@ -833,6 +1005,20 @@ cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t 
     void* fn = dst ? pick_blocks<false>(a.nw) : pick_blocks<true>(a.nw);
     void* args[] = {const_cast<FlatArgs*>(&a), &dst};
     cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);
+    ++*launches;
+    return e;
+}
+
+int hier_blocks_per_sm(int nw) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pick_hier(nw), kThreads, 0) != cudaSuccess)
+        return 1;
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launches) {
+    void* args[] = {const_cast<HierArgs*>(&a)};
+    cudaError_t e = cudaLaunchKernel(pick_hier(a.nw), dim3(grid), dim3(kThreads), args, 0, s);
     ++*launches;
     return e;
 }

@@ -41,6 +41,32 @@ struct FlatArgs {
     uint32_t* ticket;                 // [0] next block, [1] CTAs done (block streaming, zeroed)
 };
 
+// Hierarchical reduction: one GPU = one rack's PBox with its P
+// local workers; R racks exchange rack aggregates over NVLink by owner range.
+constexpr int kMaxRacks = 16;
+struct HierArgs {
+    const float* g[kMaxWorkers];      // this rack's workers (padded-layout bases)
+    int nw;                           // P
+    int R, rack;
+    float* w;
+    float* v;
+    float* agg;                       // nullptr unless keep_aggregate (owned range)
+    float lr, mu, rescale;
+    int nrep;
+    float* rep[kMaxReplicas];         // peer replicas receiving w' of the owned range
+    uint64_t own_begin[kMaxRacks], own_end[kMaxRacks];
+    uint64_t block;                   // elements per block (multiple of 2048)
+    const float* inbox[kMaxRacks];    // this owner's inbox per source rack (padded-based)
+    float* peer_inbox[kMaxRacks];     // owner o's inbox slot for this rack (padded-based)
+    const uint32_t* flags;            // this owner's arrival flags [block * R + source rack]
+    uint32_t* peer_flags[kMaxRacks];  // owner o's arrival flags (peer-mapped)
+    uint32_t epoch;
+    uint32_t* ticket;                 // [0] next item, [1] CTAs done
+    uint32_t* timeouts;               // [0] expired waits, [1] abandoned epoch
+};
+cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launches);
+int hier_blocks_per_sm(int nw);
+
 struct TileArgs {
     const Tile* tiles;
     uint64_t ntiles;

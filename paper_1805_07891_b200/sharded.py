@@ -567,3 +567,139 @@ class ChainShardedPHub:
             capi.phub_free_shared(self.device, self._flags)
         self._own = {}
         self.hub.close()
+
+
+class HierPHub:
+    """Hierarchical reduction across racks (PAPER.md
+    P:746-763, emulated in P:1002-1012).
+
+    Every GPU is one rack's PBox with its own `workers_per_rack` workers (their
+    gradients resident in its HBM, like the 1-GPU job).  One round is the
+    paper's three steps, fused in ONE persistent launch per GPU
+    (phub_hier_exchange): the rack aggregate of the local workers, the
+    cross-rack aggregation in rack order over NVLink (each GPU stores its rack
+    aggregate of every other owner's range straight into that owner's inbox),
+    and the Nesterov step on the owned range with w' stored into every rack's
+    weight replica (the per-rack broadcast).  Per-GPU work is fixed as racks are
+    added (weak scaling); the cross-rack traffic per GPU is 2(G-1)/G model
+    sizes, independent of the number of workers per rack -- the "1/N
+    cross-rack traffic" the paper trades rounds for.
+    """
+
+    def __init__(self, key_sizes, workers_per_rack=8, chunk_size_bytes=32768, lr=0.1,
+                 momentum=0.9, device=None, group=None, block=32768, nslots=2):
+        import torch
+        import torch.distributed as dist
+        from .phub import PHub, _CudaArray
+        self.group = group
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.R, self.rack, self.P = world, rank, int(workers_per_rack)
+        self.block = int(block)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        dev = self.device
+        self.hub = PHub(key_sizes, self.P, chunk_size_bytes=chunk_size_bytes, lr=lr,
+                        momentum=momentum, rescale=1.0 / (self.R * self.P), device=dev,
+                        num_owners=world, owner_rank=rank, owner_policy="contig")
+        Ep = self.hub.E_padded
+        b, e = self.hub.owner_range()
+        L = e - b
+        self.nslots = int(nslots)
+        self._own = {(sl, k): capi.phub_alloc_shared(dev, 4 * Ep)
+                     for sl in range(self.nslots) for k in range(self.P)}
+        self._grads = {key: torch.as_tensor(_CudaArray(p, Ep, self), device=f"cuda:{dev}")
+                       for key, p in self._own.items()}
+        for t in self._grads.values():
+            t.zero_()
+        # inbox: 2 epoch-parity slots x R source racks x L owned elements
+        self._inbox = capi.phub_alloc_shared(dev, 4 * 2 * world * max(L, 1))
+        nblk = max(1, -(-L // self.block))
+        self._flags = capi.phub_alloc_shared(dev, 4 * nblk * world)
+        torch.as_tensor(_CudaArray(self._flags, nblk * world, self), device=f"cuda:{dev}").zero_()
+        h = capi.phub_ipc_get_handle
+        mine = (rank, b, e, h(dev, self._inbox), h(dev, self._flags),
+                h(dev, self.hub.weights_ptr()))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        allh.sort(key=lambda x: x[0])
+        self._opened = []
+        self.inbox = [[0] * world for _ in range(2)]
+        self.peer_inbox = [[0] * world for _ in range(2)]
+        self.peer_flags = [0] * world
+        reps = []
+        for o, ob, oe, ih, fh, wh in allh:
+            if o == rank:
+                continue
+            pin, pfl, pw = capi.phub_ipc_open(dev, ih), capi.phub_ipc_open(dev, fh), \
+                capi.phub_ipc_open(dev, wh)
+            self._opened += [pin, pfl, pw]
+            reps.append(pw)
+            self.peer_flags[o] = pfl
+            for sl in range(2):
+                # padded-based: ptr + 4x addresses element x of o's range in o's slot for us
+                self.peer_inbox[sl][o] = pin + 4 * ((sl * world + rank) * (oe - ob)) - 4 * ob
+                self.inbox[sl][o] = self._inbox + 4 * ((sl * world + o) * L) - 4 * b
+        capi.phub_set_replicas(self.hub.ctx, reps)
+        self.epoch = 0
+        self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
+        self.replica = self.hub.weights()
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+    @property
+    def num_workers(self):
+        return self.R * self.P
+
+    @property
+    def hosted(self):
+        """Local worker indices of this rack (0..P-1)."""
+        return list(range(self.P))
+
+    def exchange_host(self, host_grads: dict, host_out: dict, slot: int = 0):
+        g = self.gradients(slot)
+        for k in self.hosted:
+            g[k].copy_(host_grads[k], non_blocking=True)
+        self.exchange(slot)
+        for k in self.hosted:
+            host_out[k].copy_(self.replica, non_blocking=True)
+
+    def gradients(self, slot: int = 0) -> dict:
+        """This rack's gradient buffers (padded layout), keyed by local worker index."""
+        return {k: self._grads[(slot, k)] for k in range(self.P)}
+
+    def barrier(self):
+        import torch.distributed as dist
+        dist.all_reduce(self._flag, group=self.group)
+
+    def exchange(self, slot: int = 0):
+        Ep = self.hub.E_padded
+        for k in range(self.P):
+            self.hub.push(k, self._own[(slot, k)], mode="borrow", n=Ep)
+        self.epoch += 1
+        par = self.epoch % 2
+        capi.phub_hier_exchange(self.hub.ctx, self.R, self.block, self.inbox[par],
+                                self.peer_inbox[par], self._flags, self.peer_flags, self.epoch,
+                                self.hub._stream(None))
+        self.barrier()                       # every rack's w' stores into this replica are done
+
+    def sync_timeouts(self) -> int:
+        return capi.phub_sync_timeouts(self.hub.ctx)
+
+    def weights(self):
+        return self.replica
+
+    def close(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        capi.phub_set_replicas(self.hub.ctx, [])
+        for p in self._opened:
+            capi.phub_ipc_close(self.device, p)
+        dist.barrier(group=self.group)
+        self._grads = {}
+        for p in self._own.values():
+            capi.phub_free_shared(self.device, p)
+        capi.phub_free_shared(self.device, self._inbox)
+        capi.phub_free_shared(self.device, self._flags)
+        self._own = {}
+        self.hub.close()

@@ -65,3 +65,30 @@ def test_full_size_vgg19_exchange_sampled(G, mode):
             break
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("sampled: ok") == G
+
+
+HIER = os.path.join(ROOT, "tests", "dist", "hier_exchange_worker.py")
+
+
+@pytest.mark.parametrize("G,name,P,cb,rounds,block", [
+    (2, "small", 8, 32768, 3, 2048), (2, "tiny", 3, 4096, 2, 2048), (2, "one", 1, 32768, 2, 2048),
+    (2, "resnet50", 8, 32768, 2, 16384), (4, "small", 2, 64, 2, 2048),
+    (4, "resnet50", 8, 32768, 2, 16384), (4, "one", 2, 32768, 1, 2048),
+    (2, "vgg19", 8, 32768, 2, 16384), (4, "vgg19", 8, 32768, 2, 16384),
+    (8, "resnet50", 8, 32768, 2, 16384),
+])
+def test_hierarchical_exchange_bit_exact(G, name, P, cb, rounds, block):
+    """NEXT-4: one rack per GPU, rack aggregate -> cross-rack aggregation in
+    rack order -> Nesterov, bit-exact vs oracle.hier_round (sampled at full
+    VGG-19 size), including owners with no chunk ("one")."""
+    if _ngpus() < G:
+        pytest.skip(f"needs {G} GPUs, have {_ngpus()}")
+    for _attempt in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={G}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+               HIER, name, str(P), str(cb), str(rounds), str(block)]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count(": ok") == G

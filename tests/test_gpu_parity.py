@@ -844,3 +844,40 @@ def test_randomized_configs(seed):
     assert_bits_equal(gs, s, f"seed {seed} s")
     assert_bits_equal(gv, v, f"seed {seed} v")
     assert_bits_equal(gw, w, f"seed {seed} w")
+
+
+def test_hier_exchange_single_rack_and_validation():
+    """phub_hier_exchange with one rack (no peers) is the flat round of its P
+    workers (oracle.hier_round with R = 1); bad arguments are refused with
+    the state unchanged."""
+    from paper_1805_07891_b200 import PhubError, capi
+    sizes = manifest("resnet50")
+    P = 8
+    hub = _hub(sizes, P, keep_aggregate=True)
+    w0, v0 = host_state(hub.E, 14)
+    hub.load_state(w0, v0)
+    gd = device_grads(hub, P, 14)
+    with pytest.raises(PhubError):                         # nothing pushed yet
+        capi.phub_hier_exchange(hub.ctx, 1, 16384, None, None, 0, None, 1)
+    for k, g in enumerate(gd):
+        hub.push(k, g)
+    for bad in [dict(R=2), dict(block=1000), dict(epoch=0)]:
+        with pytest.raises(PhubError):
+            capi.phub_hier_exchange(hub.ctx, bad.get("R", 1), bad.get("block", 16384), None, None,
+                                    0, None, bad.get("epoch", 1))
+    assert hub.iteration == 0
+    for epoch in (1, 2):
+        if epoch == 2:
+            for k, g in enumerate(gd):
+                hub.push(k, g)
+        capi.phub_hier_exchange(hub.ctx, 1, 16384, None, None, 0, None, epoch)
+    torch.cuda.synchronize()
+    assert hub.iteration == 2
+    w, v, s = hub.read_state()
+    hg = host_grads(hub.E, P, 14)
+    rw, rv, _ = oracle.hier_round(sizes, [hg], w0, v0, 0.1, 0.9)
+    rw, rv, rs = oracle.hier_round(sizes, [hg], rw, rv, 0.1, 0.9)
+    assert_bits_equal(s, rs, "single-rack hierarchical aggregate")
+    assert_bits_equal(w, rw, "single-rack hierarchical w")
+    assert_bits_equal(v, rv, "single-rack hierarchical v")
+    hub.close()
