@@ -459,9 +459,9 @@ def bench_multi(args, mname, N, cb):
     if plan is not None:
         mine["out"], mine["in"] = plan.nvlink_bytes_out(), plan.nvlink_bytes_in()
     if hier:    # rack aggregate of every other owner's range out, w' of the own range to G-1
-        ob, oe = hub.owner_range()
-        mine["out"] = 4 * (Ep - (oe - ob)) + 4 * (oe - ob) * (G - 1)
-        mine["in"] = 4 * (oe - ob) * (G - 1) + 4 * (Ep - (oe - ob))
+        from paper_1805_07891_b200.sharded import hier_nvlink_bytes
+        mine["out"], mine["in"] = hier_nvlink_bytes(
+            [hub.owner_range(o) for o in range(G)], Ep, rank)
     elif chain:  # one partial per link per round; the last rank stores w' into G-1 replicas
         from paper_1805_07891_b200.sharded import chain_nvlink_bytes
         mine["out"], mine["in"] = chain_nvlink_bytes(Ep, G, rank)

@@ -551,13 +551,21 @@ __device__ __forceinline__ void local_sum(const HierArgs& a, uint64_t i, float a
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
     if constexpr (NW > 0) {
-        V8 gv[NW];
+        // batches of 4 loads keep the kernel at <= 64 registers (4 CTAs/SM), so a
+        // CTA stalled in its per-block fence leaves three others streaming
 #pragma unroll
-        for (int k = 0; k < NW; ++k) gv[k] = ld_grad(reinterpret_cast<const V8*>(a.g[k]) + i);
+        for (int k0 = 0; k0 < NW; k0 += 4) {
+            V8 gv[4];
 #pragma unroll
-        for (int k = 0; k < NW; ++k)
+            for (int k = 0; k < 4; ++k)
+                if (k0 + k < NW) gv[k] = ld_grad(reinterpret_cast<const V8*>(a.g[k0 + k]) + i);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+            for (int k = 0; k < 4; ++k)
+                if (k0 + k < NW) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+                }
+        }
     } else {
         for (int k0 = 0; k0 < nw; k0 += 8) {
             V8 gv[8];
@@ -574,25 +582,8 @@ __device__ __forceinline__ void local_sum(const HierArgs& a, uint64_t i, float a
     }
 }
 
-// acc += inbox[q] for q in [q0, q1), in rack order (loads batched 4 at a time)
-__device__ __forceinline__ void add_racks(const HierArgs& a, uint64_t i, int q0, int q1,
-                                          float acc[8]) {
-    for (int b = q0; b < q1; b += 4) {
-        V8 rv[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (b + k < q1) rv[k] = ld_coherent(reinterpret_cast<const V8*>(a.inbox[b + k]) + i);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (b + k < q1) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], rv[k].x[j]);
-            }
-    }
-}
-
 template <int NW>
-__global__ void __launch_bounds__(kThreads, 2) k_hier(const __grid_constant__ HierArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ HierArgs a) {
     const uint64_t B = a.block;
     const int R = a.R;
     uint64_t J = 0;                                    // blocks of the largest owner range
@@ -662,12 +653,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_hier(const __grid_constant__ Hi
                         float acc[8];
 #pragma unroll
                         for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
-                        add_racks(a, i, 0, a.rack, acc);             // S_0 .. S_{rack-1}
-                        float own[8];
-                        local_sum<NW>(a, i, own);                  // S_rack, from +0
+                        for (int q = 0; q < R; ++q) {              // rack order (R17)
+                            if (q == a.rack) {
+                                float own[8];
+                                local_sum<NW>(a, i, own);          // S_rack, from +0
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], own[e]);
-                        add_racks(a, i, a.rack + 1, R, acc);       // S_{rack+1} .. S_{R-1}
+                                for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], own[e]);
+                            } else {
+                                const V8 rv = ld_coherent(reinterpret_cast<const V8*>(a.inbox[q]) + i);
+#pragma unroll
+                                for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], rv.x[e]);
+                            }
+                        }
                         V8 wv = ld_state<PHUB_CACHE_ENABLED>(w + i);
                         V8 vv = ld_state<PHUB_CACHE_ENABLED>(v + i);
                         V8 sv;

@@ -569,6 +569,24 @@ class ChainShardedPHub:
         self.hub.close()
 
 
+def hier_slot(slot: int, src_rack: int, racks: int, owned: int) -> int:
+    """Element offset, inside an owner's inbox allocation (2 x racks x owned
+    elements), of the slot that rack `src_rack` fills in epoch parity `slot`.
+    Producer and consumer both address the inbox through this function."""
+    return (slot * racks + src_rack) * owned
+
+
+def hier_nvlink_bytes(ranges, E_padded: int, rank: int):
+    """(out, in) NVLink bytes of one hierarchical round for `rank`: its rack
+    aggregate of every other owner's range out and the w' of its own range to
+    the other racks' replicas; symmetric inbound."""
+    b, e = ranges[rank]
+    G = len(ranges)
+    out = 4 * (E_padded - (e - b)) + 4 * (e - b) * (G - 1)
+    inn = 4 * (e - b) * (G - 1) + 4 * (E_padded - (e - b))
+    return out, inn
+
+
 class HierPHub:
     """Hierarchical reduction across racks (PAPER.md
     P:746-763, emulated in P:1002-1012).
@@ -636,8 +654,8 @@ class HierPHub:
             self.peer_flags[o] = pfl
             for sl in range(2):
                 # padded-based: ptr + 4x addresses element x of o's range in o's slot for us
-                self.peer_inbox[sl][o] = pin + 4 * ((sl * world + rank) * (oe - ob)) - 4 * ob
-                self.inbox[sl][o] = self._inbox + 4 * ((sl * world + o) * L) - 4 * b
+                self.peer_inbox[sl][o] = pin + 4 * hier_slot(sl, rank, world, oe - ob) - 4 * ob
+                self.inbox[sl][o] = self._inbox + 4 * hier_slot(sl, o, world, L) - 4 * b
         capi.phub_set_replicas(self.hub.ctx, reps)
         self.epoch = 0
         self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")

@@ -127,3 +127,26 @@ def test_c_example_builds_against_the_abi():
     assert os.path.exists(exe)
     out = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
     assert "libphub.so" in out
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of the ABI structs have the C compiler's sizes and
+    field offsets (a drifted mirror would pass garbage across the boundary)."""
+    from paper_1805_07891_b200 import capi
+    structs = {"phub_config": capi.phub_config, "phub_chunk": capi.phub_chunk,
+               "phub_sync": capi.phub_sync, "phub_hier": capi.phub_hier}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "phub.h"', "int main(void){"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for fname, _t in cls._fields_:
+            lines.append(f'printf("{name}.{fname} %zu\\n", offsetof({name}, {fname}));')
+    lines.append("return 0;}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = dict(ln.split() for ln in subprocess.check_output([str(exe)], text=True).splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == C.sizeof(cls), name
+        for fname, _t in cls._fields_:
+            assert int(got[f"{name}.{fname}"]) == getattr(cls, fname).offset, f"{name}.{fname}"

@@ -66,3 +66,25 @@ def test_chain_pieces_and_bytes():
         sharded = max(max(p.nvlink_bytes_out(), p.nvlink_bytes_in()) for p in plans)
         chain = max(max(chain_nvlink_bytes(plans[0].E_padded, G, r)) for r in range(G))
         assert (chain < sharded) == (G == 2)
+
+
+def test_hier_inbox_slots_and_bytes():
+    """Hierarchical exchange host logic: every (epoch parity, source rack)
+    slot of an owner's inbox is disjoint and inside the 2 x R x L allocation;
+    cross-rack bytes are symmetric over ranks and ~2(G-1)/G model sizes."""
+    from paper_1805_07891_b200 import capi
+    from paper_1805_07891_b200.sharded import hier_nvlink_bytes, hier_slot
+    from workloads import manifest
+    m = manifest("vgg19")
+    for G in (1, 2, 4, 8):
+        Ep, _offs, ranges = capi.phub_plan_ranges(m, 32768, G)
+        for o, (b, e) in enumerate(ranges):
+            L = e - b
+            spans = sorted((hier_slot(sl, q, G, L), hier_slot(sl, q, G, L) + L)
+                           for sl in range(2) for q in range(G))
+            assert spans[0][0] == 0 and spans[-1][1] == 2 * G * L
+            assert all(a[1] == c[0] for a, c in zip(spans, spans[1:]))
+        outs = [hier_nvlink_bytes(ranges, Ep, r) for r in range(G)]
+        assert sum(o for o, _ in outs) == sum(i for _, i in outs)
+        expect = 2 * (G - 1) / G * 4 * Ep
+        assert max(max(x) for x in outs) <= expect * 1.001 + 4 * 32768
