@@ -281,7 +281,15 @@ def main():
     N = args.workers or N
     cb = args.chunk_bytes or cb
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if args.gpus > 1 or world > 1:
+    if args.gpus > 1 or world > 1 or args.mode == "hier":
+        if world == 1:           # single-process hier (one rack): a 1-rank process group
+            import socket
+            with socket.socket() as s_:
+                s_.bind(("127.0.0.1", 0))
+                port = s_.getsockname()[1]
+            for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", str(port)),
+                         ("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0")):
+                os.environ.setdefault(k, v)
         return bench_multi(args, mname, N, cb)
     return bench_single(args, mname, N, cb)
 
