@@ -274,13 +274,32 @@ phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
  * wait_flag[b] >= wait_value; once block b's stores are performed it raises
  * signal_flag[b] = signal_value.  A downstream stage can then start on block b
  * while this launch still works on later blocks -- the pipelining of PHub's
- * streaming aggregation without one launch per piece. */
+ * streaming aggregation without one launch per piece.
+ *
+ * Back-pressure (block form only; all three zero/NULL = off): a producer
+ * launch with `credit` != NULL starts block b (the b-th block of its range)
+ * only once *credit >= credit_base + b - credit_window (bounded wait); a
+ * consumer launch with `credit_return` != NULL adds 1 to *credit_return
+ * (typically the producer's peer-mapped counter) after each block it
+ * finishes.  The producer then runs at most `credit_window` blocks ahead, so
+ * what it stores into the consumer is still in the consumer's L2 when read
+ * (with PHUB_CONSUME, dropped from L2 without a write-back).  The counter is
+ * monotonic: credit_base = blocks consumed in earlier rounds.  Any window
+ * >= 1 is deadlock-free (block b only needs consumer blocks < b - window + 1,
+ * whose tickets were taken first); a window below the consumer's resident
+ * CTAs serialises the stages.  The two launches must run on different GPUs:
+ * a producer waiting on credits from a consumer queued behind it on the same
+ * stream would only time out. */
 typedef struct {
     const uint32_t* wait_flag;
     uint32_t wait_value;
     uint32_t* signal_flag;
     uint32_t signal_value;
     uint64_t block_elems;       /* 0: one flag per launch; > 0: one flag per block */
+    const uint32_t* credit;     /* producer: consumer-progress counter (local)       */
+    uint32_t credit_base;
+    uint32_t credit_window;     /* blocks the producer may run ahead                 */
+    uint32_t* credit_return;    /* consumer: counter to advance per finished block   */
 } phub_sync;
 
 /* Chained exchange (workers hosted in rank order): the

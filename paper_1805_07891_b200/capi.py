@@ -42,7 +42,9 @@ class phub_chunk(C.Structure):
 class phub_sync(C.Structure):
     _fields_ = [("wait_flag", C.c_void_p), ("wait_value", C.c_uint32),
                 ("signal_flag", C.c_void_p), ("signal_value", C.c_uint32),
-                ("block_elems", C.c_uint64)]
+                ("block_elems", C.c_uint64), ("credit", C.c_void_p),
+                ("credit_base", C.c_uint32), ("credit_window", C.c_uint32),
+                ("credit_return", C.c_void_p)]
 
 
 class phub_hier(C.Structure):
@@ -194,10 +196,12 @@ def phub_aggregate_ready(ctx, stream: int = 0) -> int:
     return int(n.value)
 
 
-def _sync(wait=None, signal=None, block=0):
-    """phub_sync from (flag_ptr, value) pairs; None when neither is given.
-    block > 0: the flag pointers are per-block arrays (block-streaming form)."""
-    if wait is None and signal is None:
+def _sync(wait=None, signal=None, block=0, credit=None, credit_return=None):
+    """phub_sync from (flag_ptr, value) pairs; None when nothing is given.
+    block > 0: the flag pointers are per-block arrays (block-streaming form);
+    credit = (counter_ptr, base, window) on a producer, credit_return = a
+    counter pointer on a consumer (back-pressure)."""
+    if wait is None and signal is None and credit is None and credit_return is None:
         return None
     s = phub_sync()
     if wait is not None:
@@ -205,20 +209,26 @@ def _sync(wait=None, signal=None, block=0):
     if signal is not None:
         s.signal_flag, s.signal_value = signal
     s.block_elems = int(block)
+    if credit is not None:
+        s.credit, s.credit_base, s.credit_window = credit
+    if credit_return is not None:
+        s.credit_return = credit_return
     return C.byref(s)
 
 
 def phub_aggregate_range(ctx, begin: int, end: int, stream: int = 0, wait=None, signal=None,
-                         block: int = 0):
-    _check(_lib.phub_aggregate_range(ctx, begin, end, _sync(wait, signal, block), stream),
-           "phub_aggregate_range", ctx)
+                         block: int = 0, credit=None, credit_return=None):
+    _check(_lib.phub_aggregate_range(ctx, begin, end,
+                                     _sync(wait, signal, block, credit, credit_return),
+                                     stream), "phub_aggregate_range", ctx)
 
 
 def phub_partial_sum(ctx, srcs, dst: int, begin: int, end: int, stream: int = 0, wait=None,
-                     signal=None, block: int = 0):
+                     signal=None, block: int = 0, credit=None, credit_return=None):
     arr = (C.c_void_p * max(len(srcs), 1))(*srcs)
     _check(_lib.phub_partial_sum(ctx, arr, len(srcs), dst, begin, end,
-                                 _sync(wait, signal, block), stream), "phub_partial_sum", ctx)
+                                 _sync(wait, signal, block, credit, credit_return), stream),
+           "phub_partial_sum", ctx)
 
 
 def phub_sync_timeouts(ctx) -> int:

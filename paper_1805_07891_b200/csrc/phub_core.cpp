@@ -657,6 +657,12 @@ static void apply_sync(phub_ctx c, phub::FlatArgs& a, const phub_sync* sync) {
     a.signal_flag = sync->signal_flag;
     a.signal_value = sync->signal_value;
     a.block = sync->block_elems;
+    if (a.block) {
+        a.credit = sync->credit;
+        a.credit_base = sync->credit_base;
+        a.credit_window = sync->credit_window;
+        a.credit_return = sync->credit_return;
+    }
 }
 
 // Block-streaming sync: blocks are whole multiples of one 256-thread x 8-element pass.

@@ -432,6 +432,21 @@ __global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ Fla
         __syncthreads();
         const uint64_t blk = s_blk;
         if (blk >= b1) break;
+        if (a.credit && blk - b0 >= a.credit_window) {
+            // back-pressure: stay at most credit_window blocks ahead of the consumer
+            if (threadIdx.x == 0) {
+                const uint32_t need = a.credit_base + (uint32_t)(blk - b0) - a.credit_window;
+                const uint64_t t0 = globaltimer_ns();
+                while ((int32_t)(ld_acquire_sys(a.credit) - need) < 0) {
+                    if (globaltimer_ns() - t0 > 2000000000ull) {
+                        atomicAdd(a.timeouts, 1u);
+                        break;
+                    }
+                    __nanosleep(100);
+                }
+            }
+            __syncthreads();
+        }
         const bool go = a.wait_flag ? block_wait(a, a.wait_flag + blk) : true;
         const uint64_t lo = (blk * B > a.begin ? blk * B : a.begin) / 8;
         const uint64_t hi = ((blk + 1) * B < a.end ? (blk + 1) * B : a.end) / 8;
@@ -479,8 +494,9 @@ __global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ Fla
             if constexpr (NAG) {
                 V8* w = reinterpret_cast<V8*>(a.w);
                 V8* v = reinterpret_cast<V8*>(a.v);
-                V8 wv = ld_state<PHUB_CACHE_ENABLED>(w + i);
-                V8 vv = ld_state<PHUB_CACHE_ENABLED>(v + i);
+                // read once per round: evict-first, so an incoming partial keeps its L2 lines
+                V8 wv = ld_state<PHUB_CACHE_BYPASS>(w + i);
+                V8 vv = ld_state<PHUB_CACHE_BYPASS>(v + i);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     out.x[j] = acc[j];
@@ -506,6 +522,8 @@ __global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ Fla
                 st_release_sys(a.signal_flag + blk, a.signal_value);
             }
         }
+        // flow control only (the producer never rewrites a block within a round)
+        if (a.credit_return && threadIdx.x == 0) atomicAdd_system(a.credit_return, 1u);
     }
     if (NAG && a.nrep) __threadfence_system();
     // the last CTA out resets the tickets for the next launch (stream-ordered)

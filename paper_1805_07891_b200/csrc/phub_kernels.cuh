@@ -39,6 +39,9 @@ struct FlatArgs {
     uint64_t block;                   // > 0: block-streaming flags (one per `block` elements)
     uint64_t discard;                 // bit k: input k is consumed (L2 lines may be discarded)
     uint32_t* ticket;                 // [0] next block, [1] CTAs done (block streaming, zeroed)
+    const uint32_t* credit;           // back-pressure (block streaming): see phub_sync
+    uint32_t credit_base, credit_window;
+    uint32_t* credit_return;
 };
 
 // Hierarchical reduction: one GPU = one rack's PBox with its P

@@ -391,7 +391,7 @@ class ChainShardedPHub:
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
                  device=None, group=None, pieces=8, sync="blocks", nslots=2, block=16384,
-                 pull=False, consume=True):
+                 pull=False, consume=True, window=0):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -404,6 +404,8 @@ class ChainShardedPHub:
         self.block = int(block)
         self.pull = bool(pull) and sync == "blocks"
         self.consume = bool(consume)
+        # back-pressure (blocks only): a producer runs at most `window` blocks ahead
+        self.window = int(window) if sync == "blocks" else 0
         self._epoch = 0
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
@@ -435,16 +437,25 @@ class ChainShardedPHub:
         self._flags = capi.phub_alloc_shared(dev, 4 * nflags) if rank > 0 else None
         if self._flags:
             torch.as_tensor(_CudaArray(self._flags, nflags, self), device=f"cuda:{dev}").zero_()
+        # consumer-progress counter on every producer (rank < world - 1)
+        self._credit = capi.phub_alloc_shared(dev, 4) if self.window and not self.last else None
+        if self._credit:
+            torch.as_tensor(_CudaArray(self._credit, 1, self), device=f"cuda:{dev}").zero_()
+        self._nblk = -(-Ep // self.block)
         h = capi.phub_ipc_get_handle
         mine = (rank, h(dev, self._pin) if self._pin else None,
                 h(dev, self.hub.weights_ptr()),
                 h(dev, self._flags) if self._flags else None,
-                h(dev, self._pout) if self._pout else None)
+                h(dev, self._pout) if self._pout else None,
+                h(dev, self._credit) if self._credit else None)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         allh.sort(key=lambda x: x[0])
         self._opened = []
-        self._next_in = self._next_flags = self._prev_out = None
+        self._next_in = self._next_flags = self._prev_out = self._prev_credit = None
+        if rank > 0 and self.window:
+            self._prev_credit = capi.phub_ipc_open(dev, allh[rank - 1][5])
+            self._opened.append(self._prev_credit)
         if not self.last:
             if not self.pull:
                 self._next_in = capi.phub_ipc_open(dev, allh[rank + 1][1])
@@ -456,7 +467,7 @@ class ChainShardedPHub:
             self._opened.append(self._prev_out)
         if self.last:
             reps = []
-            for r, _pin, wh, _fl, _po in allh:
+            for r, _pin, wh, _fl, _po, _cr in allh:
                 if r != rank:
                     reps.append(capi.phub_ipc_open(dev, wh))
             self._opened += reps
@@ -500,12 +511,15 @@ class ChainShardedPHub:
             self._epoch += 1
             ep = self._epoch
             wait = (self._flags, ep) if self._flags else None
+            credit = (self._credit, (ep - 1) * self._nblk, self.window) if self._credit else None
             if self.last:
-                capi.phub_aggregate_range(self.hub.ctx, 0, Ep, stream, wait=wait, block=self.block)
+                capi.phub_aggregate_range(self.hub.ctx, 0, Ep, stream, wait=wait, block=self.block,
+                                          credit_return=self._prev_credit)
             else:
                 dst = self._pout if self.pull else self._next_in
                 capi.phub_partial_sum(self.hub.ctx, srcs, dst, 0, Ep, stream, wait=wait,
-                                      signal=(self._next_flags, ep), block=self.block)
+                                      signal=(self._next_flags, ep), block=self.block,
+                                      credit=credit, credit_return=self._prev_credit)
             self.barrier()                   # replicas complete; buffers free for the next round
             return
         if self.sync == "flags":
@@ -563,6 +577,8 @@ class ChainShardedPHub:
             capi.phub_free_shared(self.device, self._pin)
         if self._pout:
             capi.phub_free_shared(self.device, self._pout)
+        if self._credit:
+            capi.phub_free_shared(self.device, self._credit)
         if self._flags:
             capi.phub_free_shared(self.device, self._flags)
         self._own = {}

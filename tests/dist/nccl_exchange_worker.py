@@ -35,10 +35,11 @@ def main():
     if mode.startswith("chain"):
         # chain: block-streaming flags, partial pushed to the next rank;
         # chain_pull: ... read by the next rank; chain_flags / chain_barrier: per piece
-        sync = {"chain": "blocks", "chain_pull": "blocks", "chain_flags": "flags",
-                "chain_barrier": "barrier"}[mode]
+        sync = {"chain": "blocks", "chain_pull": "blocks", "chain_window": "blocks",
+                "chain_flags": "flags", "chain_barrier": "barrier"}[mode]
         sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=3, sync=sync,
-                              block=2048, pull=mode == "chain_pull")
+                              block=2048, pull=mode == "chain_pull",
+                              window=3 if mode == "chain_window" else 0)
     else:
         cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
         sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
