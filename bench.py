@@ -10,8 +10,9 @@ worker's push, the fused tall aggregation + Nesterov update of every chunk,
 and the pull.  N = 1: all 8 workers' gradients are resident in HBM and pushed
 zero-copy (mode M1).  N > 1: one process per GPU, 8/N workers per
 GPU, chunks sharded by owner (mode M3); `--mode auto` runs the block-streamed
-chained exchange at N = 2 and the owner-sharded peer-memory kernel above
-(DESIGN.md 8.2); NCCL send/recv and an NCCL all-reduce baseline are options.
+chained exchange at N = 2 and the owner-sharded push exchange (every NVLink
+transfer a store) above; the owner-sharded peer-load kernel
+(p2p), NCCL send/recv and an NCCL all-reduce baseline are options.
 Total work is fixed as N grows ("scaling": "strong").  `--mode hier` is the
 hierarchical reduction (one 8-worker rack per GPU, weak scaling, NEXT-4).
 
@@ -64,6 +65,8 @@ def parse():
                     help="chain mode: elements per block flag (sync=blocks)")
     ap.add_argument("--hier-block", type=int, default=32768,
                     help="hier mode: elements per block flag")
+    ap.add_argument("--push-block", type=int, default=16384,
+                    help="push mode: elements per block flag")
     ap.add_argument("--chain-pull", action="store_true",
                     help="chain mode: next rank reads the partial over NVLink (default: pushed)")
     ap.add_argument("--chain-window", type=int, default=0,
@@ -73,7 +76,7 @@ def parse():
     ap.add_argument("--chain-producer-grid", type=int, default=0,
                     help="chain mode: CTAs of the partial-sum launch on non-last ranks")
     ap.add_argument("--mode", default="auto",
-                    choices=["auto", "p2p", "chain", "nccl", "allreduce", "hier"],
+                    choices=["auto", "p2p", "push", "chain", "nccl", "allreduce", "hier"],
                     help="N>1 exchange of the 8-worker job: chained (chain) or owner-sharded "
                          "(p2p) peer-memory kernels, NCCL send/recv (nccl), NCCL all-reduce "
                          "baseline (allreduce); hier: hierarchical reduction, one 8-worker "
@@ -343,7 +346,7 @@ def bench_multi(args, mname, N, cb):
     import torch
     import torch.distributed as dist
     from paper_1805_07891_b200.sharded import (AllReduceBaseline, ChainShardedPHub, HierPHub,
-                                               P2PShardedPHub, ShardedPHub)
+                                               P2PShardedPHub, PushShardedPHub, ShardedPHub)
     from workloads import grad_stream, manifest
     from workloads.generate import values_torch
 
@@ -353,17 +356,21 @@ def bench_multi(args, mname, N, cb):
     dist.init_process_group("nccl", device_id=dev)
     rank, G = dist.get_rank(), dist.get_world_size()
     sizes = manifest(mname)
-    if args.mode == "auto":      # fewest NVLink bytes: chain at G = 2, owner-sharded P2P above
-        args.mode = "chain" if G == 2 else "p2p"
+    if args.mode == "auto":      # fewest NVLink bytes: chain at G = 2, owner-sharded (push) above
+        args.mode = "chain" if G == 2 else "push"
     hier = args.mode == "hier"
-    chain = args.mode in ("chain", "hier")      # the whole round is one exchange() call
-    p2p = args.mode in ("p2p", "chain", "hier")
+    push = args.mode == "push"
+    chain = args.mode in ("chain", "hier", "push")   # the whole round is one exchange() call
+    p2p = args.mode in ("p2p", "chain", "hier", "push")
     ar = args.mode == "allreduce"
     NT = N * G if hier else N                   # workers in the job
     try:
         if hier:
             sh = HierPHub(sizes, workers_per_rack=N, chunk_size_bytes=cb, device=local,
                           block=args.hier_block)
+        elif push:
+            sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local,
+                                 block=args.push_block)
         elif chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
                                   sync=args.chain_sync, block=args.chain_block,
@@ -473,6 +480,8 @@ def bench_multi(args, mname, N, cb):
         from paper_1805_07891_b200.sharded import hier_nvlink_bytes
         mine["out"], mine["in"] = hier_nvlink_bytes(
             [hub.owner_range(o) for o in range(G)], Ep, rank)
+    elif push:   # same bytes as the owner-sharded P2P exchange (plan), all as stores
+        pass
     elif chain:  # one partial per link per round; the last rank stores w' into G-1 replicas
         from paper_1805_07891_b200.sharded import chain_nvlink_bytes
         mine["out"], mine["in"] = chain_nvlink_bytes(Ep, G, rank)
@@ -573,6 +582,11 @@ def bench_multi(args, mname, N, cb):
                                 f"aggregation in rack order over NVLink -> Nesterov on owner "
                                 f"ranges + w' into every rack's replica; one launch per GPU, "
                                 f"{args.hier_block}-element blocks") if hier else
+                               ("M3 (full exchange) push: one ticket-ordered launch per GPU "
+                                "stores its workers' raw slices into every other owner's inbox "
+                                "over NVLink and sums its own range over all workers in worker "
+                                "order -> Nesterov -> w' into every replica (all NVLink traffic "
+                                "as stores)") if push else
                                (f"M3 (full exchange) chain: rank-ordered partial sums over "
                                 f"NVLink, last rank fused Nesterov + replica stores, " +
                                 (f"one launch per rank streamed by per-block device flags "
@@ -606,6 +620,8 @@ def bench_multi(args, mname, N, cb):
                           "traffic": None,
                           "kernel": ("hierarchical exchange round (k_hier, incl. the "
                                      "end barrier)") if hier else
+                                    ("push exchange round (k_hier worker-order, incl. the end "
+                                     "barrier)") if push else
                                     ("chained exchange round (partial-sum + fused kernels, "
                                      "incl. barriers)") if chain else
                                     ("fused exchange kernel (k_flat with peer loads/stores), "

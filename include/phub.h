@@ -372,6 +372,14 @@ typedef struct {
     const uint32_t* flags;
     uint32_t* const* peer_flags;
     uint32_t epoch;
+    /* 0: hierarchical (rack-grouped) sum as above.  != 0: the flat worker-order
+     * sum over all num_racks x N workers -- rack q's local worker k is global
+     * worker q*N + k -- i.e. the owner-sharded exchange of ONE job whose
+     * workers are spread over the GPUs (reading R3), with every transfer an
+     * NVLink store: each rack stores its workers' raw slices of owner o's
+     * range into o's inbox (worker k at inbox + k*L + x, L = o's owned
+     * length, so each slot holds N slices) and o sums them in worker order. */
+    int32_t worker_order;
 } phub_hier;
 phub_status phub_hier_exchange(phub_ctx ctx, const phub_hier* h, void* stream);
 

@@ -95,7 +95,7 @@ struct phub_ctx_s {
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     int blocks_occ[2][phub::kMaxWorkers + 1] = {};   // resident CTAs/SM of k_blocks [nag][nw]
-    int hier_occ = 0;                                  // resident CTAs/SM of k_hier
+    int hier_occ[2] = {0, 0};                          // resident CTAs/SM of k_hier [worker_order]
     uint64_t iteration = 0;
     int launches = 0;
     uint64_t launches_total = 0;
@@ -1179,12 +1179,14 @@ phub_status phub_hier_exchange(phub_ctx c, const phub_hier* h, void* stream) {
     a.block = h->block_elems;
     a.flags = R > 1 ? h->flags : nullptr;
     a.epoch = h->epoch;
+    a.worker_order = h->worker_order ? 1 : 0;
     a.ticket = c->d_sync + 3;
     a.timeouts = c->d_sync + 1;
     DeviceGuard g(c->device);
     c->launches = 0;
-    if (!c->hier_occ) c->hier_occ = phub::hier_blocks_per_sm(c->N);
-    const int grid = c->grid_override ? c->grid_override : c->num_sms * c->hier_occ;
+    int& occ = c->hier_occ[a.worker_order];
+    if (!occ) occ = phub::hier_blocks_per_sm(c->N, a.worker_order != 0);
+    const int grid = c->grid_override ? c->grid_override : c->num_sms * occ;
     cudaError_t e = phub::launch_hier(a, grid, static_cast<cudaStream_t>(stream), &c->launches);
     c->launches_total += (uint64_t)c->launches;
     if (e != cudaSuccess) return c->cuda_fail(e, "hierarchical exchange launch");

@@ -563,11 +563,15 @@ void* pick_blocks(int nw) {
 // Deadlock-free: produce items never wait, and tickets are taken in item order,
 // so every produce item a waiting consume item needs has already been taken by
 // a running CTA on its rack.
-template <int NW>
+// acc = ((+0 + g_0) + g_1) + ... over the local workers (ZERO), or acc += g_0, g_1, ...
+// in order onto a running sum (!ZERO: the flat worker-order exchange)
+template <int NW, bool ZERO = true>
 __device__ __forceinline__ void local_sum(const HierArgs& a, uint64_t i, float acc[8]) {
     const int nw = NW > 0 ? NW : a.nw;
+    if constexpr (ZERO) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    }
     if constexpr (NW > 0) {
         // batches of 4 loads keep the kernel at <= 64 registers (4 CTAs/SM), so a
         // CTA stalled in its per-block fence leaves three others streaming
@@ -600,7 +604,7 @@ __device__ __forceinline__ void local_sum(const HierArgs& a, uint64_t i, float a
     }
 }
 
-template <int NW>
+template <int NW, bool WO>
 __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ HierArgs a) {
     const uint64_t B = a.block;
     const int R = a.R;
@@ -624,14 +628,33 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ Hi
             const uint64_t lo = a.own_begin[o] + j * B;
             const uint64_t hi = lo + B < a.own_end[o] ? lo + B : a.own_end[o];
             if (lo < hi) {
-                V8* dst = reinterpret_cast<V8*>(a.peer_inbox[o]);
-                for (uint64_t i = lo / 8 + threadIdx.x; i < hi / 8; i += kThreads) {
-                    float acc[8];
-                    local_sum<NW>(a, i, acc);
-                    V8 out;
+                if constexpr (WO) {
+                    // worker-order exchange: each local worker's raw slice goes to o's
+                    // inbox (worker k at +k*L_o); o sums all workers in worker order
+                    const int nw = NW > 0 ? NW : a.nw;
+                    const uint64_t L = a.own_end[o] - a.own_begin[o];
+                    for (uint64_t i = lo / 8 + threadIdx.x; i < hi / 8; i += kThreads)
+                        for (int k0 = 0; k0 < nw; k0 += 4) {
+                            V8 gv[4];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) out.x[e] = acc[e];
-                    dst[i] = out;
+                            for (int k = 0; k < 4; ++k)
+                                if (k0 + k < nw)
+                                    gv[k] = ld_grad(reinterpret_cast<const V8*>(a.g[k0 + k]) + i);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                if (k0 + k < nw)
+                                    reinterpret_cast<V8*>(a.peer_inbox[o] + (k0 + k) * L)[i] = gv[k];
+                        }
+                } else {
+                    V8* dst = reinterpret_cast<V8*>(a.peer_inbox[o]);
+                    for (uint64_t i = lo / 8 + threadIdx.x; i < hi / 8; i += kThreads) {
+                        float acc[8];
+                        local_sum<NW>(a, i, acc);
+                        V8 out;
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) out.x[e] = acc[e];
+                        dst[i] = out;
+                    }
                 }
                 __syncthreads();                       // bar.sync + one fence (cumulative)
                 if (threadIdx.x == 0) {
@@ -671,8 +694,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ Hi
                         float acc[8];
 #pragma unroll
                         for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
-                        for (int q = 0; q < R; ++q) {              // rack order (R17)
-                            if (q == a.rack) {
+                        for (int q = 0; q < R; ++q) {
+                            if constexpr (WO) {                    // worker order (R3)
+                                if (q == a.rack) {
+                                    local_sum<NW, false>(a, i, acc);
+                                } else {
+                                    const int nw = NW > 0 ? NW : a.nw;
+                                    const uint64_t L = a.own_end[a.rack] - a.own_begin[a.rack];
+                                    for (int k = 0; k < nw; ++k) {
+                                        const V8 rv = ld_coherent(
+                                            reinterpret_cast<const V8*>(a.inbox[q] + k * L) + i);
+#pragma unroll
+                                        for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], rv.x[e]);
+                                    }
+                                }
+                            } else if (q == a.rack) {              // rack order (R17)
                                 float own[8];
                                 local_sum<NW>(a, i, own);          // S_rack, from +0
 #pragma unroll
@@ -708,15 +744,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ Hi
     }
 }
 
-void* pick_hier(int nw) {
+template <bool WO>
+void* pick_hier_wo(int nw) {
     switch (nw) {
-        case 1: return (void*)k_hier<1>;
-        case 2: return (void*)k_hier<2>;
-        case 4: return (void*)k_hier<4>;
-        case 8: return (void*)k_hier<8>;
-        default: return (void*)k_hier<0>;
+        case 1: return (void*)k_hier<1, WO>;
+        case 2: return (void*)k_hier<2, WO>;
+        case 4: return (void*)k_hier<4, WO>;
+        case 8: return (void*)k_hier<8, WO>;
+        default: return (void*)k_hier<0, WO>;
     }
 }
+void* pick_hier(int nw, bool wo) { return wo ? pick_hier_wo<true>(nw) : pick_hier_wo<false>(nw); }
 
 // ------------------------------------------------ bulk-copy (TMA) staging
 // Variant with the loads taken off the register file: one producer thread per
@@ -1024,16 +1062,18 @@ cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t 
     return e;
 }
 
-int hier_blocks_per_sm(int nw) {
+int hier_blocks_per_sm(int nw, bool worker_order) {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pick_hier(nw), kThreads, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pick_hier(nw, worker_order), kThreads, 0) !=
+        cudaSuccess)
         return 1;
     return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launches) {
     void* args[] = {const_cast<HierArgs*>(&a)};
-    cudaError_t e = cudaLaunchKernel(pick_hier(a.nw), dim3(grid), dim3(kThreads), args, 0, s);
+    cudaError_t e = cudaLaunchKernel(pick_hier(a.nw, a.worker_order != 0), dim3(grid),
+                                     dim3(kThreads), args, 0, s);
     ++*launches;
     return e;
 }

@@ -66,9 +66,10 @@ struct HierArgs {
     uint32_t epoch;
     uint32_t* ticket;                 // [0] next item, [1] CTAs done
     uint32_t* timeouts;               // [0] expired waits, [1] abandoned epoch
+    int worker_order;                 // 1: flat worker-order sum of raw slices (M3 exchange)
 };
 cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launches);
-int hier_blocks_per_sm(int nw);
+int hier_blocks_per_sm(int nw, bool worker_order);
 
 struct TileArgs {
     const Tile* tiles;

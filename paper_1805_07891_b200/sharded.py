@@ -621,7 +621,8 @@ class HierPHub:
     """
 
     def __init__(self, key_sizes, workers_per_rack=8, chunk_size_bytes=32768, lr=0.1,
-                 momentum=0.9, device=None, group=None, block=32768, nslots=2):
+                 momentum=0.9, device=None, group=None, block=32768, nslots=2,
+                 worker_order=False):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -629,6 +630,10 @@ class HierPHub:
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         self.R, self.rack, self.P = world, rank, int(workers_per_rack)
         self.block = int(block)
+        # worker_order: the flat worker-order sum of one job's R x P workers (raw
+        # slices pushed to the owners) instead of the rack-grouped sum
+        self.worker_order = bool(worker_order)
+        S = self.P if self.worker_order else 1          # slices per (slot, source rack)
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
         self.hub = PHub(key_sizes, self.P, chunk_size_bytes=chunk_size_bytes, lr=lr,
@@ -644,8 +649,8 @@ class HierPHub:
                        for key, p in self._own.items()}
         for t in self._grads.values():
             t.zero_()
-        # inbox: 2 epoch-parity slots x R source racks x L owned elements
-        self._inbox = capi.phub_alloc_shared(dev, 4 * 2 * world * max(L, 1))
+        # inbox: 2 epoch-parity slots x R source racks x S slices x L owned elements
+        self._inbox = capi.phub_alloc_shared(dev, 4 * 2 * world * S * max(L, 1))
         nblk = max(1, -(-L // self.block))
         self._flags = capi.phub_alloc_shared(dev, 4 * nblk * world)
         torch.as_tensor(_CudaArray(self._flags, nblk * world, self), device=f"cuda:{dev}").zero_()
@@ -670,8 +675,9 @@ class HierPHub:
             self.peer_flags[o] = pfl
             for sl in range(2):
                 # padded-based: ptr + 4x addresses element x of o's range in o's slot for us
-                self.peer_inbox[sl][o] = pin + 4 * hier_slot(sl, rank, world, oe - ob) - 4 * ob
-                self.inbox[sl][o] = self._inbox + 4 * hier_slot(sl, o, world, L) - 4 * b
+                self.peer_inbox[sl][o] = pin + 4 * hier_slot(sl, rank, world, S * (oe - ob)) \
+                    - 4 * ob
+                self.inbox[sl][o] = self._inbox + 4 * hier_slot(sl, o, world, S * L) - 4 * b
         capi.phub_set_replicas(self.hub.ctx, reps)
         self.epoch = 0
         self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
@@ -712,7 +718,7 @@ class HierPHub:
         par = self.epoch % 2
         capi.phub_hier_exchange(self.hub.ctx, self.R, self.block, self.inbox[par],
                                 self.peer_inbox[par], self._flags, self.peer_flags, self.epoch,
-                                self.hub._stream(None))
+                                self.hub._stream(None), worker_order=self.worker_order)
         self.barrier()                       # every rack's w' stores into this replica are done
 
     def sync_timeouts(self) -> int:
@@ -737,3 +743,42 @@ class HierPHub:
         capi.phub_free_shared(self.device, self._flags)
         self._own = {}
         self.hub.close()
+
+
+class PushShardedPHub(HierPHub):
+    """Owner-sharded exchange of the N-worker job with every NVLink transfer a
+    store (all-to-all SM stores run at ~680 GB/s per direction,
+    loads mixed with stores on the same links at ~600-670): one launch per GPU
+    (phub_hier_exchange, worker_order) stores each hosted worker's raw slice
+    of every other owner's range into that owner's inbox, and sums its own
+    range over all N workers in worker order (R3; bit-identical to the 1-GPU
+    sum) -> Nesterov -> w' into every replica.  Workers are hosted in rank
+    order: rank r hosts global workers [r*N/G, (r+1)*N/G).  Same interface as
+    P2PShardedPHub (gradients() keyed by global worker id)."""
+
+    def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
+                 device=None, group=None, block=16384, nslots=2):
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+        if num_workers % world:
+            raise ValueError(f"{num_workers} workers cannot be hosted evenly on {world} ranks")
+        super().__init__(key_sizes, workers_per_rack=num_workers // world,
+                         chunk_size_bytes=chunk_size_bytes, lr=lr, momentum=momentum,
+                         device=device, group=group, block=block, nslots=nslots,
+                         worker_order=True)
+        self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, self.rack, world)
+
+    @property
+    def hosted(self):
+        return [self.rack * self.P + k for k in range(self.P)]
+
+    def gradients(self, slot: int = 0) -> dict:
+        return {self.rack * self.P + k: self._grads[(slot, k)] for k in range(self.P)}
+
+    def exchange_host(self, host_grads: dict, host_out: dict, slot: int = 0):
+        g = self.gradients(slot)
+        for w in self.hosted:
+            g[w].copy_(host_grads[w], non_blocking=True)
+        self.exchange(slot)
+        for w in self.hosted:
+            host_out[w].copy_(self.replica, non_blocking=True)

@@ -1,6 +1,6 @@
 """Full-size multi-GPU parity worker (torchrun, NCCL): the exchange bench.py
 times at N > 1 (`--mode auto`: chained exchange with block-streaming flags at
-G = 2, owner-sharded P2P kernel above), at BASELINE.json's full model size,
+G = 2, owner-sharded push exchange above), at BASELINE.json's full model size,
 checked against the CPU oracle on sampled elements (the oracle computes them
 one by one from independently generated inputs).
 
@@ -20,7 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
-from paper_1805_07891_b200.sharded import ChainShardedPHub, P2PShardedPHub  # noqa: E402
+from paper_1805_07891_b200.sharded import (  # noqa: E402
+    ChainShardedPHub, P2PShardedPHub, PushShardedPHub)
 from workloads import grad_stream, manifest  # noqa: E402
 from workloads.generate import values_at_np, values_torch  # noqa: E402
 
@@ -47,11 +48,11 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     rank, G = dist.get_rank(), dist.get_world_size()
     if mode == "auto":                       # bench.py --mode auto
-        mode = "chain" if G == 2 else "p2p"
+        mode = "chain" if G == 2 else "push"
     sizes = manifest(name)
     E = sum(sizes)
-    sh = (ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local) if mode == "chain"
-          else P2PShardedPHub(sizes, N, chunk_size_bytes=cb, device=local))
+    cls = {"chain": ChainShardedPHub, "p2p": P2PShardedPHub, "push": PushShardedPHub}[mode]
+    sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
     hub = sh.hub
     idx = torch.as_tensor(hub.padded_index(), device=dev)
     hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
@@ -71,7 +72,7 @@ def main():
         gs = np.stack([values_at_np(grad_stream(w) + 37 * r, samp, 25) for w in range(N)])
         w_ref, v_ref, _ = oracle.elems(gs, w_ref, v_ref, 0.1, 0.9)
     ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
-    if mode == "chain" and sh.sync_timeouts() != 0:
+    if mode in ("chain", "push") and sh.sync_timeouts() != 0:
         ok = False
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))
     flag = torch.tensor([0 if ok else 1], device=dev)

@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
 from paper_1805_07891_b200.sharded import (  # noqa: E402
-    ChainShardedPHub, P2PShardedPHub, ShardedPHub)
+    ChainShardedPHub, P2PShardedPHub, PushShardedPHub, ShardedPHub)
 from workloads import grad_stream, manifest, values_np  # noqa: E402
 from workloads.generate import values_torch  # noqa: E402
 
@@ -40,10 +40,12 @@ def main():
         sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=3, sync=sync,
                               block=2048, pull=mode == "chain_pull",
                               window=3 if mode == "chain_window" else 0)
+    elif mode == "push":
+        sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048)
     else:
         cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
         sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
-    fused = mode == "p2p" or mode.startswith("chain")
+    fused = mode in ("p2p", "push") or mode.startswith("chain")
     w_ref, v_ref = values_np(1, 0, E, 20), values_np(2, 0, E, 25)
     sh.hub.load_state(w_ref, v_ref)
     idx = torch.as_tensor(sh.hub.padded_index(), device=dev)
@@ -63,7 +65,7 @@ def main():
     torch.cuda.synchronize()
     got = sh.weights()[idx].cpu().numpy()
     ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
-    if mode.startswith("chain") and sh.sync_timeouts() != 0:
+    if (mode.startswith("chain") or mode == "push") and sh.sync_timeouts() != 0:
         ok = False
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))
     flag = torch.tensor([0 if ok else 1], device=dev)

@@ -24,7 +24,7 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("mode", ["nccl", "p2p", "chain", "chain_pull", "chain_window",
+@pytest.mark.parametrize("mode", ["nccl", "p2p", "push", "chain", "chain_pull", "chain_window",
                                   "chain_flags", "chain_barrier"])
 @pytest.mark.parametrize("G,name,N,cb,rounds", [
     (2, "small", 8, 32768, 2), (2, "tiny", 4, 4096, 1), (4, "resnet50", 8, 32768, 2),
@@ -49,7 +49,7 @@ FULL = os.path.join(ROOT, "tests", "dist", "full_size_exchange_worker.py")
 
 
 @pytest.mark.parametrize("G,mode", [(2, "auto"), (2, "p2p"), (4, "auto"), (4, "chain"),
-                                    (8, "auto")])
+                                    (4, "push"), (4, "p2p"), (8, "auto")])
 def test_full_size_vgg19_exchange_sampled(G, mode):
     """bench.py's N > 1 launch configuration at BASELINE.json's full VGG-19
     size (2 rounds), every rank's replica checked against the oracle on
