@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--kernel", default="auto", choices=["auto", "flat", "flat128", "tiles", "wide", "bulk"])
     ap.add_argument("--cache", default="enabled", choices=["enabled", "bypass"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-streams", type=int, default=1,
+                    help="copy streams per direction in the 1-GPU e2e measurement")
     ap.add_argument("--grid", type=int, default=0, help="CTAs for the flat kernel (0 = auto)")
     ap.add_argument("--seg", type=int, default=-1, help="flat kernel CTA segment (vectors)")
     ap.add_argument("--minb", type=int, default=0, help="flat kernel resident-CTA build")
@@ -738,7 +740,7 @@ def bench_single(args, mname, N, cb):
     # ---- end to end through the public API with host buffers (pinned), H2D/D2H inside
     e2e = None
     if not args.no_e2e:
-        e2e = bench_e2e(hub, grads, N, E, Ep, stream, args.e2e_steps)
+        e2e = bench_e2e(hub, grads, N, E, Ep, stream, args.e2e_steps, args.e2e_streams)
 
     cpu = None
     if not args.no_cpu:
@@ -812,65 +814,77 @@ def bench_graph(hub, grads, N, E, stream, steps, rounds_per_graph=20):
             "unit": "GB/s", "rounds_per_graph": rounds_per_graph, "replays": reps}
 
 
-def bench_e2e(hub, grads, N, E, Ep, stream, steps):
+def bench_e2e(hub, grads, N, E, Ep, stream, steps, nstreams=1):
     """Same metric through the public C ABI with pinned HOST buffers: every round
     copies the N pushes host->device (PHUB_COPY), runs the kernel, and pulls
-    the model back to the host once per worker (PHUB_ALL_KEYS pull) -- all
-    inside the timed region.  Rounds are pipelined on three streams: the H2D
-    pushes of round k+1 (receive slot (k+1) % 2) overlap the D2H pulls of
-    round k on the full-duplex PCIe link; each kernel waits for its pushes and
-    for the previous round's pulls (it overwrites w)."""
+    the model back to the host once per worker (PHUB_ALL_KEYS pull, one host
+    buffer per worker) -- all inside the timed region.  Rounds are pipelined:
+    the H2D pushes of round k+1 (receive slot (k+1) % 2) overlap the D2H pulls
+    of round k on the full-duplex PCIe link; each kernel waits for its pushes
+    and for the previous round's pulls (it overwrites w).  Copies are spread
+    round-robin over `nstreams` streams per direction (several copy engines)."""
     import torch
     host_g = []
     for w in range(N):
         h = torch.empty(Ep, dtype=torch.float32, pin_memory=True)
         h.copy_(grads[w])
         host_g.append(h)
-    host_w = torch.empty(Ep, dtype=torch.float32, pin_memory=True)
+    host_w = [torch.empty(Ep, dtype=torch.float32, pin_memory=True) for _ in range(N)]
     torch.cuda.synchronize()
-    s_in, s_c, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    K = max(1, int(nstreams))
+    s_in = [torch.cuda.Stream() for _ in range(K)]
+    s_out = [torch.cuda.Stream() for _ in range(K)]
+    s_c = torch.cuda.Stream()
     total = steps + 1
 
     def ev():
         return torch.cuda.Event(enable_timing=False)
 
-    ev_in = [ev() for _ in range(total)]
+    ev_in = [[ev() for _ in range(K)] for _ in range(total)]
     ev_c = [ev() for _ in range(total)]
-    ev_out = [ev() for _ in range(total)]
+    ev_out = [[ev() for _ in range(K)] for _ in range(total)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def round_(k):
         if k >= 2:
-            s_in.wait_event(ev_c[k - 2])           # receive slot k % 2 is free again
+            for si in s_in:
+                si.wait_event(ev_c[k - 2])         # receive slot k % 2 is free again
         for w in range(N):
-            hub.push(w, host_g[w], mode="copy", stream=s_in)
-        ev_in[k].record(s_in)
-        s_c.wait_event(ev_in[k])
+            hub.push(w, host_g[w], mode="copy", stream=s_in[w % K])
+        for i, si in enumerate(s_in):
+            ev_in[k][i].record(si)
+            s_c.wait_event(ev_in[k][i])
         if k >= 1:
-            s_c.wait_event(ev_out[k - 1])          # previous pulls have read w
+            for e in ev_out[k - 1]:
+                s_c.wait_event(e)                  # previous pulls have read w
         hub.aggregate_optimize(stream=s_c)
         ev_c[k].record(s_c)
-        s_out.wait_event(ev_c[k])
+        for so in s_out:
+            so.wait_event(ev_c[k])
         for w in range(N):
-            hub.pull(host_w, stream=s_out)
-        ev_out[k].record(s_out)
+            hub.pull(host_w[w], stream=s_out[w % K])
+        for i, so in enumerate(s_out):
+            ev_out[k][i].record(so)
 
     round_(0)                                      # warm-up round
     torch.cuda.synchronize()
-    t0.record(s_in)
-    s_c.wait_event(t0)
-    s_out.wait_event(t0)
+    t0.record(s_c)
+    for si in s_in + s_out:
+        si.wait_event(t0)
     for k in range(1, total):
         round_(k)
-    t1.record(s_out)
+    for e in ev_out[total - 1]:
+        s_c.wait_event(e)
+    t1.record(s_c)
     torch.cuda.synchronize()
     t = t0.elapsed_time(t1) / 1e3 / steps
     del host_g, host_w
     return {"value": round(N * 4 * E / t / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": N * 4 * Ep, "d2h_bytes_per_step": N * 4 * Ep,
             "steps": steps, "ms_per_step": round(t * 1e3, 3),
-            "path": "phub_push(PHUB_COPY, pinned host) x N -> phub_aggregate_optimize -> "
-                    "phub_pull(host) x N; rounds pipelined on 3 streams (H2D of k+1 || D2H of k)"}
+            "path": f"phub_push(PHUB_COPY, pinned host) x N -> phub_aggregate_optimize -> "
+                    f"phub_pull(host) x N; rounds pipelined (H2D of k+1 || D2H of k), copies "
+                    f"on {K} stream(s) per direction"}
 
 
 if __name__ == "__main__":

@@ -31,3 +31,18 @@ def test_reference_arm_nonzero_rank_is_silent():
                         "--config", "tiny", "--steps", "1", "--warmup", "1"],
                        capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_results_csv_schema(tmp_path):
+    """scripts/results_csv.py: fixed header, one row per bench.py JSON line."""
+    d = tmp_path / "p"
+    d.mkdir()
+    (d / "a.json").write_text('noise\n{"metric": "m", "value": 1.5, "n_gpus": 2, "config": '
+                              '{"workload": "vgg19", "workers": 8}, "roofline": {"frac": 0.9}}\n')
+    (d / "b.json").write_text('{"not": "a bench line"}\n')
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "results_csv.py"), str(d)],
+                       capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    assert lines[0].split(",")[:4] == ["file", "impl", "workload", "n_gpus"]
+    assert len(lines) == 2 and ",vgg19,2,8," in lines[1] and ",0.9," in lines[1]
