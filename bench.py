@@ -304,6 +304,31 @@ def main():
 NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction per GPU
 
 
+def nccl_allgather_busbw(dev, G, mib=256, reps=5):
+    """Same-run NVLink probe: NCCL all-gather of `mib` MiB per
+    rank, bus bandwidth = (G-1)/G * total bytes / t (nccl-tests' definition),
+    best of `reps`, max time over ranks."""
+    import torch
+    import torch.distributed as dist
+    n = mib * (1 << 20) // 4
+    src = torch.ones(n, dtype=torch.float32, device=dev)
+    dst = torch.empty(n * G, dtype=torch.float32, device=dev)
+    best = float("inf")
+    for _ in range(reps + 2):
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dist.all_gather_into_tensor(dst, src)
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / 1e3], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        best = min(best, float(t.item()))
+    del src, dst
+    torch.cuda.empty_cache()
+    return round((G - 1) / G * 4 * n * G / best / 1e9, 1)
+
+
 def owner_phase_ms(sizes, N, cb, rank, G, steps, warmup, dev):
     """Mode M2: this rank's owner kernel alone, with the N workers'
     slices of its owned range already resident in its HBM (PHub's pushes land
@@ -494,6 +519,7 @@ def bench_multi(args, mname, N, cb):
         mine["m2_ms"], mine["m2_owned"] = mine["k_ms"], mine["owned"]
     allr = [None] * G
     dist.all_gather_object(allr, mine)
+    ag_busbw = nccl_allgather_busbw(dev, G) if G > 1 else None
 
     e2e = None
     if not args.no_e2e and not ar:
@@ -641,7 +667,10 @@ def bench_multi(args, mname, N, cb):
                                 "frac": round(nv_ach / NVLINK_PEER_GBS, 4),
                                 "bytes_per_step_max_dir": nv_bytes,
                                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s "
-                                               "per direction (900 nominal)"},
+                                               "per direction (900 nominal)",
+                                "same_run_nccl_allgather_busbw": ag_busbw,
+                                "frac_of_nccl_allgather": round(nv_ach / ag_busbw, 4)
+                                if ag_busbw else None},
             "clocks": {"sm_mhz": statistics.median(sm) if sm else None,
                        "sm_max_mhz": allr[0]["clocks"].get("sm_max_mhz"), "reasons": reasons},
             "gpu_launches": sum(r["launches"] for r in allr),

@@ -453,25 +453,42 @@ class ChainShardedPHub:
         allh.sort(key=lambda x: x[0])
         self._opened = []
         self._next_in = self._next_flags = self._prev_out = self._prev_credit = None
-        if rank > 0 and self.window:
-            self._prev_credit = capi.phub_ipc_open(dev, allh[rank - 1][5])
-            self._opened.append(self._prev_credit)
-        if not self.last:
-            if not self.pull:
-                self._next_in = capi.phub_ipc_open(dev, allh[rank + 1][1])
-                self._opened.append(self._next_in)
-            self._next_flags = capi.phub_ipc_open(dev, allh[rank + 1][3])
-            self._opened.append(self._next_flags)
-        if rank > 0 and self.pull:
-            self._prev_out = capi.phub_ipc_open(dev, allh[rank - 1][4])
-            self._opened.append(self._prev_out)
-        if self.last:
-            reps = []
-            for r, _pin, wh, _fl, _po, _cr in allh:
-                if r != rank:
-                    reps.append(capi.phub_ipc_open(dev, wh))
-            self._opened += reps
-            capi.phub_set_replicas(self.hub.ctx, reps)
+
+        def open_(hd):
+            p_ = capi.phub_ipc_open(dev, hd)
+            self._opened.append(p_)
+            return p_
+
+        err = None
+        try:
+            if rank > 0 and self.window:
+                self._prev_credit = open_(allh[rank - 1][5])
+            if not self.last:
+                if not self.pull:
+                    self._next_in = open_(allh[rank + 1][1])
+                self._next_flags = open_(allh[rank + 1][3])
+            if rank > 0 and self.pull:
+                self._prev_out = open_(allh[rank - 1][4])
+            if self.last:
+                reps = [open_(wh) for r, _pin, wh, _fl, _po, _cr in allh if r != rank]
+                capi.phub_set_replicas(self.hub.ctx, reps)
+        except capi.PhubError as ex:
+            err = ex
+        # every rank must agree before anyone relies on peer mappings
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=f"cuda:{dev}")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            for p_ in self._opened:
+                try:
+                    capi.phub_ipc_close(dev, p_)
+                except capi.PhubError:
+                    pass
+            self._grads = {}
+            for p_ in list(self._own.values()) + [x for x in (self._pin, self._pout, self._flags,
+                                                              self._credit) if x]:
+                capi.phub_free_shared(dev, p_)
+            self.hub.close()
+            raise PeerMappingError(f"peer mapping failed on some rank ({err or 'other rank'})")
         self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
         self.replica = self.hub.weights()
         torch.cuda.synchronize(dev)
@@ -665,20 +682,38 @@ class HierPHub:
         self.peer_inbox = [[0] * world for _ in range(2)]
         self.peer_flags = [0] * world
         reps = []
-        for o, ob, oe, ih, fh, wh in allh:
-            if o == rank:
-                continue
-            pin, pfl, pw = capi.phub_ipc_open(dev, ih), capi.phub_ipc_open(dev, fh), \
-                capi.phub_ipc_open(dev, wh)
-            self._opened += [pin, pfl, pw]
-            reps.append(pw)
-            self.peer_flags[o] = pfl
-            for sl in range(2):
-                # padded-based: ptr + 4x addresses element x of o's range in o's slot for us
-                self.peer_inbox[sl][o] = pin + 4 * hier_slot(sl, rank, world, S * (oe - ob)) \
-                    - 4 * ob
-                self.inbox[sl][o] = self._inbox + 4 * hier_slot(sl, o, world, S * L) - 4 * b
-        capi.phub_set_replicas(self.hub.ctx, reps)
+        err = None
+        try:
+            for o, ob, oe, ih, fh, wh in allh:
+                if o == rank:
+                    continue
+                for hd in (ih, fh, wh):
+                    self._opened.append(capi.phub_ipc_open(dev, hd))
+                pin, pfl, pw = self._opened[-3:]
+                reps.append(pw)
+                self.peer_flags[o] = pfl
+                for sl in range(2):
+                    # padded-based: ptr + 4x addresses element x of o's range in o's slot for us
+                    self.peer_inbox[sl][o] = pin + 4 * hier_slot(sl, rank, world, S * (oe - ob)) \
+                        - 4 * ob
+                    self.inbox[sl][o] = self._inbox + 4 * hier_slot(sl, o, world, S * L) - 4 * b
+            capi.phub_set_replicas(self.hub.ctx, reps)
+        except capi.PhubError as ex:
+            err = ex
+        # every rank must agree before anyone relies on peer mappings
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=f"cuda:{dev}")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            for p_ in self._opened:
+                try:
+                    capi.phub_ipc_close(dev, p_)
+                except capi.PhubError:
+                    pass
+            self._grads = {}
+            for p_ in list(self._own.values()) + [self._inbox, self._flags]:
+                capi.phub_free_shared(dev, p_)
+            self.hub.close()
+            raise PeerMappingError(f"peer mapping failed on some rank ({err or 'other rank'})")
         self.epoch = 0
         self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
         self.replica = self.hub.weights()
