@@ -300,6 +300,10 @@ typedef struct {
     uint32_t credit_base;
     uint32_t credit_window;     /* blocks the producer may run ahead                 */
     uint32_t* credit_return;    /* consumer: counter to advance per finished block   */
+    int32_t per_warp;           /* block form: 0 = each CTA takes and signals blocks
+                                   (block_elems multiple of 2048); nonzero = each WARP
+                                   does (multiple of 256): small blocks, short pipeline
+                                   fill, a fence stalls one warp instead of the CTA   */
 } phub_sync;
 
 /* Chained exchange (workers hosted in rank order): the

@@ -94,7 +94,7 @@ struct phub_ctx_s {
                                       // registered (NVLink latency; profiles/r01_multi2)
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
-    int blocks_occ[2][phub::kMaxWorkers + 1] = {};   // resident CTAs/SM of k_blocks [nag][nw]
+    int blocks_occ[2][2][phub::kMaxWorkers + 1] = {};   // resident CTAs/SM [warp][nag][nw]
     int hier_occ[2] = {0, 0};                          // resident CTAs/SM of k_hier [worker_order]
     uint64_t iteration = 0;
     int launches = 0;
@@ -662,14 +662,16 @@ static void apply_sync(phub_ctx c, phub::FlatArgs& a, const phub_sync* sync) {
         a.credit_base = sync->credit_base;
         a.credit_window = sync->credit_window;
         a.credit_return = sync->credit_return;
+        a.per_warp = sync->per_warp ? 1 : 0;
     }
 }
 
 // Block-streaming sync: blocks are whole multiples of one 256-thread x 8-element pass.
 static phub_status check_block_sync(phub_ctx c, const phub_sync* sync) {
     if (!sync || !sync->block_elems) return PHUB_OK;
-    if (sync->block_elems % 2048)
-        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block_elems must be a multiple of 2048");
+    if (sync->block_elems % (sync->per_warp ? 256 : 2048))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block_elems must be a multiple of %d",
+                       sync->per_warp ? 256 : 2048);
     if ((sync->wait_flag && reinterpret_cast<uintptr_t>(sync->wait_flag) % 4) ||
         (sync->signal_flag && reinterpret_cast<uintptr_t>(sync->signal_flag) % 4))
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block flags must be 4-B aligned");
@@ -677,12 +679,14 @@ static phub_status check_block_sync(phub_ctx c, const phub_sync* sync) {
 }
 
 // Persistent grid of a block-streaming launch: every SM x resident CTAs, at most one CTA per block.
-static int blocks_grid(phub_ctx c, int nw, bool nag, uint64_t begin, uint64_t end, uint64_t B) {
-    int& occ = c->blocks_occ[nag ? 1 : 0][std::min(nw, phub::kMaxWorkers)];
-    if (!occ) occ = phub::blocks_per_sm(nw, nag);
+static int blocks_grid(phub_ctx c, int nw, bool nag, bool warp, uint64_t begin, uint64_t end,
+                       uint64_t B) {
+    int& occ = c->blocks_occ[warp ? 1 : 0][nag ? 1 : 0][std::min(nw, phub::kMaxWorkers)];
+    if (!occ) occ = phub::blocks_per_sm(nw, nag, warp);
     const uint64_t nblk = (end + B - 1) / B - begin / B;
+    const uint64_t per_cta = warp ? phub::kThreads / 32 : 1;     // blocks in flight per CTA
     const int grid = c->grid_override ? c->grid_override : c->num_sms * occ;
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid, nblk));
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid, (nblk + per_cta - 1) / per_cta));
 }
 
 phub_status phub_sync_timeouts(phub_ctx c, uint32_t* count) {
@@ -770,7 +774,7 @@ phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count
     c->launches = 0;
     cudaError_t e;
     if (a.block) {
-        e = phub::launch_blocks(a, dst, blocks_grid(c, count, false, begin, end, a.block),
+        e = phub::launch_blocks(a, dst, blocks_grid(c, count, false, a.per_warp, begin, end, a.block),
                                 static_cast<cudaStream_t>(stream), &c->launches);
     } else {
         const uint64_t nvec = (end - begin) / 8;
@@ -832,7 +836,8 @@ phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
         const uint64_t cover = (nvec + phub::kThreads - 1) / phub::kThreads;
         if (a.block) {
             a.discard = c->consume_mask;
-            e = e_ > lo ? phub::launch_blocks(a, nullptr, blocks_grid(c, c->N, true, lo, e_, a.block),
+            e = e_ > lo ? phub::launch_blocks(a, nullptr,
+                                              blocks_grid(c, c->N, true, a.per_warp, lo, e_, a.block),
                                               static_cast<cudaStream_t>(stream), &c->launches)
                         : cudaSuccess;
         } else {

@@ -418,112 +418,144 @@ __device__ __forceinline__ bool block_wait(const FlatArgs& a, const uint32_t* fl
     return ok != 0;
 }
 
+// One 256-bit vector i of a block-streamed stage: the worker-order sum of the
+// sources, then either the fused Nesterov (w, v, replicas) or the partial sum
+// stored into dst.
+template <int NW, bool NAG>
+__device__ __forceinline__ void blocks_body(const FlatArgs& a, float* __restrict__ dst, uint64_t i) {
+    const int nw = NW > 0 ? NW : a.nw;
+    float acc[8];
+    if constexpr (NW > 0) {
+        V8 gv[NW];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) gv[k] = ld_coherent(reinterpret_cast<const V8*>(a.g[k]) + i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float s = __fadd_rn(0.0f, gv[0].x[j]);
+#pragma unroll
+            for (int k = 1; k < NW; ++k) s = __fadd_rn(s, gv[k].x[j]);
+            acc[j] = s;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+        for (int k0 = 0; k0 < nw; k0 += 8) {
+            V8 gv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < nw) gv[k] = ld_coherent(reinterpret_cast<const V8*>(a.g[k0 + k]) + i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < nw) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+                }
+        }
+    }
+    if (a.discard) {
+        // consumed inputs (PHUB_CONSUME): the lane holding the first 32 B of
+        // each 128-B line drops it from L2 once the whole warp has its data --
+        // no write-back of a staging buffer
+        __syncwarp(__activemask());
+        if ((i & 3) == 0)
+            for (int k = 0; k < nw; ++k)
+                if ((a.discard >> k) & 1)
+                    asm volatile("discard.global.L2 [%0], 128;"
+                                 :: "l"(reinterpret_cast<const V8*>(a.g[k]) + i) : "memory");
+    }
+    V8 out;
+    if constexpr (NAG) {
+        V8* w = reinterpret_cast<V8*>(a.w);
+        V8* v = reinterpret_cast<V8*>(a.v);
+        // read once per round: evict-first, so an incoming partial keeps its L2 lines
+        V8 wv = ld_state<PHUB_CACHE_BYPASS>(w + i);
+        V8 vv = ld_state<PHUB_CACHE_BYPASS>(v + i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            out.x[j] = acc[j];
+            nag(acc[j], wv.x[j], vv.x[j], a.lr, a.mu, a.rescale);
+        }
+        st_stream(w + i, wv);     // the pull is the replica stores below: keep L2
+        st_stream(v + i, vv);     // for the incoming partial, not for w'
+        if (a.agg) st_stream(reinterpret_cast<V8*>(a.agg) + i, out);
+        for (int r = 0; r < a.nrep; ++r) reinterpret_cast<V8*>(a.rep[r])[i] = wv;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) out.x[j] = acc[j];
+        reinterpret_cast<V8*>(dst)[i] = out;
+    }
+}
+
+// Bounded wait of one thread for *flag >= value (0 = gave up, counted).
+__device__ __forceinline__ int wait_bounded(const FlatArgs& a, const uint32_t* flag, uint32_t value) {
+    if (ld_acquire_sys(flag) >= value) return 1;
+    volatile uint32_t* abandoned = a.timeouts + 1;
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(flag) < value) {
+        if (*abandoned >= value) return 0;
+        if (globaltimer_ns() - t0 > 2000000000ull) {
+            atomicAdd(a.timeouts, 1u);
+            atomicMax(a.timeouts + 1, value);
+            return 0;
+        }
+        __nanosleep(100);
+    }
+    return 1;
+}
+
+// Back-pressure: block blk may start once the consumer finished blk - window blocks.
+__device__ __forceinline__ void credit_wait(const FlatArgs& a, uint64_t rel) {
+    const uint32_t need = a.credit_base + (uint32_t)rel - a.credit_window;
+    const uint64_t t0 = globaltimer_ns();
+    while ((int32_t)(ld_acquire_sys(a.credit) - need) < 0) {
+        if (globaltimer_ns() - t0 > 2000000000ull) {
+            atomicAdd(a.timeouts, 1u);
+            break;
+        }
+        __nanosleep(100);
+    }
+}
+
+// CTA-granular: each CTA takes a block (multiple of 2048 elements) per ticket.
 template <int NW, bool NAG>
 __global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ FlatArgs a,
                                                      float* __restrict__ dst) {
     const uint64_t B = a.block;
     const uint64_t b0 = a.begin / B, b1 = (a.end + B - 1) / B;
-    const int nw = NW > 0 ? NW : a.nw;
     __shared__ uint64_t s_blk;
+    __shared__ int s_go;
     for (;;) {
         // dynamic ticket: CTAs take blocks in global order as they free up, so
         // this stage's front follows the upstream stage's front closely
-        if (threadIdx.x == 0) s_blk = b0 + atomicAdd(a.ticket, 1u);
+        if (threadIdx.x == 0) {
+            const uint64_t blk = b0 + atomicAdd(a.ticket, 1u);
+            int go = 1;
+            if (blk < b1) {
+                if (a.credit && blk - b0 >= a.credit_window) credit_wait(a, blk - b0);
+                if (a.wait_flag) go = wait_bounded(a, a.wait_flag + blk, a.wait_value);
+            }
+            s_blk = blk;
+            s_go = go;
+        }
         __syncthreads();
         const uint64_t blk = s_blk;
+        const bool go = s_go != 0;
         if (blk >= b1) break;
-        if (a.credit && blk - b0 >= a.credit_window) {
-            // back-pressure: stay at most credit_window blocks ahead of the consumer
-            if (threadIdx.x == 0) {
-                const uint32_t need = a.credit_base + (uint32_t)(blk - b0) - a.credit_window;
-                const uint64_t t0 = globaltimer_ns();
-                while ((int32_t)(ld_acquire_sys(a.credit) - need) < 0) {
-                    if (globaltimer_ns() - t0 > 2000000000ull) {
-                        atomicAdd(a.timeouts, 1u);
-                        break;
-                    }
-                    __nanosleep(100);
-                }
-            }
-            __syncthreads();
-        }
-        const bool go = a.wait_flag ? block_wait(a, a.wait_flag + blk) : true;
         const uint64_t lo = (blk * B > a.begin ? blk * B : a.begin) / 8;
         const uint64_t hi = ((blk + 1) * B < a.end ? (blk + 1) * B : a.end) / 8;
-        for (uint64_t i = lo + threadIdx.x; go && i < hi; i += kThreads) {
-            float acc[8];
-            if constexpr (NW > 0) {
-                V8 gv[NW];
-#pragma unroll
-                for (int k = 0; k < NW; ++k) gv[k] = ld_coherent(reinterpret_cast<const V8*>(a.g[k]) + i);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    float s = __fadd_rn(0.0f, gv[0].x[j]);
-#pragma unroll
-                    for (int k = 1; k < NW; ++k) s = __fadd_rn(s, gv[k].x[j]);
-                    acc[j] = s;
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
-                for (int k0 = 0; k0 < nw; k0 += 8) {
-                    V8 gv[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        if (k0 + k < nw) gv[k] = ld_coherent(reinterpret_cast<const V8*>(a.g[k0 + k]) + i);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        if (k0 + k < nw) {
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
-                        }
-                }
-            }
-            if (a.discard) {
-                // consumed inputs (PHUB_CONSUME): the lane holding the first
-                // 32 B of each 128-B line drops it from L2 once the whole warp
-                // has its data -- no write-back of a staging buffer
-                __syncwarp(__activemask());
-                if ((i & 3) == 0)
-                    for (int k = 0; k < nw; ++k)
-                        if ((a.discard >> k) & 1)
-                            asm volatile("discard.global.L2 [%0], 128;"
-                                         :: "l"(reinterpret_cast<const V8*>(a.g[k]) + i) : "memory");
-            }
-            V8 out;
-            if constexpr (NAG) {
-                V8* w = reinterpret_cast<V8*>(a.w);
-                V8* v = reinterpret_cast<V8*>(a.v);
-                // read once per round: evict-first, so an incoming partial keeps its L2 lines
-                V8 wv = ld_state<PHUB_CACHE_BYPASS>(w + i);
-                V8 vv = ld_state<PHUB_CACHE_BYPASS>(v + i);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    out.x[j] = acc[j];
-                    nag(acc[j], wv.x[j], vv.x[j], a.lr, a.mu, a.rescale);
-                }
-                st_stream(w + i, wv);     // the pull is the replica stores below: keep L2
-                st_stream(v + i, vv);     // for the incoming partial, not for w'
-                if (a.agg) st_stream(reinterpret_cast<V8*>(a.agg) + i, out);
-                for (int r = 0; r < a.nrep; ++r) reinterpret_cast<V8*>(a.rep[r])[i] = wv;
-            } else {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) out.x[j] = acc[j];
-                reinterpret_cast<V8*>(dst)[i] = out;
-            }
-        }
-        // bar.sync (also retires this block's `ok` before the next wait) then
-        // one system-scope fence: cumulative over the CTA's stores (the
+        for (uint64_t i = lo + threadIdx.x; go && i < hi; i += kThreads) blocks_body<NW, NAG>(a, dst, i);
+        // bar.sync (also retires s_blk / s_go before the next ticket) then one
+        // system-scope fence: cumulative over the CTA's stores (the
         // cooperative-groups grid-sync pattern)
         __syncthreads();
-        if (a.signal_flag) {
-            if (threadIdx.x == 0 && go) {
+        if (threadIdx.x == 0) {
+            if (a.signal_flag && go) {
                 __threadfence_system();
                 st_release_sys(a.signal_flag + blk, a.signal_value);
             }
+            // flow control only (the producer never rewrites a block within a round)
+            if (a.credit_return) atomicAdd_system(a.credit_return, 1u);
         }
-        // flow control only (the producer never rewrites a block within a round)
-        if (a.credit_return && threadIdx.x == 0) atomicAdd_system(a.credit_return, 1u);
     }
     if (NAG && a.nrep) __threadfence_system();
     // the last CTA out resets the tickets for the next launch (stream-ordered)
@@ -533,20 +565,70 @@ __global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ Fla
     }
 }
 
-template <bool NAG>
-void* pick_blocks(int nw) {
-    switch (nw) {
-        case 1: return (void*)k_blocks<1, NAG>;
-        case 2: return (void*)k_blocks<2, NAG>;
-        case 3: return (void*)k_blocks<3, NAG>;
-        case 4: return (void*)k_blocks<4, NAG>;
-        case 5: return (void*)k_blocks<5, NAG>;
-        case 6: return (void*)k_blocks<6, NAG>;
-        case 7: return (void*)k_blocks<7, NAG>;
-        case 8: return (void*)k_blocks<8, NAG>;
-        case 9: return (void*)k_blocks<9, NAG>;
-        default: return (void*)k_blocks<0, NAG>;
+// Warp-granular: each WARP takes, processes and signals its own block (a
+// multiple of 256 elements).  No CTA barrier anywhere: a warp waiting in its
+// system-scope fence (its NVLink stores being acknowledged) stalls only
+// itself, so blocks can be small -- a short pipeline fill -- without the
+// per-block fence idling the SM.
+template <int NW, bool NAG>
+__global__ void __launch_bounds__(kThreads) k_wblocks(const __grid_constant__ FlatArgs a,
+                                                      float* __restrict__ dst) {
+    const uint64_t B = a.block;
+    const uint64_t b0 = a.begin / B, b1 = (a.end + B - 1) / B;
+    const unsigned lane = threadIdx.x & 31;
+    constexpr unsigned FULL = 0xffffffffu;
+    for (;;) {
+        uint64_t blk = 0;
+        int go = 1;
+        if (lane == 0) {
+            blk = b0 + atomicAdd(a.ticket, 1u);
+            if (blk < b1) {
+                if (a.credit && blk - b0 >= a.credit_window) credit_wait(a, blk - b0);
+                if (a.wait_flag) go = wait_bounded(a, a.wait_flag + blk, a.wait_value);
+            }
+        }
+        blk = __shfl_sync(FULL, blk, 0);
+        go = __shfl_sync(FULL, go, 0);
+        if (blk >= b1) break;
+        const uint64_t lo = (blk * B > a.begin ? blk * B : a.begin) / 8;
+        const uint64_t hi = ((blk + 1) * B < a.end ? (blk + 1) * B : a.end) / 8;
+        for (uint64_t i = lo + lane; go && i < hi; i += 32) blocks_body<NW, NAG>(a, dst, i);
+        __syncwarp();                        // orders the warp's stores before lane 0's fence
+        if (lane == 0) {
+            if (a.signal_flag && go) {
+                __threadfence_system();
+                st_release_sys(a.signal_flag + blk, a.signal_value);
+            }
+            if (a.credit_return) atomicAdd_system(a.credit_return, 1u);
+        }
     }
+    if (NAG && a.nrep) __threadfence_system();
+    if (lane == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x * (kThreads / 32) - 1) {
+        a.ticket[0] = 0;
+        a.ticket[1] = 0;
+    }
+}
+
+template <bool NAG, bool WARP>
+void* pick_blocks_t(int nw) {
+#define PHUB_KB(n) (WARP ? (void*)k_wblocks<n, NAG> : (void*)k_blocks<n, NAG>)
+    switch (nw) {
+        case 1: return PHUB_KB(1);
+        case 2: return PHUB_KB(2);
+        case 3: return PHUB_KB(3);
+        case 4: return PHUB_KB(4);
+        case 5: return PHUB_KB(5);
+        case 6: return PHUB_KB(6);
+        case 7: return PHUB_KB(7);
+        case 8: return PHUB_KB(8);
+        case 9: return PHUB_KB(9);
+        default: return PHUB_KB(0);
+    }
+#undef PHUB_KB
+}
+template <bool NAG>
+void* pick_blocks(int nw, bool warp) {
+    return warp ? pick_blocks_t<NAG, true>(nw) : pick_blocks_t<NAG, false>(nw);
 }
 
 // ------------------------------------------- hierarchical reduction (NEXT-4)
@@ -1046,16 +1128,16 @@ cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t 
     return cudaGetLastError();
 }
 
-int blocks_per_sm(int nw, bool nag) {
+int blocks_per_sm(int nw, bool nag, bool warp) {
     int nb = 0;
-    const void* fn = nag ? pick_blocks<true>(nw) : pick_blocks<false>(nw);
+    const void* fn = nag ? pick_blocks<true>(nw, warp) : pick_blocks<false>(nw, warp);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches) {
     if (a.end <= a.begin || a.block == 0) return cudaSuccess;
-    void* fn = dst ? pick_blocks<false>(a.nw) : pick_blocks<true>(a.nw);
+    void* fn = dst ? pick_blocks<false>(a.nw, a.per_warp != 0) : pick_blocks<true>(a.nw, a.per_warp != 0);
     void* args[] = {const_cast<FlatArgs*>(&a), &dst};
     cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);
     ++*launches;

@@ -42,6 +42,7 @@ struct FlatArgs {
     const uint32_t* credit;           // back-pressure (block streaming): see phub_sync
     uint32_t credit_base, credit_window;
     uint32_t* credit_return;
+    int per_warp;                     // block streaming: warps (not CTAs) take/signal blocks
 };
 
 // Hierarchical reduction: one GPU = one rack's PBox with its P
@@ -105,7 +106,7 @@ cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t 
 // raising a.signal_flag[b] per block.  dst == nullptr: fused Nesterov (w, v,
 // replicas); else the worker-order partial sum stored into dst.
 cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches);
-int blocks_per_sm(int nw, bool nag);
+int blocks_per_sm(int nw, bool nag, bool warp);
 // TMA-style staging: 1-D bulk async copies into a shared-memory ring (nw <= 8).
 cudaError_t launch_bulk(const FlatArgs& a, int grid, cudaStream_t s, int* launches);
 size_t bulk_smem_bytes(int nw);

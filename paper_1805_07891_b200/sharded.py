@@ -391,7 +391,7 @@ class ChainShardedPHub:
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
                  device=None, group=None, pieces=8, sync="blocks", nslots=2, block=16384,
-                 pull=False, consume=True, window=0):
+                 pull=False, consume=True, window=0, per_warp=False):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -406,6 +406,8 @@ class ChainShardedPHub:
         self.consume = bool(consume)
         # back-pressure (blocks only): a producer runs at most `window` blocks ahead
         self.window = int(window) if sync == "blocks" else 0
+        # per_warp: warps (not CTAs) take and signal blocks (block a multiple of 256)
+        self.per_warp = bool(per_warp) and sync == "blocks"
         self._epoch = 0
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
@@ -531,12 +533,13 @@ class ChainShardedPHub:
             credit = (self._credit, (ep - 1) * self._nblk, self.window) if self._credit else None
             if self.last:
                 capi.phub_aggregate_range(self.hub.ctx, 0, Ep, stream, wait=wait, block=self.block,
-                                          credit_return=self._prev_credit)
+                                          credit_return=self._prev_credit, per_warp=self.per_warp)
             else:
                 dst = self._pout if self.pull else self._next_in
                 capi.phub_partial_sum(self.hub.ctx, srcs, dst, 0, Ep, stream, wait=wait,
                                       signal=(self._next_flags, ep), block=self.block,
-                                      credit=credit, credit_return=self._prev_credit)
+                                      credit=credit, credit_return=self._prev_credit,
+                                      per_warp=self.per_warp)
             self.barrier()                   # replicas complete; buffers free for the next round
             return
         if self.sync == "flags":

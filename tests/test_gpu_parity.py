@@ -671,8 +671,10 @@ def test_stage_flags_signal_and_bounded_wait():
     tail.close()
 
 
-@pytest.mark.parametrize("block,mode", [(2048, "borrow"), (32768, "borrow"), (16384, "consume")])
-def test_block_streaming_flags_chain_on_one_gpu(block, mode):
+@pytest.mark.parametrize("block,mode,per_warp", [(2048, "borrow", False), (32768, "borrow", False),
+                                                (16384, "consume", False), (768, "borrow", True),
+                                                (4096, "consume", True)])
+def test_block_streaming_flags_chain_on_one_gpu(block, mode, per_warp):
     """phub_sync block form: a partial sum raises one flag per block and a
     range aggregate waits on them block by block (same stream here: the
     producer finishes first, so no kernel waits on a co-resident one) --
@@ -691,15 +693,16 @@ def test_block_streaming_flags_chain_on_one_gpu(block, mode):
     st = head._stream(None)
     with pytest.raises(PhubError):
         capi.phub_partial_sum(head.ctx, [g.data_ptr() for g in gd[:3]], part.data_ptr(), 0, Ep,
-                              st, signal=(flags.data_ptr(), 3), block=1000)
+                              st, signal=(flags.data_ptr(), 3), block=1000, per_warp=per_warp)
     capi.phub_partial_sum(head.ctx, [g.data_ptr() for g in gd[:3]], part.data_ptr(), 0, Ep, st,
-                          signal=(flags.data_ptr(), 3), block=block)
+                          signal=(flags.data_ptr(), 3), block=block, per_warp=per_warp)
     tail = PHub(sizes, 4, device=0, rescale=1.0 / 6, keep_aggregate=True)
     tail.load_state(w0, v0)
     tail.push(0, part, mode=mode)          # consume: its L2 lines may be discarded after reading
     for k in range(3):
         tail.push(1 + k, gd[3 + k])
-    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 3), block=block)
+    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 3), block=block,
+                              per_warp=per_warp)
     torch.cuda.synchronize()
     assert tail.iteration == 1
     f = flags.cpu().numpy()
@@ -713,7 +716,8 @@ def test_block_streaming_flags_chain_on_one_gpu(block, mode):
     # flags never raised for epoch 4: the waits expire once (~2 s), the work is skipped
     for k in range(4):
         tail.push(k, gd[k])
-    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 4), block=block)
+    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 4), block=block,
+                              per_warp=per_warp)
     torch.cuda.synchronize()
     assert capi.phub_sync_timeouts(tail.ctx) >= 1
     head.close()
