@@ -392,32 +392,6 @@ __device__ __forceinline__ V8 ld_coherent(const V8* p) {
     return r;
 }
 
-// Thread 0 waits for flag >= value (bounded, like stage_wait); the CTA learns
-// the outcome through shared memory.
-__device__ __forceinline__ bool block_wait(const FlatArgs& a, const uint32_t* flag) {
-    __shared__ int ok;
-    if (threadIdx.x == 0) {
-        volatile uint32_t* abandoned = a.timeouts + 1;
-        int good = 1;
-        if (ld_acquire_sys(flag) < a.wait_value) {
-            const uint64_t t0 = globaltimer_ns();
-            while (ld_acquire_sys(flag) < a.wait_value) {
-                if (*abandoned >= a.wait_value) { good = 0; break; }
-                if (globaltimer_ns() - t0 > 2000000000ull) {
-                    atomicAdd(a.timeouts, 1u);
-                    atomicMax(a.timeouts + 1, a.wait_value);
-                    good = 0;
-                    break;
-                }
-                __nanosleep(100);
-            }
-        }
-        ok = good;
-    }
-    __syncthreads();
-    return ok != 0;
-}
-
 // One 256-bit vector i of a block-streamed stage: the worker-order sum of the
 // sources, then either the fused Nesterov (w, v, replicas) or the partial sum
 // stored into dst.
