@@ -79,6 +79,8 @@ def parse():
                     help="chain mode: push the incoming partial as BORROW, not CONSUME")
     ap.add_argument("--chain-producer-grid", type=int, default=0,
                     help="chain mode: CTAs of the partial-sum launch on non-last ranks")
+    ap.add_argument("--chain-consumer-grid", type=int, default=0,
+                    help="chain mode: CTAs of the fused launch on the last rank")
     ap.add_argument("--mode", default="auto",
                     choices=["auto", "p2p", "push", "chain", "nccl", "allreduce", "hier"],
                     help="N>1 exchange of the 8-worker job: chained (chain) or owner-sharded "
@@ -405,9 +407,11 @@ def bench_multi(args, mname, N, cb):
                                   sync=args.chain_sync, block=args.chain_block,
                                   pull=args.chain_pull, consume=not args.chain_no_consume,
                                   window=args.chain_window, per_warp=args.chain_per_warp)
+            from paper_1805_07891_b200 import capi as _c
             if args.chain_producer_grid and not sh.last:
-                from paper_1805_07891_b200 import capi as _c
                 sh.hub.set_option(_c.PHUB_OPT_GRID, args.chain_producer_grid)
+            if args.chain_consumer_grid and sh.last:
+                sh.hub.set_option(_c.PHUB_OPT_GRID, args.chain_consumer_grid)
         else:
             cls = {"p2p": P2PShardedPHub, "nccl": ShardedPHub,
                    "allreduce": AllReduceBaseline}[args.mode]
