@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
     ap.add_argument("--pieces", type=int, default=8, help="chain mode pipeline pieces")
     ap.add_argument("--chain-sync", default="blocks", choices=["blocks", "flags", "barrier"])
-    ap.add_argument("--chain-block", type=int, default=16384,
+    ap.add_argument("--chain-block", type=int, default=12288,
                     help="chain mode: elements per block flag (sync=blocks)")
     ap.add_argument("--hier-block", type=int, default=32768,
                     help="hier mode: elements per block flag")

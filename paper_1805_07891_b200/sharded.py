@@ -390,7 +390,7 @@ class ChainShardedPHub:
     """
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, pieces=8, sync="blocks", nslots=2, block=16384,
+                 device=None, group=None, pieces=8, sync="blocks", nslots=2, block=12288,
                  pull=False, consume=True, window=0, per_warp=False):
         import torch
         import torch.distributed as dist
