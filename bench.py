@@ -71,6 +71,8 @@ def parse():
                     help="push mode: elements per block flag")
     ap.add_argument("--chain-pull", action="store_true",
                     help="chain mode: next rank reads the partial over NVLink (default: pushed)")
+    ap.add_argument("--chain-oneshot", action="store_true",
+                    help="chain mode: last rank's fused launch is one CTA per 2048 elements")
     ap.add_argument("--chain-per-warp", action="store_true",
                     help="chain mode: warps (not CTAs) take and signal blocks")
     ap.add_argument("--chain-window", type=int, default=0,
@@ -406,7 +408,8 @@ def bench_multi(args, mname, N, cb):
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
                                   sync=args.chain_sync, block=args.chain_block,
                                   pull=args.chain_pull, consume=not args.chain_no_consume,
-                                  window=args.chain_window, per_warp=args.chain_per_warp)
+                                  window=args.chain_window, per_warp=args.chain_per_warp,
+                                  oneshot=args.chain_oneshot)
             from paper_1805_07891_b200 import capi as _c
             if args.chain_producer_grid and not sh.last:
                 sh.hub.set_option(_c.PHUB_OPT_GRID, args.chain_producer_grid)

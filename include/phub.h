@@ -304,6 +304,10 @@ typedef struct {
                                    (block_elems multiple of 2048); nonzero = each WARP
                                    does (multiple of 256): small blocks, short pipeline
                                    fill, a fence stalls one warp instead of the CTA   */
+    int32_t oneshot;            /* block form, phub_aggregate_range without signal /
+                                   credit_return / per_warp only: one CTA per 2048
+                                   elements over the range (the hardware scheduler
+                                   orders them), each waiting for its block's flag   */
 } phub_sync;
 
 /* Chained exchange (workers hosted in rank order): the

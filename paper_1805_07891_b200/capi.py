@@ -44,7 +44,8 @@ class phub_sync(C.Structure):
                 ("signal_flag", C.c_void_p), ("signal_value", C.c_uint32),
                 ("block_elems", C.c_uint64), ("credit", C.c_void_p),
                 ("credit_base", C.c_uint32), ("credit_window", C.c_uint32),
-                ("credit_return", C.c_void_p), ("per_warp", C.c_int32)]
+                ("credit_return", C.c_void_p), ("per_warp", C.c_int32),
+                ("oneshot", C.c_int32)]
 
 
 class phub_hier(C.Structure):
@@ -196,7 +197,8 @@ def phub_aggregate_ready(ctx, stream: int = 0) -> int:
     return int(n.value)
 
 
-def _sync(wait=None, signal=None, block=0, credit=None, credit_return=None, per_warp=False):
+def _sync(wait=None, signal=None, block=0, credit=None, credit_return=None, per_warp=False,
+          oneshot=False):
     """phub_sync from (flag_ptr, value) pairs; None when nothing is given.
     block > 0: the flag pointers are per-block arrays (block-streaming form);
     credit = (counter_ptr, base, window) on a producer, credit_return = a
@@ -214,14 +216,16 @@ def _sync(wait=None, signal=None, block=0, credit=None, credit_return=None, per_
     if credit_return is not None:
         s.credit_return = credit_return
     s.per_warp = int(bool(per_warp))
+    s.oneshot = int(bool(oneshot))
     return C.byref(s)
 
 
 def phub_aggregate_range(ctx, begin: int, end: int, stream: int = 0, wait=None, signal=None,
-                         block: int = 0, credit=None, credit_return=None, per_warp=False):
+                         block: int = 0, credit=None, credit_return=None, per_warp=False,
+                         oneshot=False):
     _check(_lib.phub_aggregate_range(ctx, begin, end,
-                                     _sync(wait, signal, block, credit, credit_return, per_warp),
-                                     stream), "phub_aggregate_range", ctx)
+                                     _sync(wait, signal, block, credit, credit_return, per_warp,
+                                           oneshot), stream), "phub_aggregate_range", ctx)
 
 
 def phub_partial_sum(ctx, srcs, dst: int, begin: int, end: int, stream: int = 0, wait=None,

@@ -663,12 +663,16 @@ static void apply_sync(phub_ctx c, phub::FlatArgs& a, const phub_sync* sync) {
         a.credit_window = sync->credit_window;
         a.credit_return = sync->credit_return;
         a.per_warp = sync->per_warp ? 1 : 0;
+        a.oneshot = sync->oneshot ? 1 : 0;
     }
 }
 
 // Block-streaming sync: blocks are whole multiples of one 256-thread x 8-element pass.
 static phub_status check_block_sync(phub_ctx c, const phub_sync* sync) {
     if (!sync || !sync->block_elems) return PHUB_OK;
+    if (sync->oneshot && (sync->per_warp || sync->signal_flag || sync->credit_return))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT,
+                       "oneshot is for a fused consumer launch: no per_warp, signal or credit_return");
     if (sync->block_elems % (sync->per_warp ? 256 : 2048))
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block_elems must be a multiple of %d",
                        sync->per_warp ? 256 : 2048);

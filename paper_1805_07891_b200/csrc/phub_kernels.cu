@@ -583,6 +583,24 @@ __global__ void __launch_bounds__(kThreads) k_wblocks(const __grid_constant__ Fl
     }
 }
 
+// One-shot consumer: one CTA per 2048 elements over the whole range (the
+// hardware block scheduler hands CTAs out in order, like k_flat's one-shot
+// schedule); each CTA waits for the upstream flag of the block holding its
+// elements, then runs the fused step on one 256-bit vector per thread.
+template <int NW>
+__global__ void __launch_bounds__(kThreads) k_oneshot_consume(const __grid_constant__ FlatArgs a) {
+    __shared__ int s_go;
+    const uint64_t i = a.begin / 8 + (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (threadIdx.x == 0) {
+        const uint64_t blk = (a.begin + (uint64_t)blockIdx.x * kThreads * 8) / a.block;
+        s_go = a.wait_flag ? wait_bounded(a, a.wait_flag + blk, a.wait_value) : 1;
+    }
+    __syncthreads();
+    if (s_go && i < a.end / 8) blocks_body<NW, true>(a, nullptr, i);
+    // no per-CTA system fence: the replica stores are ordered before the
+    // caller's next stream operation by the kernel boundary
+}
+
 template <bool NAG, bool WARP>
 void* pick_blocks_t(int nw) {
 #define PHUB_KB(n) (WARP ? (void*)k_wblocks<n, NAG> : (void*)k_blocks<n, NAG>)
@@ -603,6 +621,21 @@ void* pick_blocks_t(int nw) {
 template <bool NAG>
 void* pick_blocks(int nw, bool warp) {
     return warp ? pick_blocks_t<NAG, true>(nw) : pick_blocks_t<NAG, false>(nw);
+}
+
+void* pick_oneshot(int nw) {
+    switch (nw) {
+        case 1: return (void*)k_oneshot_consume<1>;
+        case 2: return (void*)k_oneshot_consume<2>;
+        case 3: return (void*)k_oneshot_consume<3>;
+        case 4: return (void*)k_oneshot_consume<4>;
+        case 5: return (void*)k_oneshot_consume<5>;
+        case 6: return (void*)k_oneshot_consume<6>;
+        case 7: return (void*)k_oneshot_consume<7>;
+        case 8: return (void*)k_oneshot_consume<8>;
+        case 9: return (void*)k_oneshot_consume<9>;
+        default: return (void*)k_oneshot_consume<0>;
+    }
 }
 
 // ------------------------------------------- hierarchical reduction (NEXT-4)
@@ -1111,6 +1144,14 @@ int blocks_per_sm(int nw, bool nag, bool warp) {
 
 cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches) {
     if (a.end <= a.begin || a.block == 0) return cudaSuccess;
+    if (a.oneshot && !dst) {                          // one CTA per 2048 elements
+        const uint64_t ctas = (a.end / 8 - a.begin / 8 + kThreads - 1) / kThreads;
+        void* args[] = {const_cast<FlatArgs*>(&a)};
+        cudaError_t e = cudaLaunchKernel(pick_oneshot(a.nw), dim3((unsigned)ctas), dim3(kThreads),
+                                         args, 0, s);
+        ++*launches;
+        return e;
+    }
     void* fn = dst ? pick_blocks<false>(a.nw, a.per_warp != 0) : pick_blocks<true>(a.nw, a.per_warp != 0);
     void* args[] = {const_cast<FlatArgs*>(&a), &dst};
     cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);

@@ -43,6 +43,7 @@ struct FlatArgs {
     uint32_t credit_base, credit_window;
     uint32_t* credit_return;
     int per_warp;                     // block streaming: warps (not CTAs) take/signal blocks
+    int oneshot;                      // block streaming, fused consumer: one CTA per 2048 elements
 };
 
 // Hierarchical reduction: one GPU = one rack's PBox with its P

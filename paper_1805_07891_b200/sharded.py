@@ -391,7 +391,7 @@ class ChainShardedPHub:
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
                  device=None, group=None, pieces=8, sync="blocks", nslots=2, block=12288,
-                 pull=False, consume=True, window=0, per_warp=False):
+                 pull=False, consume=True, window=0, per_warp=False, oneshot=False):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -408,6 +408,8 @@ class ChainShardedPHub:
         self.window = int(window) if sync == "blocks" else 0
         # per_warp: warps (not CTAs) take and signal blocks (block a multiple of 256)
         self.per_warp = bool(per_warp) and sync == "blocks"
+        # oneshot: the last rank's fused launch is one CTA per 2048 elements
+        self.oneshot = bool(oneshot) and sync == "blocks" and not self.window
         self._epoch = 0
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
@@ -533,7 +535,8 @@ class ChainShardedPHub:
             credit = (self._credit, (ep - 1) * self._nblk, self.window) if self._credit else None
             if self.last:
                 capi.phub_aggregate_range(self.hub.ctx, 0, Ep, stream, wait=wait, block=self.block,
-                                          credit_return=self._prev_credit, per_warp=self.per_warp)
+                                          credit_return=self._prev_credit, per_warp=self.per_warp,
+                                          oneshot=self.oneshot and self.world > 1)
             else:
                 dst = self._pout if self.pull else self._next_in
                 capi.phub_partial_sum(self.hub.ctx, srcs, dst, 0, Ep, stream, wait=wait,

@@ -36,10 +36,12 @@ def main():
         # chain: block-streaming flags, partial pushed to the next rank;
         # chain_pull: ... read by the next rank; chain_flags / chain_barrier: per piece
         sync = {"chain": "blocks", "chain_pull": "blocks", "chain_window": "blocks",
-                "chain_warp": "blocks", "chain_flags": "flags", "chain_barrier": "barrier"}[mode]
+                "chain_warp": "blocks", "chain_oneshot": "blocks", "chain_flags": "flags",
+                "chain_barrier": "barrier"}[mode]
         sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=3, sync=sync,
                               block=512 if mode == "chain_warp" else 2048,
                               pull=mode == "chain_pull", per_warp=mode == "chain_warp",
+                              oneshot=mode == "chain_oneshot",
                               window=3 if mode == "chain_window" else 0)
     elif mode == "push":
         sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048)

@@ -25,7 +25,7 @@ def _port():
 
 
 @pytest.mark.parametrize("mode", ["nccl", "p2p", "push", "chain", "chain_pull", "chain_window",
-                                  "chain_warp", "chain_flags", "chain_barrier"])
+                                  "chain_warp", "chain_oneshot", "chain_flags", "chain_barrier"])
 @pytest.mark.parametrize("G,name,N,cb,rounds", [
     (2, "small", 8, 32768, 2), (2, "tiny", 4, 4096, 1), (4, "resnet50", 8, 32768, 2),
     (8, "resnet50", 8, 32768, 2), (8, "small", 8, 64, 1), (2, "one", 2, 32768, 2),

@@ -671,10 +671,11 @@ def test_stage_flags_signal_and_bounded_wait():
     tail.close()
 
 
-@pytest.mark.parametrize("block,mode,per_warp", [(2048, "borrow", False), (32768, "borrow", False),
-                                                (16384, "consume", False), (768, "borrow", True),
-                                                (4096, "consume", True)])
-def test_block_streaming_flags_chain_on_one_gpu(block, mode, per_warp):
+@pytest.mark.parametrize("block,mode,per_warp,oneshot", [
+    (2048, "borrow", False, False), (32768, "borrow", False, False),
+    (16384, "consume", False, False), (768, "borrow", True, False), (4096, "consume", True, False),
+    (12288, "borrow", False, True), (2048, "consume", False, True)])
+def test_block_streaming_flags_chain_on_one_gpu(block, mode, per_warp, oneshot):
     """phub_sync block form: a partial sum raises one flag per block and a
     range aggregate waits on them block by block (same stream here: the
     producer finishes first, so no kernel waits on a co-resident one) --
@@ -702,7 +703,7 @@ def test_block_streaming_flags_chain_on_one_gpu(block, mode, per_warp):
     for k in range(3):
         tail.push(1 + k, gd[3 + k])
     capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 3), block=block,
-                              per_warp=per_warp)
+                              per_warp=per_warp, oneshot=oneshot)
     torch.cuda.synchronize()
     assert tail.iteration == 1
     f = flags.cpu().numpy()
@@ -717,7 +718,7 @@ def test_block_streaming_flags_chain_on_one_gpu(block, mode, per_warp):
     for k in range(4):
         tail.push(k, gd[k])
     capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 4), block=block,
-                              per_warp=per_warp)
+                              per_warp=per_warp, oneshot=oneshot)
     torch.cuda.synchronize()
     assert capi.phub_sync_timeouts(tail.ctx) >= 1
     head.close()
