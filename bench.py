@@ -784,6 +784,9 @@ def bench_single(args, mname, N, cb):
     if not args.no_cpu:
         cpu = cpu_oracle_sample(mname, N, cb, args.cpu_seconds)
         cpu = {k: v for k, v in cpu.items() if not k.startswith("_")}
+        # the oracle is timed both on all host cores and on one
+        one = cpu_oracle_sample(mname, N, cb, min(3.0, args.cpu_seconds), nthreads=1)
+        cpu["single_thread"] = {"value": one["value"], "unit": "GB/s", "cores": 1}
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
