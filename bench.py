@@ -63,8 +63,8 @@ def parse():
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
     ap.add_argument("--pieces", type=int, default=8, help="chain mode pipeline pieces")
     ap.add_argument("--chain-sync", default="blocks", choices=["blocks", "flags", "barrier"])
-    ap.add_argument("--chain-block", type=int, default=12288,
-                    help="chain mode: elements per block flag (sync=blocks)")
+    ap.add_argument("--chain-block", type=int, default=0,
+                    help="chain mode: elements per block flag (sync=blocks; 0 = by model size)")
     ap.add_argument("--hier-block", type=int, default=32768,
                     help="hier mode: elements per block flag")
     ap.add_argument("--push-block", type=int, default=16384,
@@ -85,10 +85,10 @@ def parse():
                     help="chain mode: CTAs of the fused launch on the last rank")
     ap.add_argument("--mode", default="auto",
                     choices=["auto", "p2p", "push", "chain", "nccl", "allreduce", "hier"],
-                    help="N>1 exchange of the 8-worker job: chained (chain) or owner-sharded "
-                         "(p2p) peer-memory kernels, NCCL send/recv (nccl), NCCL all-reduce "
-                         "baseline (allreduce); hier: hierarchical reduction, one 8-worker "
-                         "rack per GPU (SURVEY NEXT-4, weak scaling)")
+                    help="N>1 exchange of the 8-worker job: chained (chain), owner-sharded "
+                         "all-store (push) or peer-load (p2p) kernels, NCCL send/recv (nccl), "
+                         "NCCL all-reduce baseline (allreduce); hier: hierarchical reduction, "
+                         "one 8-worker rack per GPU (SURVEY NEXT-4, weak scaling)")
     return ap.parse_args()
 
 
@@ -627,7 +627,7 @@ def bench_multi(args, mname, N, cb):
                                (f"M3 (full exchange) chain: rank-ordered partial sums over "
                                 f"NVLink, last rank fused Nesterov + replica stores, " +
                                 (f"one launch per rank streamed by per-block device flags "
-                                 f"({args.chain_block} elements/block, partial "
+                                 f"({sh.block} elements/block, partial "
                                  f"{'pulled' if args.chain_pull else 'pushed'})"
                                  if args.chain_sync == "blocks" else
                                  f"pipelined over {args.pieces} pieces ({args.chain_sync} sync)"))

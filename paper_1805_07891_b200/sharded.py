@@ -364,6 +364,14 @@ def chain_nvlink_bytes(E_padded: int, world: int, rank: int):
     return out, inn
 
 
+def chain_block_for(E_padded: int) -> int:
+    """Block size of the block-streamed chain (elements): 8K blocks up to 64 M
+    elements, 12K above -- measured optimum at G = 2 (profiles/r01_chain_blocks:
+    ResNet-50 / AlexNet best at 8K, VGG-19 at 12K; smaller blocks pay the
+    per-block fence, larger ones the pipeline fill)."""
+    return 8192 if E_padded < (64 << 20) else 12288
+
+
 class ChainShardedPHub:
     """Chained exchange.
 
@@ -390,7 +398,7 @@ class ChainShardedPHub:
     """
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, pieces=8, sync="blocks", nslots=2, block=12288,
+                 device=None, group=None, pieces=8, sync="blocks", nslots=2, block=0,
                  pull=False, consume=True, window=0, per_warp=False, oneshot=False):
         import torch
         import torch.distributed as dist
@@ -401,7 +409,7 @@ class ChainShardedPHub:
         if sync not in ("blocks", "flags", "barrier"):
             raise ValueError("sync must be 'blocks', 'flags' or 'barrier'")
         self.sync = sync
-        self.block = int(block)
+        self.block = int(block)          # 0: chosen from the model size below
         self.pull = bool(pull) and sync == "blocks"
         self.consume = bool(consume)
         # back-pressure (blocks only): a producer runs at most `window` blocks ahead
@@ -424,6 +432,8 @@ class ChainShardedPHub:
             self.hub = PHub(key_sizes, per, chunk_size_bytes=chunk_size_bytes, lr=lr,
                             momentum=momentum, device=dev)
         Ep = self.hub.E_padded
+        if self.block <= 0:
+            self.block = chain_block_for(Ep)
         self.nslots = int(nslots)
         self._own = {(sl, w): capi.phub_alloc_shared(dev, 4 * Ep)
                      for sl in range(self.nslots) for w in self.plan.hosted()}

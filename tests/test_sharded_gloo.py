@@ -88,3 +88,12 @@ def test_hier_inbox_slots_and_bytes():
         assert sum(o for o, _ in outs) == sum(i for _, i in outs)
         expect = 2 * (G - 1) / G * 4 * Ep
         assert max(max(x) for x in outs) <= expect * 1.001 + 4 * 32768
+
+
+def test_chain_block_choice():
+    from paper_1805_07891_b200.sharded import chain_block_for
+    from workloads import manifest
+    for name, want in (("resnet50", 8192), ("alexnet", 8192), ("resnet269", 12288),
+                       ("vgg19", 12288)):
+        b = chain_block_for(sum(manifest(name)))
+        assert b == want and b % 2048 == 0
