@@ -67,7 +67,7 @@ def parse():
                     help="chain mode: elements per block flag (sync=blocks; 0 = by model size)")
     ap.add_argument("--hier-block", type=int, default=32768,
                     help="hier mode: elements per block flag")
-    ap.add_argument("--push-block", type=int, default=16384,
+    ap.add_argument("--push-block", type=int, default=12288,
                     help="push mode: elements per block flag")
     ap.add_argument("--chain-pull", action="store_true",
                     help="chain mode: next rank reads the partial over NVLink (default: pushed)")

@@ -522,7 +522,11 @@ class ChainShardedPHub:
     def exchange(self, slot: int = 0):
         Ep = self.hub.E_padded
         hosted = self.hosted
-        self.barrier()                       # gradients of this round are in place everywhere
+        if self.sync != "blocks" or self.pull or self._epoch == 0:
+            # every rank's kernel reads only its own gradients plus the upstream
+            # partial, whose inbox the previous round's end barrier freed; only
+            # the per-piece modes and the pulled partial need a start barrier
+            self.barrier()
         upstream = self._prev_out if self.pull else self._pin     # partial of ranks 0..p-1
         if self.last:
             w0 = 0
@@ -808,7 +812,7 @@ class PushShardedPHub(HierPHub):
     P2PShardedPHub (gradients() keyed by global worker id)."""
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, block=16384, nslots=2):
+                 device=None, group=None, block=12288, nslots=2):
         import torch.distributed as dist
         world = dist.get_world_size(group)
         if num_workers % world:
