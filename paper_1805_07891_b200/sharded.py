@@ -522,11 +522,10 @@ class ChainShardedPHub:
     def exchange(self, slot: int = 0):
         Ep = self.hub.E_padded
         hosted = self.hosted
-        if self.sync != "blocks" or self.pull or self._epoch == 0:
-            # every rank's kernel reads only its own gradients plus the upstream
-            # partial, whose inbox the previous round's end barrier freed; only
-            # the per-piece modes and the pulled partial need a start barrier
-            self.barrier()
+        # start barrier: the last rank's kernel stores w' into every other rank's
+        # replica, so every rank must be done reading its replica (e.g. the
+        # previous round's pull, enqueued after that round's end barrier) first
+        self.barrier()
         upstream = self._prev_out if self.pull else self._pin     # partial of ranks 0..p-1
         if self.last:
             w0 = 0
@@ -767,6 +766,10 @@ class HierPHub:
 
     def exchange(self, slot: int = 0):
         Ep = self.hub.E_padded
+        # start barrier: this round's kernels store w' into every rank's replica,
+        # so every rank must be done reading its replica from the previous round
+        # (e.g. a pull enqueued after that round's end barrier)
+        self.barrier()
         for k in range(self.P):
             self.hub.push(k, self._own[(slot, k)], mode="borrow", n=Ep)
         self.epoch += 1
