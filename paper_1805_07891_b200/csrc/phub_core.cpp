@@ -1147,9 +1147,19 @@ phub_status phub_hier_exchange(phub_ctx c, const phub_hier* h, void* stream) {
     const int R = h->num_racks, me = c->rank;
     if (R > 1 && (!h->inbox || !h->peer_inbox || !h->flags || !h->peer_flags))
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "inbox / flag pointers required for > 1 rack");
-    for (int q = 0; R > 1 && q < R; ++q)
-        if (q != me && (!h->inbox[q] || !h->peer_inbox[q] || !h->peer_flags[q]))
+    for (int q = 0; R > 1 && q < R; ++q) {
+        if (q == me) continue;
+        if (!h->inbox[q] || !h->peer_inbox[q] || !h->peer_flags[q])
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "rack %d: inbox / peer pointers missing", q);
+        // 256-bit accesses at padded offsets that are multiples of 8 elements
+        if (reinterpret_cast<uintptr_t>(h->inbox[q]) % 32 ||
+            reinterpret_cast<uintptr_t>(h->peer_inbox[q]) % 32 ||
+            reinterpret_cast<uintptr_t>(h->peer_flags[q]) % 4)
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "rack %d: inbox pointers must be 32-B "
+                           "aligned, flags 4-B aligned", q);
+    }
+    if (R > 1 && reinterpret_cast<uintptr_t>(h->flags) % 4)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "flags must be 4-B aligned");
     if (c->got_count != (uint64_t)c->K * c->N)
         return c->fail(PHUB_ERR_INCOMPLETE, "%llu of %llu (worker,key) pushes received (S:181)",
                        (unsigned long long)c->got_count,

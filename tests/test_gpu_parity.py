@@ -886,3 +886,34 @@ def test_hier_exchange_single_rack_and_validation():
     assert_bits_equal(w, rw, "single-rack hierarchical w")
     assert_bits_equal(v, rv, "single-rack hierarchical v")
     hub.close()
+
+
+def test_hier_exchange_rejects_bad_peer_pointers():
+    """phub_hier_exchange validates its peer tables on the host before any
+    launch: missing or misaligned inbox / flag pointers are refused and the
+    iteration is left untouched (a 2-owner context on one GPU, never launched)."""
+    from paper_1805_07891_b200 import PHub, PhubError, capi
+    sizes = manifest("tiny")
+    hub = PHub(sizes, 2, device=0, num_owners=2, owner_rank=0, owner_policy="contig")
+    gd = device_grads(hub, 2, 15)
+    for k, g in enumerate(gd):
+        hub.push(k, g)
+    buf = torch.zeros(1 << 16, device=DEV)
+    flags = torch.zeros(64, dtype=torch.int32, device=DEV)
+    p = buf.data_ptr()
+    good = dict(inbox=[0, p], peer=[0, p], pflags=[0, flags.data_ptr()])
+    bad_cases = [
+        dict(good, inbox=[0, 0]),                      # missing inbox for rack 1
+        dict(good, inbox=[0, p + 16]),                 # misaligned inbox
+        dict(good, peer=[0, p + 4]),                   # misaligned peer inbox
+        dict(good, pflags=[0, flags.data_ptr() + 2]),  # misaligned peer flags
+    ]
+    for case in bad_cases:
+        with pytest.raises(PhubError):
+            capi.phub_hier_exchange(hub.ctx, 2, 16384, case["inbox"], case["peer"],
+                                    flags.data_ptr(), case["pflags"], 1)
+    with pytest.raises(PhubError):                      # flags themselves misaligned
+        capi.phub_hier_exchange(hub.ctx, 2, 16384, good["inbox"], good["peer"],
+                                flags.data_ptr() + 1, good["pflags"], 1)
+    assert hub.iteration == 0
+    hub.close()
