@@ -677,8 +677,11 @@ static phub_status check_block_sync(phub_ctx c, const phub_sync* sync) {
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block_elems must be a multiple of %d",
                        sync->per_warp ? 256 : 2048);
     if ((sync->wait_flag && reinterpret_cast<uintptr_t>(sync->wait_flag) % 4) ||
-        (sync->signal_flag && reinterpret_cast<uintptr_t>(sync->signal_flag) % 4))
-        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block flags must be 4-B aligned");
+        (sync->signal_flag && reinterpret_cast<uintptr_t>(sync->signal_flag) % 4) ||
+        (sync->credit && reinterpret_cast<uintptr_t>(sync->credit) % 4) ||
+        (sync->credit_return && reinterpret_cast<uintptr_t>(sync->credit_return) % 4))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block flags and credit counters must be 4-B "
+                       "aligned");
     return PHUB_OK;
 }
 
