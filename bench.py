@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import datetime
 import os
 import statistics
 import sys
@@ -386,7 +387,7 @@ def bench_multi(args, mname, N, cb):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    dist.init_process_group("nccl", device_id=dev)
+    dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
     rank, G = dist.get_rank(), dist.get_world_size()
     sizes = manifest(mname)
     if args.mode == "auto":      # fewest NVLink bytes: chain at G = 2, owner-sharded (push) above

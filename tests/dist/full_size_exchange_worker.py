@@ -9,6 +9,7 @@ one by one from independently generated inputs).
 Every rank's pulled replica is checked at key starts/ends, chunk boundaries,
 owner-range and block boundaries and random elements.
 """
+import datetime
 import os
 import sys
 
@@ -45,7 +46,7 @@ def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    dist.init_process_group("nccl", device_id=dev)
+    dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
     rank, G = dist.get_rank(), dist.get_world_size()
     if mode == "auto":                       # bench.py --mode auto
         mode = "chain" if G == 2 else "push"

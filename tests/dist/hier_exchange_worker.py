@@ -6,6 +6,7 @@ small manifests, sampled elements (oracle.hier_elems) for full-size ones.
 
     torchrun --nproc-per-node G hier_exchange_worker.py NAME P CHUNK_BYTES ROUNDS BLOCK
 """
+import datetime
 import os
 import sys
 
@@ -31,7 +32,7 @@ def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    dist.init_process_group("nccl", device_id=dev)
+    dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
     rack, R = dist.get_rank(), dist.get_world_size()
     sizes = SPECIAL[name] if name in SPECIAL else manifest(name)
     E = sum(sizes)

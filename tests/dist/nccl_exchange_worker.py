@@ -4,6 +4,7 @@ Each rank hosts N/G workers, pushes through NCCL to the chunk owners, runs the
 fused kernel on its owned range and pulls the all-gather-v; after R rounds
 every rank's full replica must equal R oracle rounds bit for bit.
 """
+import datetime
 import os
 import sys
 
@@ -27,7 +28,7 @@ def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    dist.init_process_group("nccl", device_id=dev)
+    dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
     rank, G = dist.get_rank(), dist.get_world_size()
     special = {"small": [3, 3, 9408, 64, 64, 4096, 20000, 1000, 7], "one": [5]}
     sizes = special[name] if name in special else manifest(name)
