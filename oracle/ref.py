@@ -47,3 +47,24 @@ def round_(key_sizes, grads, w, v, lr, mu, rescale=0.0, chunk_bytes=32768):
         v2[a:b] = vn
         agg[a:b] = merge
     return w2, v2, agg
+
+
+def hier_round(key_sizes, rack_grads, w, v, lr, mu, rescale=0.0):
+    """Hierarchical reduction (reading R17), whole-array
+    numpy float32: per rack the worker-order sum from +0, then the racks'
+    sums added one rack after another from +0, then the same optimizer."""
+    f32 = np.float32
+    R, P = len(rack_grads), len(rack_grads[0])
+    resc = f32(1.0) / f32(R * P) if rescale == 0.0 else f32(rescale)
+    lr, mu = f32(lr), f32(mu)
+    total = np.zeros(int(sum(key_sizes)), f32)
+    for rack in rack_grads:                          # step 2: rack by rack, in rack order
+        s_r = np.zeros_like(total)                   # step 1: this rack's own merge buffer
+        for g in rack:
+            s_r = (s_r + g).astype(f32)
+        total = (total + s_r).astype(f32)
+    gg = (total * resc).astype(f32)                  # step 3: the optimizer
+    vn = ((mu * np.asarray(v, f32)).astype(f32) + gg).astype(f32)
+    t3 = (gg + (mu * vn).astype(f32)).astype(f32)
+    wn = (np.asarray(w, f32) - (lr * t3).astype(f32)).astype(f32)
+    return wn, vn, total

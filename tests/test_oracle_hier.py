@@ -84,3 +84,16 @@ def test_hier_elems_matches_round():
     ew, ev, es = oracle.hier_elems(g, w0[idx], v0[idx], 0.1, 0.9)
     for a, b in ((ew, w[idx]), (ev, v[idx]), (es, s[idx])):
         assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.parametrize("R,P", [(2, 4), (3, 2), (4, 1), (1, 5)])
+def test_independent_numpy_oracle_agrees(R, P):
+    """oracle/ref.py re-derives the hierarchical round with whole-array numpy
+    fp32 ops (no chunking, no C); it must agree with the C oracle bit for bit."""
+    from oracle import ref
+    sizes = [1000, 33, 70000, 3]
+    racks, w0, v0 = _racks(sizes, R, P, seed=6 + R)
+    cw, cv, cs = oracle.hier_round(sizes, racks, w0, v0, 0.1, 0.9, chunk_bytes=4096)
+    nw, nv, ns = ref.hier_round(sizes, racks, w0, v0, 0.1, 0.9)
+    for a, b in ((cw, nw), (cv, nv), (cs, ns)):
+        assert np.array_equal(bits(a), bits(b))
