@@ -68,6 +68,9 @@ def parse():
                     help="chain mode: elements per block flag (sync=blocks; 0 = by model size)")
     ap.add_argument("--hier-block", type=int, default=32768,
                     help="hier mode: elements per block flag")
+    ap.add_argument("--double-replica", action="store_true",
+                    help="push/hier: alternate two replica buffers per round, so a round's "
+                         "pull may overlap the next exchange (e2e)")
     ap.add_argument("--push-block", type=int, default=12288,
                     help="push mode: elements per block flag")
     ap.add_argument("--chain-pull", action="store_true",
@@ -401,10 +404,10 @@ def bench_multi(args, mname, N, cb):
     try:
         if hier:
             sh = HierPHub(sizes, workers_per_rack=N, chunk_size_bytes=cb, device=local,
-                          block=args.hier_block)
+                          block=args.hier_block, double_replica=args.double_replica)
         elif push:
             sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local,
-                                 block=args.push_block)
+                                 block=args.push_block, double_replica=args.double_replica)
         elif chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
                                   sync=args.chain_sync, block=args.chain_block,
@@ -559,8 +562,9 @@ def bench_multi(args, mname, N, cb):
                     g[w].copy_(host_g[w], non_blocking=True)
             ev_in[k].record(s_in)
             stream.wait_event(ev_in[k])
-            if k >= 1:
-                stream.wait_event(ev_out[k - 1])        # previous pulls have read w
+            lag = 2 if getattr(sh, "double_replica", False) else 1
+            if k >= lag:                                # the pulls that read the replica
+                stream.wait_event(ev_out[k - lag])      # slot this round overwrites
             sh.exchange(slot)
             ev_x[k].record(stream)
             s_out.wait_event(ev_x[k])

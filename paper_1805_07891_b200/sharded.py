@@ -658,7 +658,7 @@ class HierPHub:
 
     def __init__(self, key_sizes, workers_per_rack=8, chunk_size_bytes=32768, lr=0.1,
                  momentum=0.9, device=None, group=None, block=32768, nslots=2,
-                 worker_order=False):
+                 worker_order=False, double_replica=False):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -690,9 +690,15 @@ class HierPHub:
         nblk = max(1, -(-L // self.block))
         self._flags = capi.phub_alloc_shared(dev, 4 * nblk * world)
         torch.as_tensor(_CudaArray(self._flags, nblk * world, self), device=f"cuda:{dev}").zero_()
+        # double_replica: a second replica buffer; round k stores w' into slot k % 2
+        # (slot 0 = the context's w), so a pull of round k may overlap round k+1
+        self.double_replica = bool(double_replica)
+        self._r1 = capi.phub_alloc_shared(dev, 4 * Ep) if self.double_replica else None
+        self._r1_t = (torch.as_tensor(_CudaArray(self._r1, Ep, self), device=f"cuda:{dev}")
+                      if self._r1 else None)
         h = capi.phub_ipc_get_handle
         mine = (rank, b, e, h(dev, self._inbox), h(dev, self._flags),
-                h(dev, self.hub.weights_ptr()))
+                h(dev, self.hub.weights_ptr()), h(dev, self._r1) if self._r1 else None)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         allh.sort(key=lambda x: x[0])
@@ -700,16 +706,19 @@ class HierPHub:
         self.inbox = [[0] * world for _ in range(2)]
         self.peer_inbox = [[0] * world for _ in range(2)]
         self.peer_flags = [0] * world
-        reps = []
+        reps, reps1 = [], []
         err = None
         try:
-            for o, ob, oe, ih, fh, wh in allh:
+            for o, ob, oe, ih, fh, wh, r1h in allh:
                 if o == rank:
                     continue
                 for hd in (ih, fh, wh):
                     self._opened.append(capi.phub_ipc_open(dev, hd))
                 pin, pfl, pw = self._opened[-3:]
                 reps.append(pw)
+                if r1h is not None:
+                    self._opened.append(capi.phub_ipc_open(dev, r1h))
+                    reps1.append(self._opened[-1])
                 self.peer_flags[o] = pfl
                 for sl in range(2):
                     # padded-based: ptr + 4x addresses element x of o's range in o's slot for us
@@ -719,6 +728,9 @@ class HierPHub:
             capi.phub_set_replicas(self.hub.ctx, reps)
         except capi.PhubError as ex:
             err = ex
+        # slot 1 replicas: the peers' second buffers plus this rank's own (its
+        # owned range; slot 0's own copy is the context's w, always written)
+        self._reps = (reps, reps1 + ([self._r1] if self._r1 else []))
         # every rank must agree before anyone relies on peer mappings
         ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=f"cuda:{dev}")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
@@ -729,15 +741,22 @@ class HierPHub:
                 except capi.PhubError:
                     pass
             self._grads = {}
-            for p_ in list(self._own.values()) + [self._inbox, self._flags]:
+            self._r1_t = None
+            for p_ in list(self._own.values()) + [self._inbox, self._flags] + \
+                    ([self._r1] if self._r1 else []):
                 capi.phub_free_shared(dev, p_)
             self.hub.close()
             raise PeerMappingError(f"peer mapping failed on some rank ({err or 'other rank'})")
         self.epoch = 0
         self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
-        self.replica = self.hub.weights()
+        self._w0 = self.hub.weights()
         torch.cuda.synchronize(dev)
         dist.barrier(group=group)
+
+    @property
+    def replica(self):
+        """This rank's full replica of the weights of the latest round."""
+        return self._r1_t if self.double_replica and self.epoch % 2 == 1 else self._w0
 
     @property
     def num_workers(self):
@@ -774,6 +793,8 @@ class HierPHub:
             self.hub.push(k, self._own[(slot, k)], mode="borrow", n=Ep)
         self.epoch += 1
         par = self.epoch % 2
+        if self.double_replica:
+            capi.phub_set_replicas(self.hub.ctx, self._reps[par])
         capi.phub_hier_exchange(self.hub.ctx, self.R, self.block, self.inbox[par],
                                 self.peer_inbox[par], self._flags, self.peer_flags, self.epoch,
                                 self.hub._stream(None), worker_order=self.worker_order)
@@ -795,8 +816,11 @@ class HierPHub:
             capi.phub_ipc_close(self.device, p)
         dist.barrier(group=self.group)
         self._grads = {}
+        self._r1_t = None
         for p in self._own.values():
             capi.phub_free_shared(self.device, p)
+        if self._r1:
+            capi.phub_free_shared(self.device, self._r1)
         capi.phub_free_shared(self.device, self._inbox)
         capi.phub_free_shared(self.device, self._flags)
         self._own = {}
@@ -815,7 +839,7 @@ class PushShardedPHub(HierPHub):
     P2PShardedPHub (gradients() keyed by global worker id)."""
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, block=12288, nslots=2):
+                 device=None, group=None, block=12288, nslots=2, double_replica=False):
         import torch.distributed as dist
         world = dist.get_world_size(group)
         if num_workers % world:
@@ -823,7 +847,7 @@ class PushShardedPHub(HierPHub):
         super().__init__(key_sizes, workers_per_rack=num_workers // world,
                          chunk_size_bytes=chunk_size_bytes, lr=lr, momentum=momentum,
                          device=device, group=group, block=block, nslots=nslots,
-                         worker_order=True)
+                         worker_order=True, double_replica=double_replica)
         self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, self.rack, world)
 
     @property

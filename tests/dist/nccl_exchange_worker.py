@@ -44,12 +44,13 @@ def main():
                               pull=mode == "chain_pull", per_warp=mode == "chain_warp",
                               oneshot=mode == "chain_oneshot",
                               window=3 if mode == "chain_window" else 0)
-    elif mode == "push":
-        sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048)
+    elif mode in ("push", "push_dr"):
+        sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048,
+                             double_replica=mode == "push_dr")
     else:
         cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
         sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
-    fused = mode in ("p2p", "push") or mode.startswith("chain")
+    fused = mode in ("p2p", "push", "push_dr") or mode.startswith("chain")
     w_ref, v_ref = values_np(1, 0, E, 20), values_np(2, 0, E, 25)
     sh.hub.load_state(w_ref, v_ref)
     idx = torch.as_tensor(sh.hub.padded_index(), device=dev)
@@ -69,7 +70,7 @@ def main():
     torch.cuda.synchronize()
     got = sh.weights()[idx].cpu().numpy()
     ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
-    if (mode.startswith("chain") or mode == "push") and sh.sync_timeouts() != 0:
+    if (mode.startswith("chain") or mode.startswith("push")) and sh.sync_timeouts() != 0:
         ok = False
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))
     flag = torch.tensor([0 if ok else 1], device=dev)

@@ -24,7 +24,8 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("mode", ["nccl", "p2p", "push", "chain", "chain_pull", "chain_window",
+@pytest.mark.parametrize("mode", ["nccl", "p2p", "push", "push_dr", "chain", "chain_pull",
+                                  "chain_window",
                                   "chain_warp", "chain_oneshot", "chain_flags", "chain_barrier"])
 @pytest.mark.parametrize("G,name,N,cb,rounds", [
     (2, "small", 8, 32768, 2), (2, "tiny", 4, 4096, 1), (4, "resnet50", 8, 32768, 2),
