@@ -52,15 +52,17 @@ def parse():
     ap.add_argument("--e2e-streams", type=int, default=1,
                     help="copy streams per direction in the 1-GPU e2e measurement")
     ap.add_argument("--grid", type=int, default=0, help="CTAs for the flat kernel (0 = auto)")
-    ap.add_argument("--seg", type=int, default=-1, help="flat kernel CTA segment (vectors)")
-    ap.add_argument("--minb", type=int, default=0, help="flat kernel resident-CTA build")
     ap.add_argument("--tile-elems", type=int, default=0, help="chunk-tile kernel tile size")
     ap.add_argument("--oneshot", type=int, default=-1, help="flat kernel one-vector-per-thread grid")
     ap.add_argument("--graph", action="store_true",
                     help="also time the round replayed from a captured CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-rounds", type=int, default=3,
+                    help="full-model oracle rounds per thread count (median reported)")
+    ap.add_argument("--cache-table", action="store_true",
+                    help="N=1: also time the caching table of P:913-935 on B200 (fused kernel "
+                         "with w' evict-last vs all evict-first, alone and followed by the pull)")
     ap.add_argument("--owner-policy", default="contig", choices=["contig"])
     ap.add_argument("--pieces", type=int, default=8, help="chain mode pipeline pieces")
     ap.add_argument("--chain-sync", default="blocks", choices=["blocks", "flags", "barrier"])
@@ -68,21 +70,8 @@ def parse():
                     help="chain mode: elements per block flag (sync=blocks; 0 = by model size)")
     ap.add_argument("--hier-block", type=int, default=32768,
                     help="hier mode: elements per block flag")
-    ap.add_argument("--double-replica", action="store_true",
-                    help="push/hier: alternate two replica buffers per round, so a round's "
-                         "pull may overlap the next exchange (e2e)")
     ap.add_argument("--push-block", type=int, default=12288,
                     help="push mode: elements per block flag")
-    ap.add_argument("--chain-pull", action="store_true",
-                    help="chain mode: next rank reads the partial over NVLink (default: pushed)")
-    ap.add_argument("--chain-oneshot", action="store_true",
-                    help="chain mode: last rank's fused launch is one CTA per 2048 elements")
-    ap.add_argument("--chain-per-warp", action="store_true",
-                    help="chain mode: warps (not CTAs) take and signal blocks")
-    ap.add_argument("--chain-window", type=int, default=0,
-                    help="chain mode: producer back-pressure window in blocks (0 = off)")
-    ap.add_argument("--chain-no-consume", action="store_true",
-                    help="chain mode: push the incoming partial as BORROW, not CONSUME")
     ap.add_argument("--chain-producer-grid", type=int, default=0,
                     help="chain mode: CTAs of the partial-sum launch on non-last ranks")
     ap.add_argument("--chain-consumer-grid", type=int, default=0,
@@ -190,101 +179,169 @@ def measured_peaks():
 
 
 def ncu_traffic(config, kernel):
-    """dram bytes per launch of the hot kernel from the committed ncu summary."""
+    """(dram bytes per launch, source) of the hot kernel from the committed ncu
+    summary -- an `ncu --set full` capture of an earlier run, NOT measured in
+    this run (ncu cannot run inside a timed bench)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return None, None
     with open(p) as f:
         d = json.load(f)
     ent = d.get(f"{config}:{kernel}") or d.get(config)
-    return ent.get("dram_bytes_per_launch") if ent else None
+    if not ent:
+        return None, None
+    return ent.get("dram_bytes_per_launch"), (
+        f"committed ncu --set full capture ({ent.get('source', 'profiles/ncu_traffic.json')}), "
+        "dram__bytes_read.sum + dram__bytes_write.sum per launch; not measured in this run")
 
 
 # -------------------------------------------------------------- CPU oracle
 _CPU_INPUTS = {}
 
 
-def cpu_oracle_sample(config_name, workers, chunk_bytes, seconds, nthreads=None):
-    """Time the CPU oracle (as it stands) on a bounded prefix of the workload."""
-    import numpy as np
-    import oracle
-    from workloads import grad_stream, manifest, values_np
-    sizes_full = manifest(config_name)
-    budget = 1 << 23                   # 8 Mi elements per worker: 32 MiB, x workers
-    sizes, tot = [], 0
-    for n in sizes_full:
-        take = min(n, budget - tot)
-        if take <= 0:
-            break
-        sizes.append(take)
-        tot += take
-    E = sum(sizes)
-    key = (config_name, workers, E)
+def cpu_inputs(config_name, workers):
+    """Host arrays of the FULL workload: the same counter-based streams the GPU
+    arm generates (workloads.generate; torch CPU ops, all host threads)."""
+    import torch
+    from workloads import grad_stream, manifest
+    from workloads.generate import values_torch
+    key = (config_name, workers)
     if key not in _CPU_INPUTS:
         _CPU_INPUTS.clear()
-        _CPU_INPUTS[key] = ([values_np(grad_stream(w), 0, E, 25) for w in range(workers)],
-                            values_np(1, 0, E, 20), values_np(2, 0, E, 25))
-    grads, w0, v0 = _CPU_INPUTS[key]
-    cores = len(os.sched_getaffinity(0))
-    nt = nthreads or cores
-    times = []
-    t_end = time.perf_counter() + seconds
-    while time.perf_counter() < t_end or len(times) < 2:
-        t0 = time.perf_counter()
-        oracle.round_(sizes, grads, w0, v0, 0.1, 0.9, chunk_bytes=chunk_bytes, keep_agg=False,
-                      nthreads=nt)
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    gbs = workers * 4 * E / t / 1e9
-    cpu_model = ""
+        sizes = manifest(config_name)
+        E = sum(sizes)
+        torch.set_num_threads(len(os.sched_getaffinity(0)))
+        grads = [values_torch(grad_stream(w), 0, E, 25, "cpu").numpy() for w in range(workers)]
+        _CPU_INPUTS[key] = (sizes, grads, values_torch(1, 0, E, 20, "cpu").numpy(),
+                            values_torch(2, 0, E, 25, "cpu").numpy())
+    return _CPU_INPUTS[key]
+
+
+def host_cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
             for line in f:
                 if line.startswith("model name"):
-                    cpu_model = line.split(":", 1)[1].strip()
-                    break
+                    return line.split(":", 1)[1].strip()
     except OSError:
         pass
-    return {"value": round(gbs, 3), "unit": "GB/s", "cores": nt, "kind": "oracle",
-            "sample": f"{config_name} key-prefix of {E} elements ({len(sizes)} keys), "
-                      f"{workers} workers, {chunk_bytes} B chunks, OpenMP static over vkeys "
-                      f"({nt} threads, PHub chunk->core layout); median of {len(times)} rounds",
-            "host_cpu": cpu_model, "host_cores_available": cores,
-            "exchanges_per_s_full_model": round(workers / (t * sum(sizes_full) / E), 3),
-            "_round_s": t, "_E": E}
+    return ""
+
+
+def cpu_oracle_rounds(config_name, workers, chunk_bytes, rounds, nthreads=None):
+    """The CPU oracle, as it stands, on `rounds` FULL rounds of the workload
+    (every key, every worker, no sampling); returns the per-round seconds."""
+    import oracle
+    sizes, grads, w0, v0 = cpu_inputs(config_name, workers)
+    nt = nthreads or len(os.sched_getaffinity(0))
+    times = []
+    for _ in range(rounds):
+        t0 = time.perf_counter()
+        oracle.round_(sizes, grads, w0, v0, 0.1, 0.9, chunk_bytes=chunk_bytes, keep_agg=False,
+                      nthreads=nt)
+        times.append(time.perf_counter() - t0)
+    return times, nt
+
+
+def cpu_baseline(config_name, workers, chunk_bytes, rounds):
+    """SURVEY 8(d) "Oracle timing": median of `rounds` full rounds on all host
+    cores (OpenMP static over vkeys: PHub's chunk -> core layout), and
+    the same on one thread."""
+    from workloads import manifest
+    E = sum(manifest(config_name))
+    t_all, nt = cpu_oracle_rounds(config_name, workers, chunk_bytes, rounds)
+    t_one, _ = cpu_oracle_rounds(config_name, workers, chunk_bytes, rounds, nthreads=1)
+    m_all, m_one = statistics.median(t_all), statistics.median(t_one)
+    return {"value": round(workers * 4 * E / m_all / 1e9, 3), "unit": "GB/s", "cores": nt,
+            "kind": "oracle",
+            "sample": f"full {config_name} round ({E} elements x {workers} workers, every key, no "
+                      f"sampling), {chunk_bytes} B chunks, OpenMP static over vkeys ({nt} threads, "
+                      f"PHub chunk->core layout); median of {len(t_all)} rounds",
+            "ms_per_round": round(m_all * 1e3, 2), "exchanges_per_s": round(workers / m_all, 3),
+            "host_cpu": host_cpu_model(), "host_cores_available": len(os.sched_getaffinity(0)),
+            "single_thread": {"value": round(workers * 4 * E / m_one / 1e9, 3), "unit": "GB/s",
+                              "cores": 1, "ms_per_round": round(m_one * 1e3, 2),
+                              "rounds": len(t_one)}}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only); every
+    warm-up and timed step is one FULL round of the workload on all host cores."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from workloads.manifests import CONFIGS
+    from workloads import manifest
     mname, N, cb = CONFIGS[args.config]
     N = args.workers or N
     cb = args.chunk_bytes or cb
-    from workloads import manifest
-    E_full = sum(manifest(mname))
-    per_step = max(args.cpu_seconds / max(args.steps + args.warmup, 1), 0.05)
-    res = [cpu_oracle_sample(mname, N, cb, per_step) for _ in range(args.warmup)]
-    res = [cpu_oracle_sample(mname, N, cb, per_step) for _ in range(args.steps)]
-    t_round = statistics.median(r["_round_s"] for r in res) * E_full / res[0]["_E"]
-    value = N * 4 * E_full / t_round / 1e9
-    base = {k: v for k, v in res[0].items() if not k.startswith("_")}
-    base["value"] = round(value, 3)
+    E = sum(manifest(mname))
+    cpu_oracle_rounds(mname, N, cb, args.warmup)
+    times, nt = cpu_oracle_rounds(mname, N, cb, args.steps)
+    t_round = statistics.median(times)
+    value = N * 4 * E / t_round / 1e9
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t_round * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": round(value / PAPER_GBS, 4), "dtype": "f32",
         "data": "synthetic", "exchanges_per_s": round(N / t_round, 3),
-        "config": {"workload": args.config, "workers": N, "chunk_bytes": cb,
-                   "note": "each step times the oracle on a bounded key-prefix sample and "
-                           "scales the round time to the full model"},
-        "cpu_baseline": base,
+        "config": {"workload": args.config, "keys": len(manifest(mname)), "E": E, "workers": N,
+                   "chunk_bytes": cb, "timing": "median over the timed steps; one step = one "
+                                                 "full round (no sampling, no extrapolation)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": nt, "kind": "oracle",
+                         "sample": f"full {mname} round every step ({E} elements x {N} workers)",
+                         "host_cpu": host_cpu_model()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))
+
+
+def pcie_probe(dev, mib=1024, reps=5):
+    """Same-run PCIe ceiling for the e2e numbers: pinned host <-> device copies
+    of `mib` MiB (H2D alone, D2H alone, both at once on two streams), best of
+    `reps` (CUDA events)."""
+    import torch
+    n = mib * (1 << 20) // 4
+    h_in = torch.ones(n, pin_memory=True)
+    h_out = torch.empty(n, pin_memory=True)
+    d_in = torch.empty(n, device=dev)
+    d_out = torch.ones(n, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    cur = torch.cuda.current_stream(dev)
+
+    def timed(fn):
+        best = float("inf")
+        for _ in range(reps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            a.record(cur)
+            fn()
+            b.record(cur)
+            torch.cuda.synchronize(dev)
+            best = min(best, a.elapsed_time(b) / 1e3)
+        return best
+
+    def both():
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
+    th = timed(lambda: d_in.copy_(h_in, non_blocking=True))
+    td = timed(lambda: h_out.copy_(d_out, non_blocking=True))
+    tb = timed(both)
+    nb = 4 * n
+    out = {"h2d_gbs": round(nb / th / 1e9, 2), "d2h_gbs": round(nb / td / 1e9, 2),
+           "bidir_gbs_per_direction": round(nb / tb / 1e9, 2), "bytes": nb,
+           "how": f"pinned {mib} MiB copies, best of {reps}, CUDA events"}
+    del h_in, h_out, d_in, d_out
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------------ ours
@@ -337,6 +394,26 @@ def nccl_allgather_busbw(dev, G, mib=256, reps=5):
     del src, dst
     torch.cuda.empty_cache()
     return round((G - 1) / G * 4 * n * G / best / 1e9, 1)
+
+
+def hier_model(P, R, b_nvlink, b_hbm):
+    """The paper's benefit model for hierarchical reduction (P:760-763,
+    phub_hier_beneficial) evaluated with this box's measured rates: a rack's
+    PBox is a GPU whose network port is its NVLink (B_PBox = same-run NCCL
+    all-gather bus bandwidth), its P workers' gradients stream from its HBM
+    (B_Wkr = measured HBM copy rate / P), and the NVSwitch core is
+    non-blocking (B_Core = R x B_PBox).  Reported next to the measured rounds;
+    DESIGN.md R18 discusses the mapping."""
+    from paper_1805_07891_b200 import capi
+    bw = {"b_pbox": float(b_nvlink), "b_wkr": float(b_hbm) / P, "b_core": R * float(b_nvlink)}
+    out = {"workers_per_rack": P, "racks": R, **{k: round(v, 1) for k, v in bw.items()},
+           "unit": "GB/s"}
+    for mode, name in ((capi.PHUB_CROSS_RACK_SHARDED, "sharded"),
+                       (capi.PHUB_CROSS_RACK_RING, "ring")):
+        ben, lhs, rhs = capi.phub_hier_beneficial(P, R, bw["b_pbox"], bw["b_wkr"], bw["b_core"],
+                                                  mode)
+        out[name] = {"beneficial": ben, "lhs": lhs, "rhs": rhs}
+    return out
 
 
 def owner_phase_ms(sizes, N, cb, rank, G, steps, warmup, dev):
@@ -404,16 +481,13 @@ def bench_multi(args, mname, N, cb):
     try:
         if hier:
             sh = HierPHub(sizes, workers_per_rack=N, chunk_size_bytes=cb, device=local,
-                          block=args.hier_block, double_replica=args.double_replica)
+                          block=args.hier_block)
         elif push:
             sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local,
-                                 block=args.push_block, double_replica=args.double_replica)
+                                 block=args.push_block)
         elif chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
-                                  sync=args.chain_sync, block=args.chain_block,
-                                  pull=args.chain_pull, consume=not args.chain_no_consume,
-                                  window=args.chain_window, per_warp=args.chain_per_warp,
-                                  oneshot=args.chain_oneshot)
+                                  sync=args.chain_sync, block=args.chain_block)
             from paper_1805_07891_b200 import capi as _c
             if args.chain_producer_grid and not sh.last:
                 sh.hub.set_option(_c.PHUB_OPT_GRID, args.chain_producer_grid)
@@ -433,10 +507,6 @@ def bench_multi(args, mname, N, cb):
     from paper_1805_07891_b200 import capi
     if args.grid:
         hub.set_option(capi.PHUB_OPT_GRID, args.grid)
-    if args.seg >= 0:
-        hub.set_option(capi.PHUB_OPT_FLAT_SEG, args.seg)
-    if args.minb:
-        hub.set_option(capi.PHUB_OPT_FLAT_MINB, args.minb)
     if args.oneshot >= 0:
         hub.set_option(capi.PHUB_OPT_FLAT_ONESHOT, args.oneshot)
     if args.tile_elems:
@@ -509,8 +579,8 @@ def bench_multi(args, mname, N, cb):
     dist.barrier()
     clocks.stop()
     launches = hub.kernel_launches - k0
-    if chain and sh.sync_timeouts():
-        raise RuntimeError("chained exchange: device-side waits timed out")
+    if chain:
+        sh.check()               # collective: raises on every rank if any device wait expired
     mine = {"rank": rank, "ms": t0.elapsed_time(t1) / args.steps,
             "k_ms": sum(a.elapsed_time(b) for a, b in ev) / args.steps,
             "owned": hub.owned_elements(), "launches": launches, "clocks": clocks.summary()}
@@ -562,9 +632,8 @@ def bench_multi(args, mname, N, cb):
                     g[w].copy_(host_g[w], non_blocking=True)
             ev_in[k].record(s_in)
             stream.wait_event(ev_in[k])
-            lag = 2 if getattr(sh, "double_replica", False) else 1
-            if k >= lag:                                # the pulls that read the replica
-                stream.wait_event(ev_out[k - lag])      # slot this round overwrites
+            if k >= 1:                                  # the pulls that read the replica
+                stream.wait_event(ev_out[k - 1])        # this round overwrites
             sh.exchange(slot)
             ev_x[k].record(stream)
             s_out.wait_event(ev_x[k])
@@ -589,9 +658,20 @@ def bench_multi(args, mname, N, cb):
         t = torch.tensor([a.elapsed_time(b) / args.e2e_steps], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item()) / 1e3
+        if p2p:
+            sh.check()
+        del host_g, host_o
+        probe = pcie_probe(dev)
+        pr = [None] * G
+        dist.all_gather_object(pr, probe)
+        slowest = min(pr, key=lambda x: x["bidir_gbs_per_direction"])
+        per_gpu_dir = len(sh.hosted) * 4 * Ep / te / 1e9
         e2e = {"value": round(NT * 4 * E / te / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": NT * 4 * Ep, "d2h_bytes_per_step": NT * 4 * Ep,
                "steps": args.e2e_steps, "ms_per_step": round(te * 1e3, 3),
+               "pcie_probe_slowest_rank": slowest,
+               "gbs_per_direction_per_gpu": round(per_gpu_dir, 2),
+               "frac_of_pcie_bidir": round(per_gpu_dir / slowest["bidir_gbs_per_direction"], 4),
                "path": f"{type(sh).__name__}: H2D of hosted grads -> exchange ({args.mode}) -> "
                        f"D2H of the replica per hosted worker" +
                        (" ; rounds pipelined (2 gradient slots, H2D of k+1 || D2H of k)"
@@ -632,8 +712,8 @@ def bench_multi(args, mname, N, cb):
                                (f"M3 (full exchange) chain: rank-ordered partial sums over "
                                 f"NVLink, last rank fused Nesterov + replica stores, " +
                                 (f"one launch per rank streamed by per-block device flags "
-                                 f"({sh.block} elements/block, partial "
-                                 f"{'pulled' if args.chain_pull else 'pushed'})"
+                                 f"({sh.block} elements/block, partial stored into the next "
+                                 f"rank's inbox)"
                                  if args.chain_sync == "blocks" else
                                  f"pipelined over {args.pieces} pieces ({args.chain_sync} sync)"))
                                if chain else
@@ -646,7 +726,7 @@ def bench_multi(args, mname, N, cb):
                                ("M3 (full exchange) nccl: NCCL grouped send/recv push, fused "
                                 "kernel on owner range, NCCL all-gather-v pull"),
                        "parallelism": f"owner-sharded x{G}", "kernel": args.kernel,
-                       "seg": args.seg, "minb": args.minb, "grid": args.grid,
+                       "grid": args.grid,
                        "l2": "no flush: inputs exceed L2"},
             "owner_phase": None if ar else {
                 "mode": "M2 (SURVEY 8(d)): owner kernel alone, the N workers' slices of its "
@@ -673,7 +753,8 @@ def bench_multi(args, mname, N, cb):
                                          "direction"} if p2p else
                          {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                           "unit": "GB/s", "frac": round(achieved / peak, 4),
-                          "traffic": ncu_traffic(args.config, "flat"),
+                          "traffic": ncu_traffic(args.config, "flat")[0],
+                          "traffic_source": ncu_traffic(args.config, "flat")[1],
                           "kernel": "phub_agg_nag (k_flat) on the slowest owner",
                           "kernel_ms": round(slow["k_ms"], 4), "peak_source": peak_src}),
             "roofline_nvlink": {"bound": "nvlink", "achieved": round(nv_ach, 1),
@@ -688,6 +769,8 @@ def bench_multi(args, mname, N, cb):
             "clocks": {"sm_mhz": statistics.median(sm) if sm else None,
                        "sm_max_mhz": allr[0]["clocks"].get("sm_max_mhz"), "reasons": reasons},
             "gpu_launches": sum(r["launches"] for r in allr),
+            "hier_model": hier_model(N, G, ag_busbw, measured_peaks()[0])
+            if hier and G > 1 and ag_busbw else None,
             "e2e": e2e,
             "cpu_baseline": None,
         }
@@ -718,10 +801,6 @@ def bench_single(args, mname, N, cb):
                    else capi.PHUB_CACHE_ENABLED)
     if args.grid:
         hub.set_option(capi.PHUB_OPT_GRID, args.grid)
-    if args.seg >= 0:
-        hub.set_option(capi.PHUB_OPT_FLAT_SEG, args.seg)
-    if args.minb:
-        hub.set_option(capi.PHUB_OPT_FLAT_MINB, args.minb)
     if args.tile_elems:
         hub.set_option(capi.PHUB_OPT_TILE_ELEMS, args.tile_elems)
     if args.oneshot >= 0:
@@ -785,13 +864,11 @@ def bench_single(args, mname, N, cb):
     if not args.no_e2e:
         e2e = bench_e2e(hub, grads, N, E, Ep, stream, args.e2e_steps, args.e2e_streams)
 
+    cache_table = bench_cache_table(hub, grads, N, E, stream, args) if args.cache_table else None
+
     cpu = None
-    if not args.no_cpu:
-        cpu = cpu_oracle_sample(mname, N, cb, args.cpu_seconds)
-        cpu = {k: v for k, v in cpu.items() if not k.startswith("_")}
-        # the oracle is timed both on all host cores and on one
-        one = cpu_oracle_sample(mname, N, cb, min(3.0, args.cpu_seconds), nthreads=1)
-        cpu["single_thread"] = {"value": one["value"], "unit": "GB/s", "cores": 1}
+    if not args.no_cpu:      # full rounds on all host cores and on one
+        cpu = cpu_baseline(mname, N, cb, args.cpu_rounds)
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
@@ -800,8 +877,7 @@ def bench_single(args, mname, N, cb):
         "vs_baseline": round(value / PAPER_GBS, 2), "dtype": "f32", "data": "synthetic",
         "exchanges_per_s": round(N / t_step, 1),
         "config": {"workload": args.config, "keys": len(sizes), "E": E, "E_padded": Ep,
-                   "workers": N, "chunk_bytes": cb, "seg": args.seg, "minb": args.minb,
-                   "grid": args.grid, "tile_elems": args.tile_elems, "oneshot": args.oneshot,
+                   "workers": N, "chunk_bytes": cb, "grid": args.grid, "tile_elems": args.tile_elems, "oneshot": args.oneshot,
                    "mode": "M1 (1 GPU, pushes resident, "
                    "zero-copy BORROW)", "kernel": kname, "cache": args.cache,
                    "l2": f"no flush: inputs exceed L2 ({(4 * N + 16) * E / 1e9:.2f} GB/round "
@@ -811,7 +887,8 @@ def bench_single(args, mname, N, cb):
                                         "8 workers; BASELINE.md), other hardware: context"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": ncu_traffic(args.config, kname),
+                     "traffic": ncu_traffic(args.config, kname)[0],
+                     "traffic_source": ncu_traffic(args.config, kname)[1],
                      "kernel": "phub_agg_nag (k_flat)", "kernel_ms": round(k_ms_mean, 4),
                      "kernel_ms_min": round(min(k_ms), 4),
                      "kernel_ms_median": round(statistics.median(k_ms), 4),
@@ -823,6 +900,7 @@ def bench_single(args, mname, N, cb):
         "clocks": clocks.summary(),
         "gpu_launches": launches,
         "graph": graph,
+        "cache_table": cache_table,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
@@ -858,6 +936,56 @@ def bench_graph(hub, grads, N, E, stream, steps, rounds_per_graph=20):
     t = a.elapsed_time(b) / 1e3 / (reps * rounds_per_graph)
     return {"us_per_round": round(t * 1e6, 3), "value": round(N * 4 * E / t / 1e9, 2),
             "unit": "GB/s", "rounds_per_graph": rounds_per_graph, "replays": reps}
+
+
+def bench_cache_table(hub, grads, N, E, stream, args, reps=20):
+    """The caching table of P:913-935 (S 5, "Caching Effectiveness") on B200: the
+    fused aggregate + Nesterov kernel with the cache-enabled policy (w' stored
+    L2 evict-last so the pull that follows reads it from L2) vs all
+    streams evict-first (the cache-bypass analog), each timed alone and followed
+    by the pull of the whole model (phub_pull ALL_KEYS into a device buffer),
+    plus the pull alone ("Opt/Agg Off").  Mean ms over `reps` (CUDA events on
+    the launching stream); DRAM bytes come from the committed ncu capture."""
+    import torch
+    from paper_1805_07891_b200 import capi
+    dst = torch.empty(hub.E_padded, dtype=torch.float32, device=grads[0].device)
+    batch = [(w, capi.PHUB_ALL_KEYS, grads[w]) for w in range(N)]
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    def agg():
+        hub.push_batch(batch)
+        hub.aggregate_optimize()
+
+    def pull():
+        hub.pull(dst)
+
+    def agg_pull():
+        agg()
+        pull()
+
+    rows = {"pull_only_ms": timed(pull)}
+    for mode, val in (("cached", capi.PHUB_CACHE_ENABLED), ("bypass", capi.PHUB_CACHE_BYPASS)):
+        hub.set_option(capi.PHUB_OPT_CACHE, val)
+        rows[f"{mode}_kernel_ms"] = timed(agg)
+        rows[f"{mode}_kernel_pull_ms"] = timed(agg_pull)
+    hub.set_option(capi.PHUB_OPT_CACHE, capi.PHUB_CACHE_ENABLED)
+    out = {k: round(v, 4) for k, v in rows.items()}
+    for mode in ("cached", "bypass"):
+        out[f"{mode}_exchanges_per_s"] = round(N / (rows[f"{mode}_kernel_pull_ms"] / 1e3), 1)
+    out["how"] = ("mean of %d rounds each; pull = phub_pull(ALL_KEYS) D2D of the padded model "
+                  "(cudaMemcpyAsync: %.0f MB read + written)" % (reps, 4 * hub.E_padded / 1e6))
+    return out
 
 
 def bench_e2e(hub, grads, N, E, Ep, stream, steps, nstreams=1):
@@ -925,9 +1053,13 @@ def bench_e2e(hub, grads, N, E, Ep, stream, steps, nstreams=1):
     torch.cuda.synchronize()
     t = t0.elapsed_time(t1) / 1e3 / steps
     del host_g, host_w
+    probe = pcie_probe(grads[0].device)
+    per_dir = N * 4 * Ep / t / 1e9
     return {"value": round(N * 4 * E / t / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": N * 4 * Ep, "d2h_bytes_per_step": N * 4 * Ep,
             "steps": steps, "ms_per_step": round(t * 1e3, 3),
+            "pcie_probe": probe, "gbs_per_direction": round(per_dir, 2),
+            "frac_of_pcie_bidir": round(per_dir / probe["bidir_gbs_per_direction"], 4),
             "path": f"phub_push(PHUB_COPY, pinned host) x N -> phub_aggregate_optimize -> "
                     f"phub_pull(host) x N; rounds pipelined (H2D of k+1 || D2H of k), copies "
                     f"on {K} stream(s) per direction"}

@@ -9,7 +9,7 @@
  * process) shard the chunks by owner.
  *
  * Citations: P:n = PAPER.md line n (canonical copy P:377-1120), S:n = SPEC.md
- * line n.  DESIGN.md lists every reading of the paper used here (R1..R16).
+ * line n.  DESIGN.md lists every reading of the paper used here (R1..R18).
  *
  *   problem statement ........ P:634-638 (InitService allocates receive and
  *                               merge buffers; Push / Pull / PushPull)
@@ -27,6 +27,14 @@
  *   - A CUDA runtime error makes the context sticky-failed: the failing call
  *     and every later call (except the introspection/destroy calls) return
  *     PHUB_ERR_CUDA.
+ *   - Device-side flag waits (phub_sync, phub_hier_exchange) are bounded
+ *     (~2 s).  A launch whose wait expires skips that work and raises a
+ *     host-mapped error word; the context then becomes sticky-failed with
+ *     PHUB_ERR_SYNC_TIMEOUT, reported by the first call that starts after the
+ *     expiry -- like an asynchronous CUDA error.  Every synchronizing call
+ *     (phub_synchronize, phub_read_state, phub_load_state) reports it for all
+ *     work enqueued before it, so a partly skipped round is never returned as
+ *     PHUB_OK by a call that waited for it.
  *   - `stream` arguments are a cudaStream_t passed as void* (NULL = legacy
  *     default stream).  Work is enqueued on it; validation is synchronous on
  *     the host before anything is enqueued.
@@ -64,13 +72,14 @@ typedef enum {
     PHUB_ERR_INCOMPLETE = 9,         /* aggregate before all N x K pushes arrived   */
     PHUB_ERR_CUDA = 10,              /* CUDA runtime/launch error; context sticky-failed    */
     PHUB_ERR_OUT_OF_MEMORY = 11,     /* device allocation failed                            */
-    PHUB_ERR_UNSUPPORTED = 12        /* option/variant not available for this context       */
+    PHUB_ERR_UNSUPPORTED = 12,       /* option/variant not available for this context       */
+    PHUB_ERR_SYNC_TIMEOUT = 13       /* a device-side flag wait expired; sticky              */
 } phub_status;
 
 #define PHUB_ALL_KEYS (-1)            /* whole-model push/pull in the padded layout        */
 #define PHUB_OWNED_RANGE (-2)         /* push of exactly this context's owned padded range  */
 
-enum { PHUB_COPY = 0, PHUB_BORROW = 1, PHUB_CONSUME = 2 };   /* ownership mode of a pushed buffer */
+enum { PHUB_COPY = 0, PHUB_BORROW = 1 };          /* ownership mode of a pushed buffer   */
 enum { PHUB_OWNER_LPT = 0, PHUB_OWNER_CONTIG = 1 };  /* chunk -> owner policy    */
 
 /* One virtual key: chunk `vkey_id` of key `key_id` covers elements
@@ -129,15 +138,6 @@ phub_status phub_destroy(phub_ctx ctx);
  *     the next phub_aggregate_optimize.  `grad` must be device memory
  *     (this or a peer-mapped GPU), 16-byte aligned.  The caller must keep it
  *     valid and unmodified until that aggregate has completed on its stream.
- *   mode PHUB_CONSUME: as PHUB_BORROW, and the buffer's contents become
- *     UNDEFINED once the aggregate that reads it has run: a block-streaming
- *     kernel (phub_sync.block_elems > 0) may drop the buffer's lines from L2
- *     right after reading them (discard.global.L2) instead of letting them be
- *     written back -- for a transient staging buffer, e.g. a partial sum
- *     another GPU stored over NVLink moments earlier, which then costs the
- *     consumer neither an HBM write nor an HBM read.  Whole-model
- *     (PHUB_ALL_KEYS) pushes of 128-B aligned buffers by workers < 64;
- *     otherwise it behaves exactly as PHUB_BORROW.
  *   mode PHUB_COPY: the data (host or device memory) is copied into the
  *     context's receive arena on `stream`; the caller may reuse `grad` once
  *     the copy has completed on `stream`.  The arena has two slots (iteration
@@ -260,11 +260,13 @@ phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
  * process).  `wait_flag` (nullable) is a uint32 in this GPU's memory that a
  * previous stage raises; every CTA of the launch first waits until
  * *wait_flag >= wait_value (system-scope acquire; bounded: after ~2 s it
- * gives up, counts a timeout -- see phub_sync_timeouts -- and skips its
- * work).  `signal_flag` (nullable, typically peer-mapped) is written with
+ * gives up, skips its work and the context becomes sticky-failed with
+ * PHUB_ERR_SYNC_TIMEOUT -- see the conventions above and phub_sync_timeouts).
+ * `signal_flag` (nullable, typically peer-mapped) is written with
  * `signal_value` (system-scope release) once every CTA of the launch has
- * finished its stores.  At most one signalling (or block-streaming) launch per
- * context in flight.
+ * finished its stores -- and never if any CTA of the launch gave up its wait,
+ * so a downstream stage cannot consume a partly computed partial.  At most one
+ * signalling (or block-streaming) launch per context in flight.
  *
  * Block-streaming form (`block_elems` > 0, a multiple of 2048): the model is
  * cut into blocks b = [b*block_elems, (b+1)*block_elems) of the padded layout
@@ -272,42 +274,16 @@ phub_status phub_kernel_launches(phub_ctx ctx, uint64_t* launches);
  * (ceil(E_padded / block_elems) entries).  One persistent launch walks its
  * range block by block: before reading block b a CTA waits for
  * wait_flag[b] >= wait_value; once block b's stores are performed it raises
- * signal_flag[b] = signal_value.  A downstream stage can then start on block b
- * while this launch still works on later blocks -- the pipelining of PHub's
- * streaming aggregation without one launch per piece.
- *
- * Back-pressure (block form only; all three zero/NULL = off): a producer
- * launch with `credit` != NULL starts block b (the b-th block of its range)
- * only once *credit >= credit_base + b - credit_window (bounded wait); a
- * consumer launch with `credit_return` != NULL adds 1 to *credit_return
- * (typically the producer's peer-mapped counter) after each block it
- * finishes.  The producer then runs at most `credit_window` blocks ahead, so
- * what it stores into the consumer is still in the consumer's L2 when read
- * (with PHUB_CONSUME, dropped from L2 without a write-back).  The counter is
- * monotonic: credit_base = blocks consumed in earlier rounds.  Any window
- * >= 1 is deadlock-free (block b only needs consumer blocks < b - window + 1,
- * whose tickets were taken first); a window below the consumer's resident
- * CTAs serialises the stages.  The two launches must run on different GPUs:
- * a producer waiting on credits from a consumer queued behind it on the same
- * stream would only time out. */
+ * signal_flag[b] = signal_value (a skipped block is never raised).  A
+ * downstream stage can then start on block b while this launch still works on
+ * later blocks -- the pipelining of PHub's streaming aggregation
+ * without one launch per piece.  Flags must be 4-B aligned. */
 typedef struct {
     const uint32_t* wait_flag;
     uint32_t wait_value;
     uint32_t* signal_flag;
     uint32_t signal_value;
     uint64_t block_elems;       /* 0: one flag per launch; > 0: one flag per block */
-    const uint32_t* credit;     /* producer: consumer-progress counter (local)       */
-    uint32_t credit_base;
-    uint32_t credit_window;     /* blocks the producer may run ahead                 */
-    uint32_t* credit_return;    /* consumer: counter to advance per finished block   */
-    int32_t per_warp;           /* block form: 0 = each CTA takes and signals blocks
-                                   (block_elems multiple of 2048); nonzero = each WARP
-                                   does (multiple of 256): small blocks, short pipeline
-                                   fill, a fence stalls one warp instead of the CTA   */
-    int32_t oneshot;            /* block form, phub_aggregate_range without signal /
-                                   credit_return / per_warp only: one CTA per 2048
-                                   elements over the range (the hardware scheduler
-                                   orders them), each waiting for its block's flag   */
 } phub_sync;
 
 /* Chained exchange (workers hosted in rank order): the
@@ -330,8 +306,20 @@ phub_status phub_partial_sum(phub_ctx ctx, const float* const* srcs, int32_t cou
 phub_status phub_aggregate_range(phub_ctx ctx, uint64_t begin, uint64_t end,
                                  const phub_sync* sync, void* stream);
 
-/* Number of phub_sync waits that timed out on this context (synchronous). */
+/* Number of device-side waits (phub_sync, phub_hier_exchange) that expired on
+ * this context (synchronous; reported even when the context is failed --
+ * a nonzero count also makes it sticky-failed with PHUB_ERR_SYNC_TIMEOUT). */
 phub_status phub_sync_timeouts(phub_ctx ctx, uint32_t* count);
+
+/* The context's status now, without synchronizing: PHUB_OK, or the sticky
+ * PHUB_ERR_SYNC_TIMEOUT / PHUB_ERR_CUDA (a wait that expired after this call
+ * shows up in a later one). */
+phub_status phub_check(phub_ctx ctx);
+
+/* Wait for `stream` (NULL: the whole device) and return the context's status:
+ * PHUB_OK, or the sticky PHUB_ERR_SYNC_TIMEOUT / PHUB_ERR_CUDA of any work
+ * waited for. */
+phub_status phub_synchronize(phub_ctx ctx, void* stream);
 
 /* Every later phub_aggregate_optimize also stores w' of the owned range into
  * replicas[0..count) (padded layout, E_padded elements each; device pointers,
@@ -391,6 +379,24 @@ typedef struct {
 } phub_hier;
 phub_status phub_hier_exchange(phub_ctx ctx, const phub_hier* h, void* stream);
 
+/* Hierarchical-reduction benefit model (S 3.4; R18),
+ * host-only, as printed in the paper: with N = workers_per_rack, r = racks,
+ *   B_bn = min((r-1) * B_PBox, B_Core)
+ *   lhs  = max((N-1)/B_bn, 1/(N*B_Wkr))         time of the flat cross-rack step
+ *   rhs  = max(1/B_PBox, N/B_Wkr) + C           local aggregation + cross-rack cost
+ *   C    = (N-1)/(N*B_bn)   PHUB_CROSS_RACK_SHARDED (sharded PSs; this build's
+ *                           k_hier cross-rack step)
+ *        = (r-1)/(r*B_bn)   PHUB_CROSS_RACK_RING (racks in a ring; the paper's
+ *                           emulation)
+ * *beneficial = lhs > rhs.  Bandwidths in any one consistent unit (> 0,
+ * finite); lhs/rhs (nullable) are in its reciprocal (time per model byte).
+ * INVALID_ARGUMENT for N < 1, r < 2 (no cross-rack step), bad bandwidths or
+ * mode.  Needs no device. */
+enum { PHUB_CROSS_RACK_SHARDED = 0, PHUB_CROSS_RACK_RING = 1 };
+phub_status phub_hier_beneficial(int32_t workers_per_rack, int32_t racks, double b_pbox,
+                                 double b_wkr, double b_core, int32_t cross_rack,
+                                 int32_t* beneficial, double* lhs, double* rhs);
+
 /* Shared device allocations that can be exported to peer processes.
  * phub_alloc_shared: cudaMalloc of `bytes` on `device` (whole allocation, so an
  * IPC handle maps exactly this buffer).  phub_free_shared releases it. */
@@ -411,10 +417,7 @@ enum {
     PHUB_OPT_GRID = 2,        /* CTAs for the flat kernels, 0 = auto (SMs x occupancy)   */
     PHUB_OPT_TILE_ELEMS = 3,  /* max elements per CTA tile in the chunk-tile kernel (1024) */
     PHUB_OPT_CACHE = 4,       /* PHUB_CACHE_*: L2 policy of the pulled weights   */
-    PHUB_OPT_FLAT_SEG = 5,    /* flat kernels: 0 = grid-stride, else CTA-contiguous      */
-                              /* segments of this many vectors                           */
-    PHUB_OPT_FLAT_MINB = 6,   /* tuning: 0 = default build; 1,2,4,6,8 = N=8 256-bit flat */
-                              /* kernel compiled for that many resident CTAs per SM      */
+                              /* (5, 6: removed in round 2 -- measured without gain)     */
     PHUB_OPT_FLAT_ONESHOT = 7 /* flat kernels: 1 = one vector per thread, grid covering */
                               /* the range (the hardware CTA scheduler balances like     */
                               /* PHub's chunk -> core map); 0 = persistent grid (SMs x   */

@@ -20,15 +20,17 @@ STATUS_NAMES = [
     "PHUB_ERR_INVALID_CHUNK_SIZE", "PHUB_ERR_INVALID_INIT", "PHUB_ERR_BAD_WORKER",
     "PHUB_ERR_BAD_KEY", "PHUB_ERR_LENGTH_MISMATCH", "PHUB_ERR_DUPLICATE_PUSH",
     "PHUB_ERR_INCOMPLETE", "PHUB_ERR_CUDA", "PHUB_ERR_OUT_OF_MEMORY", "PHUB_ERR_UNSUPPORTED",
+    "PHUB_ERR_SYNC_TIMEOUT",
 ]
 for _i, _n in enumerate(STATUS_NAMES):
     globals()[_n] = _i
 PHUB_ALL_KEYS = -1
 PHUB_OWNED_RANGE = -2
-PHUB_COPY, PHUB_BORROW, PHUB_CONSUME = 0, 1, 2
+PHUB_COPY, PHUB_BORROW = 0, 1
 PHUB_OWNER_LPT, PHUB_OWNER_CONTIG = 0, 1
 PHUB_OPT_KERNEL, PHUB_OPT_GRID, PHUB_OPT_TILE_ELEMS, PHUB_OPT_CACHE = 1, 2, 3, 4
-PHUB_OPT_FLAT_SEG, PHUB_OPT_FLAT_MINB, PHUB_OPT_FLAT_ONESHOT = 5, 6, 7
+PHUB_OPT_FLAT_ONESHOT = 7
+PHUB_CROSS_RACK_SHARDED, PHUB_CROSS_RACK_RING = 0, 1
 (PHUB_KERNEL_AUTO, PHUB_KERNEL_FLAT, PHUB_KERNEL_TILES, PHUB_KERNEL_FLAT128,
  PHUB_KERNEL_WIDE, PHUB_KERNEL_BULK) = range(6)
 PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS = 0, 1
@@ -42,10 +44,7 @@ class phub_chunk(C.Structure):
 class phub_sync(C.Structure):
     _fields_ = [("wait_flag", C.c_void_p), ("wait_value", C.c_uint32),
                 ("signal_flag", C.c_void_p), ("signal_value", C.c_uint32),
-                ("block_elems", C.c_uint64), ("credit", C.c_void_p),
-                ("credit_base", C.c_uint32), ("credit_window", C.c_uint32),
-                ("credit_return", C.c_void_p), ("per_warp", C.c_int32),
-                ("oneshot", C.c_int32)]
+                ("block_elems", C.c_uint64)]
 
 
 class phub_hier(C.Structure):
@@ -93,6 +92,11 @@ _SIGS = {
     "phub_partial_sum": (C.c_int, [phub_ctx, C.POINTER(C.c_void_p), C.c_int32, C.c_void_p,
                                    C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]),
     "phub_sync_timeouts": (C.c_int, [phub_ctx, C.POINTER(C.c_uint32)]),
+    "phub_synchronize": (C.c_int, [phub_ctx, C.c_void_p]),
+    "phub_check": (C.c_int, [phub_ctx]),
+    "phub_hier_beneficial": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                       C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]),
     "phub_pull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
     "phub_pushpull": (C.c_int, [phub_ctx, C.c_int32, C.c_void_p, C.c_uint64, C.c_int32,
                                 C.c_void_p, C.c_void_p]),
@@ -197,13 +201,10 @@ def phub_aggregate_ready(ctx, stream: int = 0) -> int:
     return int(n.value)
 
 
-def _sync(wait=None, signal=None, block=0, credit=None, credit_return=None, per_warp=False,
-          oneshot=False):
+def _sync(wait=None, signal=None, block=0):
     """phub_sync from (flag_ptr, value) pairs; None when nothing is given.
-    block > 0: the flag pointers are per-block arrays (block-streaming form);
-    credit = (counter_ptr, base, window) on a producer, credit_return = a
-    counter pointer on a consumer (back-pressure)."""
-    if wait is None and signal is None and credit is None and credit_return is None:
+    block > 0: the flag pointers are per-block arrays (block-streaming form)."""
+    if wait is None and signal is None:
         return None
     s = phub_sync()
     if wait is not None:
@@ -211,36 +212,45 @@ def _sync(wait=None, signal=None, block=0, credit=None, credit_return=None, per_
     if signal is not None:
         s.signal_flag, s.signal_value = signal
     s.block_elems = int(block)
-    if credit is not None:
-        s.credit, s.credit_base, s.credit_window = credit
-    if credit_return is not None:
-        s.credit_return = credit_return
-    s.per_warp = int(bool(per_warp))
-    s.oneshot = int(bool(oneshot))
     return C.byref(s)
 
 
 def phub_aggregate_range(ctx, begin: int, end: int, stream: int = 0, wait=None, signal=None,
-                         block: int = 0, credit=None, credit_return=None, per_warp=False,
-                         oneshot=False):
-    _check(_lib.phub_aggregate_range(ctx, begin, end,
-                                     _sync(wait, signal, block, credit, credit_return, per_warp,
-                                           oneshot), stream), "phub_aggregate_range", ctx)
+                         block: int = 0):
+    _check(_lib.phub_aggregate_range(ctx, begin, end, _sync(wait, signal, block), stream),
+           "phub_aggregate_range", ctx)
 
 
 def phub_partial_sum(ctx, srcs, dst: int, begin: int, end: int, stream: int = 0, wait=None,
-                     signal=None, block: int = 0, credit=None, credit_return=None,
-                     per_warp=False):
+                     signal=None, block: int = 0):
     arr = (C.c_void_p * max(len(srcs), 1))(*srcs)
     _check(_lib.phub_partial_sum(ctx, arr, len(srcs), dst, begin, end,
-                                 _sync(wait, signal, block, credit, credit_return, per_warp),
-                                 stream), "phub_partial_sum", ctx)
+                                 _sync(wait, signal, block), stream), "phub_partial_sum", ctx)
 
 
 def phub_sync_timeouts(ctx) -> int:
     n = C.c_uint32()
     _check(_lib.phub_sync_timeouts(ctx, C.byref(n)), "phub_sync_timeouts", ctx)
     return int(n.value)
+
+
+def phub_check(ctx) -> int:
+    """The context's status without synchronizing (0 = PHUB_OK; never raises)."""
+    return int(_lib.phub_check(ctx))
+
+
+def phub_synchronize(ctx, stream: int = 0):
+    _check(_lib.phub_synchronize(ctx, stream), "phub_synchronize", ctx)
+
+
+def phub_hier_beneficial(workers_per_rack: int, racks: int, b_pbox: float, b_wkr: float,
+                         b_core: float, cross_rack: int = PHUB_CROSS_RACK_SHARDED):
+    """(beneficial, lhs, rhs) of the P:760-763 model (host-only)."""
+    ben, lhs, rhs = C.c_int32(), C.c_double(), C.c_double()
+    _check(_lib.phub_hier_beneficial(workers_per_rack, racks, b_pbox, b_wkr, b_core, cross_rack,
+                                     C.byref(ben), C.byref(lhs), C.byref(rhs)),
+           "phub_hier_beneficial", None)
+    return bool(ben.value), float(lhs.value), float(rhs.value)
 
 
 def phub_pull(ctx, key: int, dst_ptr: int, n: int, stream: int = 0):

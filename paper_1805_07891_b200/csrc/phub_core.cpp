@@ -79,27 +79,27 @@ struct phub_ctx_s {
     std::vector<uintptr_t> base_uploaded;
     uintptr_t* d_base = nullptr;
     std::vector<float*> replicas;     // peer weight replicas written by the kernel
-    uint64_t consume_mask = 0;        // workers pushed with PHUB_CONSUME this iteration
     uint64_t range_cursor = UINT64_MAX;   // phub_aggregate_range progress (UINT64_MAX: none)
     uint32_t* d_sync = nullptr;           // [0] CTA counter, [1] timeouts, [2] abandoned wait value,
                                           // [3] block ticket, [4] CTAs done (block streaming)
+    uint32_t* h_err = nullptr;            // host-mapped word a kernel sets on an expired wait
+    uint32_t* d_err = nullptr;            // its device address (kernel argument)
 
     // options + counters
     int kernel = PHUB_KERNEL_AUTO;
     int grid_override = 0;
-    uint64_t flat_seg = 0;
-    int flat_minb = 0;
     int flat_oneshot = -1;            // -1 auto: one-shot for local HBM streams (profiles/
                                       // r01_tune2), persistent grid when peer replicas are
                                       // registered (NVLink latency; profiles/r01_multi2)
     int cache = PHUB_CACHE_ENABLED;
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
-    int blocks_occ[2][2][phub::kMaxWorkers + 1] = {};   // resident CTAs/SM [warp][nag][nw]
+    int blocks_occ[2][phub::kMaxWorkers + 1] = {};      // resident CTAs/SM [nag][nw]
     int hier_occ[2] = {0, 0};                          // resident CTAs/SM of k_hier [worker_order]
     uint64_t iteration = 0;
     int launches = 0;
     uint64_t launches_total = 0;
     bool failed = false;
+    phub_status sticky = PHUB_OK;     // status every later call returns once failed
     std::string err;
 
     phub_status fail(phub_status s, const char* fmt, ...) {
@@ -113,8 +113,21 @@ struct phub_ctx_s {
     }
     phub_status cuda_fail(cudaError_t e, const char* where) {
         failed = true;
+        sticky = PHUB_ERR_CUDA;
         err = std::string(where) + ": " + cudaGetErrorString(e);
         return e == cudaErrorMemoryAllocation ? PHUB_ERR_OUT_OF_MEMORY : PHUB_ERR_CUDA;
+    }
+    // Entry check of every state-changing or data-returning call: a sticky
+    // failure, or a device-side wait that expired since the last call (the
+    // kernel raised the host-mapped word; reading it needs no synchronize).
+    phub_status guard() {
+        if (!failed && h_err && *reinterpret_cast<volatile uint32_t*>(h_err)) {
+            failed = true;
+            sticky = PHUB_ERR_SYNC_TIMEOUT;
+            err = "a device-side flag wait expired (~2 s): that launch skipped work, so the "
+                  "round's results are incomplete; the context is sticky-failed";
+        }
+        return failed ? sticky : PHUB_OK;
     }
 };
 
@@ -132,6 +145,7 @@ static const char* kStatusNames[] = {
     "PHUB_ERR_CUDA",
     "PHUB_ERR_OUT_OF_MEMORY",
     "PHUB_ERR_UNSUPPORTED",
+    "PHUB_ERR_SYNC_TIMEOUT",
 };
 
 // ------------------------------------------------------------ table logic
@@ -302,6 +316,7 @@ static void free_ctx(phub_ctx c) {
     cudaFree(c->d_tiles);
     cudaFree(c->d_base);
     cudaFree(c->d_sync);
+    if (c->h_err) cudaFreeHost(c->h_err);
     delete c;
 }
 
@@ -368,12 +383,15 @@ phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
         (c->keep_agg && (e = cudaMalloc(&c->d_agg, bytes)) != cudaSuccess) ||
         (e = cudaMalloc(&c->d_base, sizeof(uintptr_t) * c->base.size())) != cudaSuccess ||
         (e = cudaMalloc(&c->d_sync, 5 * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaHostAlloc(&c->h_err, sizeof(uint32_t), cudaHostAllocMapped)) != cudaSuccess ||
+        (e = cudaHostGetDevicePointer(&c->d_err, c->h_err, 0)) != cudaSuccess ||
         (c->n_tiles && (e = cudaMalloc(&c->d_tiles, sizeof(Tile) * c->n_tiles)) != cudaSuccess)) {
         cudaGetLastError();
         free_ctx(c);
         why = std::string("device arenas: ") + cudaGetErrorString(e);
         return PHUB_ERR_OUT_OF_MEMORY;
     }
+    *c->h_err = 0;
     bool ok = cudaMemset(c->d_sync, 0, 5 * sizeof(uint32_t)) == cudaSuccess &&
               cudaMemset(c->d_w, 0, bytes) == cudaSuccess &&
               cudaMemset(c->d_v, 0, bytes) == cudaSuccess &&
@@ -474,7 +492,7 @@ static bool is_device_ptr(const void* p) {
 phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad, uint64_t n,
                       int32_t mode, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     if (worker < 0 || worker >= c->N)
         return c->fail(PHUB_ERR_BAD_WORKER, "worker %d not in [0,%d) (S:170)", worker, c->N);
     const bool ranged = key == PHUB_OWNED_RANGE;
@@ -490,11 +508,8 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
         return c->fail(PHUB_ERR_LENGTH_MISMATCH, "push length %llu != %llu (S:172)",
                        (unsigned long long)n, (unsigned long long)want);
     if (!grad && n) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "grad is NULL");
-    if (mode != PHUB_COPY && mode != PHUB_BORROW && mode != PHUB_CONSUME)
-        return c->fail(PHUB_ERR_INVALID_ARGUMENT,
-                       "mode must be PHUB_COPY, PHUB_BORROW or PHUB_CONSUME");
-    const bool consume = mode == PHUB_CONSUME;
-    if (consume) mode = PHUB_BORROW;
+    if (mode != PHUB_COPY && mode != PHUB_BORROW)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "mode must be PHUB_COPY or PHUB_BORROW");
     const int k0 = all ? 0 : key, k1 = all ? c->K : key + 1;
     for (int k = k0; k < k1; ++k)
         if (c->got[(size_t)k * c->N + worker])
@@ -509,10 +524,6 @@ phub_status phub_push(phub_ctx c, int32_t worker, int32_t key, const float* grad
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW needs device memory");
         if (reinterpret_cast<uintptr_t>(grad) % 16 != 0)
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "PHUB_BORROW pointer must be 16-B aligned");
-        // the kernel may drop a consumed buffer's 128-B lines from L2 after reading them
-        if (consume && key == PHUB_ALL_KEYS && worker < 64 &&
-            reinterpret_cast<uintptr_t>(grad) % 128 == 0)
-            c->consume_mask |= 1ull << worker;
         // base + 4*dev_off is the byte address of padded element dev_off
         for (int k = k0; k < k1; ++k)
             c->base[(size_t)worker * c->K + k] =
@@ -609,7 +620,6 @@ static cudaError_t launch_keys(phub_ctx c, cudaStream_t s, const std::vector<uin
 static void end_iteration(phub_ctx c) {
     std::fill(c->got.begin(), c->got.end(), 0);
     c->got_count = 0;
-    c->consume_mask = 0;
     std::fill(c->done.begin(), c->done.end(), 0);
     c->done_count = 0;
     ++c->iteration;
@@ -617,7 +627,7 @@ static void end_iteration(phub_ctx c) {
 
 phub_status phub_aggregate_ready(phub_ctx c, void* stream, uint64_t* keys_done) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     if (c->range_cursor != UINT64_MAX)
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "iteration is being aggregated by ranges");
     if (!c->replicas.empty())
@@ -651,49 +661,33 @@ static void apply_sync(phub_ctx c, phub::FlatArgs& a, const phub_sync* sync) {
     a.cta_counter = c->d_sync;
     a.timeouts = c->d_sync + 1;
     a.ticket = c->d_sync + 3;
+    a.err_host = c->d_err;
     if (!sync) return;
     a.wait_flag = sync->wait_flag;
     a.wait_value = sync->wait_value;
     a.signal_flag = sync->signal_flag;
     a.signal_value = sync->signal_value;
     a.block = sync->block_elems;
-    if (a.block) {
-        a.credit = sync->credit;
-        a.credit_base = sync->credit_base;
-        a.credit_window = sync->credit_window;
-        a.credit_return = sync->credit_return;
-        a.per_warp = sync->per_warp ? 1 : 0;
-        a.oneshot = sync->oneshot ? 1 : 0;
-    }
 }
 
-// Block-streaming sync: blocks are whole multiples of one 256-thread x 8-element pass.
-static phub_status check_block_sync(phub_ctx c, const phub_sync* sync) {
-    if (!sync || !sync->block_elems) return PHUB_OK;
-    if (sync->oneshot && (sync->per_warp || sync->signal_flag || sync->credit_return))
-        return c->fail(PHUB_ERR_INVALID_ARGUMENT,
-                       "oneshot is for a fused consumer launch: no per_warp, signal or credit_return");
-    if (sync->block_elems % (sync->per_warp ? 256 : 2048))
-        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block_elems must be a multiple of %d",
-                       sync->per_warp ? 256 : 2048);
+// Flags must be 4-B aligned; blocks whole multiples of one 256-thread x 8-element pass.
+static phub_status check_sync(phub_ctx c, const phub_sync* sync) {
+    if (!sync) return PHUB_OK;
     if ((sync->wait_flag && reinterpret_cast<uintptr_t>(sync->wait_flag) % 4) ||
-        (sync->signal_flag && reinterpret_cast<uintptr_t>(sync->signal_flag) % 4) ||
-        (sync->credit && reinterpret_cast<uintptr_t>(sync->credit) % 4) ||
-        (sync->credit_return && reinterpret_cast<uintptr_t>(sync->credit_return) % 4))
-        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block flags and credit counters must be 4-B "
-                       "aligned");
+        (sync->signal_flag && reinterpret_cast<uintptr_t>(sync->signal_flag) % 4))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "flags must be 4-B aligned");
+    if (sync->block_elems % 2048)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "block_elems must be a multiple of 2048");
     return PHUB_OK;
 }
 
 // Persistent grid of a block-streaming launch: every SM x resident CTAs, at most one CTA per block.
-static int blocks_grid(phub_ctx c, int nw, bool nag, bool warp, uint64_t begin, uint64_t end,
-                       uint64_t B) {
-    int& occ = c->blocks_occ[warp ? 1 : 0][nag ? 1 : 0][std::min(nw, phub::kMaxWorkers)];
-    if (!occ) occ = phub::blocks_per_sm(nw, nag, warp);
+static int blocks_grid(phub_ctx c, int nw, bool nag, uint64_t begin, uint64_t end, uint64_t B) {
+    int& occ = c->blocks_occ[nag ? 1 : 0][std::min(nw, phub::kMaxWorkers)];
+    if (!occ) occ = phub::blocks_per_sm(nw, nag);
     const uint64_t nblk = (end + B - 1) / B - begin / B;
-    const uint64_t per_cta = warp ? phub::kThreads / 32 : 1;     // blocks in flight per CTA
     const int grid = c->grid_override ? c->grid_override : c->num_sms * occ;
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid, (nblk + per_cta - 1) / per_cta));
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)grid, nblk));
 }
 
 phub_status phub_sync_timeouts(phub_ctx c, uint32_t* count) {
@@ -701,7 +695,22 @@ phub_status phub_sync_timeouts(phub_ctx c, uint32_t* count) {
     DeviceGuard g(c->device);
     cudaError_t e = cudaMemcpy(count, c->d_sync + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return c->cuda_fail(e, "cudaMemcpy(timeouts)");
+    c->guard();            // the count is reported either way; a timeout also makes ctx sticky
     return PHUB_OK;
+}
+
+phub_status phub_check(phub_ctx c) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    return c->guard();
+}
+
+phub_status phub_synchronize(phub_ctx c, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    DeviceGuard g(c->device);
+    cudaError_t e = stream ? cudaStreamSynchronize(static_cast<cudaStream_t>(stream))
+                           : cudaDeviceSynchronize();
+    if (e != cudaSuccess && !c->failed) return c->cuda_fail(e, "synchronize");
+    return c->guard();
 }
 
 phub_status phub_push_batch(phub_ctx c, int32_t count, const int32_t* workers,
@@ -710,7 +719,7 @@ phub_status phub_push_batch(phub_ctx c, int32_t count, const int32_t* workers,
                             int32_t* failed_index) {
     if (failed_index) *failed_index = -1;
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     if (count < 0 || (count && (!workers || !keys || !grads || !lens)))
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "batch arrays are NULL");
     // all-or-nothing: validate every entry (including duplicates inside the
@@ -739,7 +748,6 @@ phub_status phub_push_batch(phub_ctx c, int32_t count, const int32_t* workers,
     std::vector<uint8_t> got_before = c->got;
     const uint64_t count_before = c->got_count;
     std::vector<uintptr_t> base_before = c->base;
-    const uint64_t consume_before = c->consume_mask;
     for (int32_t j = 0; j < count; ++j) {
         phub_status st = phub_push(c, workers[j], keys[j], grads[j], lens[j], mode, stream);
         if (st != PHUB_OK) {
@@ -747,7 +755,6 @@ phub_status phub_push_batch(phub_ctx c, int32_t count, const int32_t* workers,
             c->got = got_before;
             c->got_count = count_before;
             c->base = base_before;
-            c->consume_mask = consume_before;
             if (failed_index) *failed_index = j;
             return st;
         }
@@ -758,7 +765,7 @@ phub_status phub_push_batch(phub_ctx c, int32_t count, const int32_t* workers,
 phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count, float* dst,
                              uint64_t begin, uint64_t end, const phub_sync* sync, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     if (count < 1 || count > phub::kMaxWorkers || !srcs || !dst)
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "need 1..%d sources and a destination",
                        phub::kMaxWorkers);
@@ -775,13 +782,13 @@ phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count
     a.nw = count;
     a.begin = begin;
     a.end = end;
-    if (phub_status bs = check_block_sync(c, sync)) return bs;
+    if (phub_status bs = check_sync(c, sync)) return bs;
     apply_sync(c, a, sync);
     DeviceGuard g(c->device);
     c->launches = 0;
     cudaError_t e;
     if (a.block) {
-        e = phub::launch_blocks(a, dst, blocks_grid(c, count, false, a.per_warp, begin, end, a.block),
+        e = phub::launch_blocks(a, dst, blocks_grid(c, count, false, begin, end, a.block),
                                 static_cast<cudaStream_t>(stream), &c->launches);
     } else {
         const uint64_t nvec = (end - begin) / 8;
@@ -797,7 +804,7 @@ phub_status phub_partial_sum(phub_ctx c, const float* const* srcs, int32_t count
 phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
                                  const phub_sync* sync, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     if (c->got_count != (uint64_t)c->K * c->N)
         return c->fail(PHUB_ERR_INCOMPLETE, "%llu of %llu (worker,key) pushes received (S:181)",
                        (unsigned long long)c->got_count,
@@ -819,7 +826,7 @@ phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
     if (!flat)
         return c->fail(PHUB_ERR_UNSUPPORTED, "range aggregation needs whole-model / owned-range "
                        "pushes, 32-B aligned");
-    if (phub_status bs = check_block_sync(c, sync)) return bs;
+    if (phub_status bs = check_sync(c, sync)) return bs;
     DeviceGuard g(c->device);
     c->launches = 0;
     cudaError_t e = cudaSuccess;
@@ -842,9 +849,7 @@ phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
         const uint64_t nvec = (e_ - lo) / 8;
         const uint64_t cover = (nvec + phub::kThreads - 1) / phub::kThreads;
         if (a.block) {
-            a.discard = c->consume_mask;
-            e = e_ > lo ? phub::launch_blocks(a, nullptr,
-                                              blocks_grid(c, c->N, true, a.per_warp, lo, e_, a.block),
+            e = e_ > lo ? phub::launch_blocks(a, nullptr, blocks_grid(c, c->N, true, lo, e_, a.block),
                                               static_cast<cudaStream_t>(stream), &c->launches)
                         : cudaSuccess;
         } else {
@@ -869,7 +874,7 @@ phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
 
 phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     if (c->got_count != (uint64_t)c->K * c->N)
         return c->fail(PHUB_ERR_INCOMPLETE, "%llu of %llu (worker,key) pushes received (S:181)",
                        (unsigned long long)c->got_count,
@@ -939,6 +944,7 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
         a.nw = c->N;
         a.nrep = (int)c->replicas.size();
         for (int r = 0; r < a.nrep; ++r) a.rep[r] = c->replicas[r];
+        a.err_host = c->d_err;
         const int vec = variant == PHUB_KERNEL_FLAT ? 8 : 4;
         const uint64_t nvec = (eend - b) / vec;
         const uint64_t cover = (nvec + phub::kThreads - 1) / phub::kThreads;
@@ -947,16 +953,9 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
                          ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
                                      : c->flat_grid[vec == 8][c->keep_agg];
         grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, cover));
-        a.seg = c->flat_seg;
         if (variant == PHUB_KERNEL_BULK)
             e = phub::launch_bulk(a, c->grid_override ? c->grid_override : c->num_sms, s,
                                   &c->launches);
-        else if (c->flat_minb && vec == 8 && c->N == 8 && !c->keep_agg)
-            e = phub::launch_flat_minb(
-                a, c->flat_minb,
-                c->grid_override ? c->grid_override
-                                 : c->num_sms * phub::flat_minb_blocks_per_sm(c->flat_minb),
-                s, &c->launches);
         else
             e = phub::launch_flat(a, vec, c->cache, grid, s, &c->launches);
     } else if (variant == PHUB_KERNEL_WIDE) {
@@ -984,7 +983,7 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
 
 phub_status phub_pull(phub_ctx c, int32_t key, float* dst, uint64_t n, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     const bool all = key == PHUB_ALL_KEYS;
     if (!all && (key < 0 || key >= c->K))
         return c->fail(PHUB_ERR_BAD_KEY, "key %d not in [0,%d) and not PHUB_ALL_KEYS", key, c->K);
@@ -1013,6 +1012,7 @@ phub_status phub_pushpull(phub_ctx c, int32_t worker, const float* grad, uint64_
 
 phub_status phub_weights(phub_ctx c, float** w_dev) {
     if (!c || !w_dev) return PHUB_ERR_INVALID_ARGUMENT;
+    if (phub_status st0 = c->guard()) return st0;
     *w_dev = c->d_w;
     return PHUB_OK;
 }
@@ -1080,10 +1080,11 @@ static phub_status gather_keys(phub_ctx c, float* dst, const float* src_dev) {
 
 phub_status phub_load_state(phub_ctx c, const float* w, const float* v) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     DeviceGuard g(c->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return c->cuda_fail(e, "cudaDeviceSynchronize");
+    if (phub_status st1 = c->guard()) return st1;      // a wait expired in the launches waited for
     phub_status st = PHUB_OK;
     if (w && (st = scatter_keys(c, c->d_w, w)) != PHUB_OK) return st;
     if (v && (st = scatter_keys(c, c->d_v, v)) != PHUB_OK) return st;
@@ -1092,12 +1093,13 @@ phub_status phub_load_state(phub_ctx c, const float* w, const float* v) {
 
 phub_status phub_read_state(phub_ctx c, float* w, float* v, float* agg) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     if (agg && !c->keep_agg)
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "agg requested but keep_aggregate is off");
     DeviceGuard g(c->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return c->cuda_fail(e, "cudaDeviceSynchronize");
+    if (phub_status st1 = c->guard()) return st1;      // never return a partly skipped round
     phub_status st = PHUB_OK;
     if (w && (st = gather_keys(c, w, c->d_w)) != PHUB_OK) return st;
     if (v && (st = gather_keys(c, v, c->d_v)) != PHUB_OK) return st;
@@ -1137,7 +1139,7 @@ phub_status phub_set_replicas(phub_ctx c, float* const* replicas, int32_t count)
 
 phub_status phub_hier_exchange(phub_ctx c, const phub_hier* h, void* stream) {
     if (!c) return PHUB_ERR_INVALID_ARGUMENT;
-    if (c->failed) return PHUB_ERR_CUDA;
+    if (phub_status st0 = c->guard()) return st0;
     if (!h || h->num_racks != c->G || h->num_racks > phub::kMaxRacks)
         return c->fail(PHUB_ERR_INVALID_ARGUMENT, "num_racks must equal the context's owners (<= %d)",
                        phub::kMaxRacks);
@@ -1204,6 +1206,7 @@ phub_status phub_hier_exchange(phub_ctx c, const phub_hier* h, void* stream) {
     a.worker_order = h->worker_order ? 1 : 0;
     a.ticket = c->d_sync + 3;
     a.timeouts = c->d_sync + 1;
+    a.err_host = c->d_err;
     DeviceGuard g(c->device);
     c->launches = 0;
     int& occ = c->hier_occ[a.worker_order];
@@ -1305,23 +1308,14 @@ phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
                         c->num_sms * phub::flat_blocks_per_sm(vec8 ? 8 : 4, c->N, agg, c->cache);
             return PHUB_OK;
         }
-        case PHUB_OPT_FLAT_SEG:
-            if (value < 0) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "segment must be >= 0");
-            c->flat_seg = (uint64_t)value;
-            return PHUB_OK;
         case PHUB_OPT_FLAT_ONESHOT:
             if (value < -1 || value > 1) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "-1, 0 or 1");
             c->flat_oneshot = (int)value;
             return PHUB_OK;
-        case PHUB_OPT_FLAT_MINB:
-            if (!(value == 0 || value == 1 || value == 2 || value == 4 || value == 6 || value == 8))
-                return c->fail(PHUB_ERR_INVALID_ARGUMENT, "minb must be 0,1,2,4,6,8");
-            c->flat_minb = (int)value;
-            return PHUB_OK;
         case PHUB_OPT_TILE_ELEMS: {
             if (value < 1 || value > (1 << 30))
                 return c->fail(PHUB_ERR_INVALID_ARGUMENT, "tile elements must be in [1, 2^30]");
-            if (c->failed) return PHUB_ERR_CUDA;
+            if (phub_status st0 = c->guard()) return st0;
             DeviceGuard g(c->device);
             const uint32_t old = c->tile_elems;
             c->tile_elems = (uint32_t)value;
@@ -1347,6 +1341,36 @@ phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
         default:
             return c->fail(PHUB_ERR_INVALID_ARGUMENT, "unknown option %d", option);
     }
+}
+
+// Hierarchical-reduction benefit model, PAPER.md P:760-763 (S 3.4 "Rack
+// Deployment and Topology-Aware Reduction"), as printed (R18):
+//   B_bn = min((r-1) B_PBox, B_Core)
+//   beneficial  <=>  max((N-1)/B_bn, 1/(N B_Wkr)) > max(1/B_PBox, N/B_Wkr) + C
+//   C = (N-1)/(N B_bn)  sharded cross-rack step,  C = (r-1)/(r B_bn)  ring.
+phub_status phub_hier_beneficial(int32_t workers_per_rack, int32_t racks, double b_pbox,
+                                 double b_wkr, double b_core, int32_t cross_rack,
+                                 int32_t* beneficial, double* lhs, double* rhs) {
+    std::string& why = g_init_err;
+    why.clear();
+    if (!beneficial) return why = "beneficial is NULL", PHUB_ERR_INVALID_ARGUMENT;
+    if (workers_per_rack < 1 || racks < 2)
+        return why = "need >= 1 worker per rack and >= 2 racks", PHUB_ERR_INVALID_ARGUMENT;
+    if (!(std::isfinite(b_pbox) && b_pbox > 0) || !(std::isfinite(b_wkr) && b_wkr > 0) ||
+        !(std::isfinite(b_core) && b_core > 0))
+        return why = "bandwidths must be finite and > 0", PHUB_ERR_INVALID_ARGUMENT;
+    if (cross_rack != PHUB_CROSS_RACK_SHARDED && cross_rack != PHUB_CROSS_RACK_RING)
+        return why = "cross_rack must be PHUB_CROSS_RACK_SHARDED or _RING", PHUB_ERR_INVALID_ARGUMENT;
+    const double N = workers_per_rack, r = racks;
+    const double b_bn = std::min((r - 1) * b_pbox, b_core);
+    const double C = cross_rack == PHUB_CROSS_RACK_SHARDED ? (N - 1) / (N * b_bn)
+                                                           : (r - 1) / (r * b_bn);
+    const double L = std::max((N - 1) / b_bn, 1.0 / (N * b_wkr));
+    const double R = std::max(1.0 / b_pbox, N / b_wkr) + C;
+    *beneficial = L > R ? 1 : 0;
+    if (lhs) *lhs = L;
+    if (rhs) *rhs = R;
+    return PHUB_OK;
 }
 
 }  // extern "C"

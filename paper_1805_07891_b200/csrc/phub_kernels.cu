@@ -15,11 +15,17 @@
 //
 // Kernels:
 //   k_flat   owned padded range walked as 256-bit (LDG.E.256/STG.E.256, new on
-//            sm_100a) or 128-bit vectors; persistent grid sized to
-//            SMs x resident CTAs; workers' bases in kernel params.  Bases may
-//            be peer-mapped (NVLink loads) and w' may also be stored into peer
-//            replicas: the push, the aggregate+optimize and the pull's
+//            sm_100a) or 128-bit vectors; one-shot grid (one vector per
+//            thread, the hardware CTA scheduler hands out 2048-element pieces
+//            like PHub's chunk -> core map), or a persistent grid when peer
+//            replicas are registered; workers' bases in kernel params.  Bases
+//            may be peer-mapped (NVLink loads) and w' may also be stored into
+//            peer replicas: the push, the aggregate+optimize and the pull's
 //            all-gather fused in one kernel over peer memory.
+//   k_blocks block-streamed chain stage (per-block device flags)
+//   k_hier   owner-sharded push exchange / hierarchical reduction (one
+//            ticket-ordered launch per GPU)
+//   k_bulk   TMA-engine staging variant (1-D cp.async.bulk into a smem ring)
 //   k_tiles  one CTA per chunk tile (PHub's chunk -> core mapping, P:708-713,
 //            with the hardware CTA scheduler as the "core" assigner); worker
 //            pointers per (worker, key) for per-key pushes; 128-bit body +
@@ -130,8 +136,23 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 
+// An expired wait: counted on the device (timeouts[0]), the value given up on
+// recorded (timeouts[1], so the rest of the launch stops waiting for it), and
+// the host-mapped error word raised -- the host makes the context
+// sticky-failed (PHUB_ERR_SYNC_TIMEOUT) on its next call, so skipped work is
+// never reported as a completed round.
+__device__ __forceinline__ void record_timeout(uint32_t* timeouts, volatile uint32_t* err_host,
+                                               uint32_t value) {
+    atomicAdd(timeouts, 1u);
+    atomicMax(timeouts + 1, value);
+    if (err_host) {
+        *err_host = 1u;
+        __threadfence_system();
+    }
+}
+
 // Every CTA waits for the previous stage's flag (bounded); returns false when
-// the wait expired (the CTA then skips its work; the timeout is counted).
+// the wait expired (the CTA then skips its work; the timeout is recorded).
 __device__ __forceinline__ bool stage_wait(const FlatArgs& a) {
     if (!a.wait_flag) return true;
     __shared__ int ok;
@@ -147,8 +168,7 @@ __device__ __forceinline__ bool stage_wait(const FlatArgs& a) {
                 break;
             }
             if (globaltimer_ns() - t0 > 2000000000ull) {
-                atomicAdd(a.timeouts, 1u);
-                atomicMax(a.timeouts + 1, a.wait_value);
+                record_timeout(a.timeouts, a.err_host, a.wait_value);
                 good = 0;
                 break;
             }
@@ -160,7 +180,11 @@ __device__ __forceinline__ bool stage_wait(const FlatArgs& a) {
     return ok != 0;
 }
 
-// After all CTAs' stores: the last CTA to finish raises the next stage's flag.
+// After all CTAs' stores: the last CTA to finish raises the next stage's flag
+// -- unless a CTA of this launch gave up its wait (its work was skipped): then
+// the flag stays down, the downstream stage times out too and records its own
+// error instead of consuming a stale partial (every CTA still counts itself,
+// so the counter resets for the next launch).
 __device__ __forceinline__ void stage_signal(const FlatArgs& a) {
     if (!a.signal_flag) return;
     __threadfence_system();                       // this thread's (peer) stores are visible
@@ -169,8 +193,10 @@ __device__ __forceinline__ void stage_signal(const FlatArgs& a) {
         const uint32_t done = atomicAdd(a.cta_counter, 1u);
         if (done == gridDim.x - 1) {
             *a.cta_counter = 0;
+            // every other CTA's atomicMax (if any) preceded its fence + counter add
+            const bool abandoned = a.wait_flag && atomicAdd(a.timeouts + 1, 0u) >= a.wait_value;
             __threadfence_system();
-            st_release_sys(a.signal_flag, a.signal_value);
+            if (!abandoned) st_release_sys(a.signal_flag, a.signal_value);
         }
     }
 }
@@ -245,23 +271,15 @@ __device__ __forceinline__ void flat_body(const FlatArgs& a, uint64_t i) {
     }
 }
 
-// Schedules: seg == 0 -> grid-stride over vectors (all CTAs sweep the range
-// together); seg > 0 -> each CTA takes contiguous segments of `seg` vectors
-// (CTAs spread over the range, like one CTA per chunk tile).
+// Grid-stride over vectors: with a grid covering the range (one-shot, the
+// default) every thread handles one vector; with a persistent grid (SMs x
+// resident CTAs) the CTAs sweep the range together.
 template <int NW, int VEC, int CACHE, bool AGG>
 __device__ __forceinline__ void flat_loop(const FlatArgs& a) {
     const uint64_t n = (a.end - a.begin) / VEC;
-    if (a.seg == 0) {
-        const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-        for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
-            flat_body<NW, VEC, CACHE, AGG>(a, i);
-    } else {
-        for (uint64_t b0 = (uint64_t)blockIdx.x * a.seg; b0 < n; b0 += (uint64_t)gridDim.x * a.seg) {
-            const uint64_t b1 = b0 + a.seg < n ? b0 + a.seg : n;
-            for (uint64_t i = b0 + threadIdx.x; i < b1; i += kThreads)
-                flat_body<NW, VEC, CACHE, AGG>(a, i);
-        }
-    }
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
+        flat_body<NW, VEC, CACHE, AGG>(a, i);
     if (a.nrep) __threadfence_system();   // peer stores performed before the grid retires
 }
 
@@ -269,11 +287,6 @@ template <int NW, int VEC, int CACHE, bool AGG>
 __global__ void __launch_bounds__(kThreads) k_flat(const __grid_constant__ FlatArgs a) {
     if (stage_wait(a)) flat_loop<NW, VEC, CACHE, AGG>(a);
     stage_signal(a);
-}
-
-template <int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_flat_minb(const __grid_constant__ FlatArgs a) {
-    flat_loop<8, 8, PHUB_CACHE_ENABLED, false>(a);
 }
 
 // ---------------------------------------------------------- chunk tiles
@@ -371,7 +384,7 @@ __global__ void __launch_bounds__(kThreads) k_prefix(const __grid_constant__ Fla
         reinterpret_cast<V8*>(dst + a.begin)[i] = out;
     }
     __threadfence_system();
-    stage_signal(a);
+    stage_signal(a);                              // held back if any CTA's wait expired
 }
 
 // ------------------------------------------- block-streaming chain stages
@@ -426,17 +439,6 @@ __device__ __forceinline__ void blocks_body(const FlatArgs& a, float* __restrict
                 }
         }
     }
-    if (a.discard) {
-        // consumed inputs (PHUB_CONSUME): the lane holding the first 32 B of
-        // each 128-B line drops it from L2 once the whole warp has its data --
-        // no write-back of a staging buffer
-        __syncwarp(__activemask());
-        if ((i & 3) == 0)
-            for (int k = 0; k < nw; ++k)
-                if ((a.discard >> k) & 1)
-                    asm volatile("discard.global.L2 [%0], 128;"
-                                 :: "l"(reinterpret_cast<const V8*>(a.g[k]) + i) : "memory");
-    }
     V8 out;
     if constexpr (NAG) {
         V8* w = reinterpret_cast<V8*>(a.w);
@@ -468,26 +470,12 @@ __device__ __forceinline__ int wait_bounded(const FlatArgs& a, const uint32_t* f
     while (ld_acquire_sys(flag) < value) {
         if (*abandoned >= value) return 0;
         if (globaltimer_ns() - t0 > 2000000000ull) {
-            atomicAdd(a.timeouts, 1u);
-            atomicMax(a.timeouts + 1, value);
+            record_timeout(a.timeouts, a.err_host, value);
             return 0;
         }
         __nanosleep(100);
     }
     return 1;
-}
-
-// Back-pressure: block blk may start once the consumer finished blk - window blocks.
-__device__ __forceinline__ void credit_wait(const FlatArgs& a, uint64_t rel) {
-    const uint32_t need = a.credit_base + (uint32_t)rel - a.credit_window;
-    const uint64_t t0 = globaltimer_ns();
-    while ((int32_t)(ld_acquire_sys(a.credit) - need) < 0) {
-        if (globaltimer_ns() - t0 > 2000000000ull) {
-            atomicAdd(a.timeouts, 1u);
-            break;
-        }
-        __nanosleep(100);
-    }
 }
 
 // CTA-granular: each CTA takes a block (multiple of 2048 elements) per ticket.
@@ -504,10 +492,7 @@ __global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ Fla
         if (threadIdx.x == 0) {
             const uint64_t blk = b0 + atomicAdd(a.ticket, 1u);
             int go = 1;
-            if (blk < b1) {
-                if (a.credit && blk - b0 >= a.credit_window) credit_wait(a, blk - b0);
-                if (a.wait_flag) go = wait_bounded(a, a.wait_flag + blk, a.wait_value);
-            }
+            if (blk < b1 && a.wait_flag) go = wait_bounded(a, a.wait_flag + blk, a.wait_value);
             s_blk = blk;
             s_go = go;
         }
@@ -522,13 +507,9 @@ __global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ Fla
         // system-scope fence: cumulative over the CTA's stores (the
         // cooperative-groups grid-sync pattern)
         __syncthreads();
-        if (threadIdx.x == 0) {
-            if (a.signal_flag && go) {
-                __threadfence_system();
-                st_release_sys(a.signal_flag + blk, a.signal_value);
-            }
-            // flow control only (the producer never rewrites a block within a round)
-            if (a.credit_return) atomicAdd_system(a.credit_return, 1u);
+        if (threadIdx.x == 0 && a.signal_flag && go) {   // a skipped block is never signalled
+            __threadfence_system();
+            st_release_sys(a.signal_flag + blk, a.signal_value);
         }
     }
     if (NAG && a.nrep) __threadfence_system();
@@ -539,102 +520,19 @@ __global__ void __launch_bounds__(kThreads) k_blocks(const __grid_constant__ Fla
     }
 }
 
-// Warp-granular: each WARP takes, processes and signals its own block (a
-// multiple of 256 elements).  No CTA barrier anywhere: a warp waiting in its
-// system-scope fence (its NVLink stores being acknowledged) stalls only
-// itself, so blocks can be small -- a short pipeline fill -- without the
-// per-block fence idling the SM.
-template <int NW, bool NAG>
-__global__ void __launch_bounds__(kThreads) k_wblocks(const __grid_constant__ FlatArgs a,
-                                                      float* __restrict__ dst) {
-    const uint64_t B = a.block;
-    const uint64_t b0 = a.begin / B, b1 = (a.end + B - 1) / B;
-    const unsigned lane = threadIdx.x & 31;
-    constexpr unsigned FULL = 0xffffffffu;
-    for (;;) {
-        uint64_t blk = 0;
-        int go = 1;
-        if (lane == 0) {
-            blk = b0 + atomicAdd(a.ticket, 1u);
-            if (blk < b1) {
-                if (a.credit && blk - b0 >= a.credit_window) credit_wait(a, blk - b0);
-                if (a.wait_flag) go = wait_bounded(a, a.wait_flag + blk, a.wait_value);
-            }
-        }
-        blk = __shfl_sync(FULL, blk, 0);
-        go = __shfl_sync(FULL, go, 0);
-        if (blk >= b1) break;
-        const uint64_t lo = (blk * B > a.begin ? blk * B : a.begin) / 8;
-        const uint64_t hi = ((blk + 1) * B < a.end ? (blk + 1) * B : a.end) / 8;
-        for (uint64_t i = lo + lane; go && i < hi; i += 32) blocks_body<NW, NAG>(a, dst, i);
-        __syncwarp();                        // orders the warp's stores before lane 0's fence
-        if (lane == 0) {
-            if (a.signal_flag && go) {
-                __threadfence_system();
-                st_release_sys(a.signal_flag + blk, a.signal_value);
-            }
-            if (a.credit_return) atomicAdd_system(a.credit_return, 1u);
-        }
-    }
-    if (NAG && a.nrep) __threadfence_system();
-    if (lane == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x * (kThreads / 32) - 1) {
-        a.ticket[0] = 0;
-        a.ticket[1] = 0;
-    }
-}
-
-// One-shot consumer: one CTA per 2048 elements over the whole range (the
-// hardware block scheduler hands CTAs out in order, like k_flat's one-shot
-// schedule); each CTA waits for the upstream flag of the block holding its
-// elements, then runs the fused step on one 256-bit vector per thread.
-template <int NW>
-__global__ void __launch_bounds__(kThreads) k_oneshot_consume(const __grid_constant__ FlatArgs a) {
-    __shared__ int s_go;
-    const uint64_t i = a.begin / 8 + (uint64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (threadIdx.x == 0) {
-        const uint64_t blk = (a.begin + (uint64_t)blockIdx.x * kThreads * 8) / a.block;
-        s_go = a.wait_flag ? wait_bounded(a, a.wait_flag + blk, a.wait_value) : 1;
-    }
-    __syncthreads();
-    if (s_go && i < a.end / 8) blocks_body<NW, true>(a, nullptr, i);
-    // no per-CTA system fence: the replica stores are ordered before the
-    // caller's next stream operation by the kernel boundary
-}
-
-template <bool NAG, bool WARP>
-void* pick_blocks_t(int nw) {
-#define PHUB_KB(n) (WARP ? (void*)k_wblocks<n, NAG> : (void*)k_blocks<n, NAG>)
-    switch (nw) {
-        case 1: return PHUB_KB(1);
-        case 2: return PHUB_KB(2);
-        case 3: return PHUB_KB(3);
-        case 4: return PHUB_KB(4);
-        case 5: return PHUB_KB(5);
-        case 6: return PHUB_KB(6);
-        case 7: return PHUB_KB(7);
-        case 8: return PHUB_KB(8);
-        case 9: return PHUB_KB(9);
-        default: return PHUB_KB(0);
-    }
-#undef PHUB_KB
-}
 template <bool NAG>
-void* pick_blocks(int nw, bool warp) {
-    return warp ? pick_blocks_t<NAG, true>(nw) : pick_blocks_t<NAG, false>(nw);
-}
-
-void* pick_oneshot(int nw) {
+void* pick_blocks(int nw) {
     switch (nw) {
-        case 1: return (void*)k_oneshot_consume<1>;
-        case 2: return (void*)k_oneshot_consume<2>;
-        case 3: return (void*)k_oneshot_consume<3>;
-        case 4: return (void*)k_oneshot_consume<4>;
-        case 5: return (void*)k_oneshot_consume<5>;
-        case 6: return (void*)k_oneshot_consume<6>;
-        case 7: return (void*)k_oneshot_consume<7>;
-        case 8: return (void*)k_oneshot_consume<8>;
-        case 9: return (void*)k_oneshot_consume<9>;
-        default: return (void*)k_oneshot_consume<0>;
+        case 1: return (void*)k_blocks<1, NAG>;
+        case 2: return (void*)k_blocks<2, NAG>;
+        case 3: return (void*)k_blocks<3, NAG>;
+        case 4: return (void*)k_blocks<4, NAG>;
+        case 5: return (void*)k_blocks<5, NAG>;
+        case 6: return (void*)k_blocks<6, NAG>;
+        case 7: return (void*)k_blocks<7, NAG>;
+        case 8: return (void*)k_blocks<8, NAG>;
+        case 9: return (void*)k_blocks<9, NAG>;
+        default: return (void*)k_blocks<0, NAG>;
     }
 }
 
@@ -765,8 +663,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ Hi
                         while (ld_acquire_sys(f) < a.epoch) {
                             if (*abandoned >= a.epoch) { good = 0; break; }
                             if (globaltimer_ns() - t0 > 2000000000ull) {
-                                atomicAdd(a.timeouts, 1u);
-                                atomicMax(a.timeouts + 1, a.epoch);
+                                record_timeout(a.timeouts, a.err_host, a.epoch);
                                 good = 0;
                                 break;
                             }
@@ -1067,35 +964,6 @@ TileFn pick_tiles_nw(int nw) {
 
 }  // namespace
 
-static const void* minb_fn(int minb) {
-    switch (minb) {
-        case 1: return reinterpret_cast<const void*>(k_flat_minb<1>);
-        case 2: return reinterpret_cast<const void*>(k_flat_minb<2>);
-        case 4: return reinterpret_cast<const void*>(k_flat_minb<4>);
-        case 6: return reinterpret_cast<const void*>(k_flat_minb<6>);
-        case 8: return reinterpret_cast<const void*>(k_flat_minb<8>);
-        default: return nullptr;
-    }
-}
-
-int flat_minb_blocks_per_sm(int minb) {
-    int nb = 0;
-    const void* fn = minb_fn(minb);
-    if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess)
-        return 1;
-    return nb > 0 ? nb : 1;
-}
-
-cudaError_t launch_flat_minb(const FlatArgs& a, int minb, int grid, cudaStream_t s, int* launches) {
-    if (a.end <= a.begin) return cudaSuccess;
-    const void* fn = minb_fn(minb);
-    if (!fn || a.nw != 8 || a.agg) return cudaErrorInvalidValue;
-    void* args[] = {const_cast<FlatArgs*>(&a)};
-    cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);
-    ++*launches;
-    return e;
-}
-
 int flat_blocks_per_sm(int vec, int nw, bool agg, int cache) {
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -1135,24 +1003,16 @@ cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t 
     return cudaGetLastError();
 }
 
-int blocks_per_sm(int nw, bool nag, bool warp) {
+int blocks_per_sm(int nw, bool nag) {
     int nb = 0;
-    const void* fn = nag ? pick_blocks<true>(nw, warp) : pick_blocks<false>(nw, warp);
+    const void* fn = nag ? pick_blocks<true>(nw) : pick_blocks<false>(nw);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kThreads, 0) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches) {
     if (a.end <= a.begin || a.block == 0) return cudaSuccess;
-    if (a.oneshot && !dst) {                          // one CTA per 2048 elements
-        const uint64_t ctas = (a.end / 8 - a.begin / 8 + kThreads - 1) / kThreads;
-        void* args[] = {const_cast<FlatArgs*>(&a)};
-        cudaError_t e = cudaLaunchKernel(pick_oneshot(a.nw), dim3((unsigned)ctas), dim3(kThreads),
-                                         args, 0, s);
-        ++*launches;
-        return e;
-    }
-    void* fn = dst ? pick_blocks<false>(a.nw, a.per_warp != 0) : pick_blocks<true>(a.nw, a.per_warp != 0);
+    void* fn = dst ? pick_blocks<false>(a.nw) : pick_blocks<true>(a.nw);
     void* args[] = {const_cast<FlatArgs*>(&a), &dst};
     cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);
     ++*launches;

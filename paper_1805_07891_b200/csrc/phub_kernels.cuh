@@ -28,22 +28,17 @@ struct FlatArgs {
     int nw;
     int nrep;                         // extra replicas (peer-mapped) that also receive w'
     float* rep[kMaxReplicas];
-    uint64_t seg;                     // 0: grid-stride; else CTA-contiguous segments (vectors)
     // optional device-side stage ordering (chained exchange)
     const uint32_t* wait_flag;
     uint32_t wait_value;
     uint32_t* signal_flag;
     uint32_t signal_value;
     uint32_t* cta_counter;            // local counter: last CTA raises signal_flag
-    uint32_t* timeouts;               // local counter of expired waits
+    uint32_t* timeouts;               // [0] expired waits, [1] highest wait value given up on
+    volatile uint32_t* err_host;      // host-mapped word set to 1 on any expired wait: the
+                                      // host turns it into a sticky PHUB_ERR_SYNC_TIMEOUT
     uint64_t block;                   // > 0: block-streaming flags (one per `block` elements)
-    uint64_t discard;                 // bit k: input k is consumed (L2 lines may be discarded)
     uint32_t* ticket;                 // [0] next block, [1] CTAs done (block streaming, zeroed)
-    const uint32_t* credit;           // back-pressure (block streaming): see phub_sync
-    uint32_t credit_base, credit_window;
-    uint32_t* credit_return;
-    int per_warp;                     // block streaming: warps (not CTAs) take/signal blocks
-    int oneshot;                      // block streaming, fused consumer: one CTA per 2048 elements
 };
 
 // Hierarchical reduction: one GPU = one rack's PBox with its P
@@ -68,6 +63,7 @@ struct HierArgs {
     uint32_t epoch;
     uint32_t* ticket;                 // [0] next item, [1] CTAs done
     uint32_t* timeouts;               // [0] expired waits, [1] abandoned epoch
+    volatile uint32_t* err_host;      // host-mapped sticky-error word (see FlatArgs)
     int worker_order;                 // 1: flat worker-order sum of raw slices (M3 exchange)
 };
 cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launches);
@@ -107,7 +103,7 @@ cudaError_t launch_prefix(const FlatArgs& a, float* dst, int grid, cudaStream_t 
 // raising a.signal_flag[b] per block.  dst == nullptr: fused Nesterov (w, v,
 // replicas); else the worker-order partial sum stored into dst.
 cudaError_t launch_blocks(const FlatArgs& a, float* dst, int grid, cudaStream_t s, int* launches);
-int blocks_per_sm(int nw, bool nag, bool warp);
+int blocks_per_sm(int nw, bool nag);
 // TMA-style staging: 1-D bulk async copies into a shared-memory ring (nw <= 8).
 cudaError_t launch_bulk(const FlatArgs& a, int grid, cudaStream_t s, int* launches);
 size_t bulk_smem_bytes(int nw);
@@ -115,10 +111,5 @@ cudaError_t launch_wide(const WideArgs& a, int grid, cudaStream_t s, int* launch
 
 // Resident CTAs per SM of the flat kernel for (vec, nw, agg) -- grid sizing.
 int flat_blocks_per_sm(int vec, int nw, bool agg, int cache);
-
-// Tuning experiment: the N=8, 256-bit flat kernel compiled for `minb` resident
-// CTAs per SM (launch bounds 1, 2, 4, 6 or 8).
-cudaError_t launch_flat_minb(const FlatArgs& a, int minb, int grid, cudaStream_t s, int* launches);
-int flat_minb_blocks_per_sm(int minb);
 
 }  // namespace phub

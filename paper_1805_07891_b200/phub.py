@@ -17,10 +17,9 @@ import ctypes as C
 import numpy as np
 
 from . import capi
-from .capi import PHUB_ALL_KEYS, PHUB_BORROW, PHUB_CONSUME, PHUB_COPY
+from .capi import PHUB_ALL_KEYS, PHUB_BORROW, PHUB_COPY
 
-_MODES = {"borrow": PHUB_BORROW, "copy": PHUB_COPY, "consume": PHUB_CONSUME,
-          PHUB_BORROW: PHUB_BORROW, PHUB_COPY: PHUB_COPY, PHUB_CONSUME: PHUB_CONSUME}
+_MODES = {"borrow": PHUB_BORROW, "copy": PHUB_COPY, PHUB_BORROW: PHUB_BORROW, PHUB_COPY: PHUB_COPY}
 _POLICIES = {"lpt": capi.PHUB_OWNER_LPT, "contig": capi.PHUB_OWNER_CONTIG,
              capi.PHUB_OWNER_LPT: capi.PHUB_OWNER_LPT, capi.PHUB_OWNER_CONTIG: capi.PHUB_OWNER_CONTIG}
 
@@ -171,6 +170,11 @@ class PHub:
             if buf is not None and _ptr_len(buf)[1] != self.E:
                 raise ValueError("state arrays must have E elements")
         capi.phub_load_state(self.ctx, pw, pv)
+
+    def synchronize(self, stream=None):
+        """Wait for this context's work; raises PhubError(PHUB_ERR_SYNC_TIMEOUT) if a
+        device-side wait expired (the round is then incomplete)."""
+        capi.phub_synchronize(self.ctx, self._stream(stream) if stream is not None else 0)
 
     def set_option(self, option, value):
         capi.phub_set_option(self.ctx, int(option), int(value))

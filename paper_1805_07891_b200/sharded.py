@@ -372,7 +372,64 @@ def chain_block_for(E_padded: int) -> int:
     return 8192 if E_padded < (64 << 20) else 12288
 
 
-class ChainShardedPHub:
+class ExchangeFailed(RuntimeError):
+    """A device-side flag wait of this job expired on this rank (PHUB_ERR_SYNC_TIMEOUT):
+    the round is incomplete.  Raised by exchange() on every later round; the rank
+    still takes part in the round's collectives first, so its peers never hang --
+    their waits on its flags expire and their next exchange() raises too."""
+
+
+class _DeviceWaitExchange:
+    """Shared failure handling of the exchanges whose kernels wait on device flags
+    (chain, push, hierarchical): a failed context skips its kernels but keeps
+    every collective of the round, then raises."""
+
+    def barrier(self):
+        """Stream-ordered one-float all-reduce (counted, see _round)."""
+        import torch.distributed as dist
+        self._nbar = getattr(self, "_nbar", 0) + 1
+        dist.all_reduce(self._flag, group=self.group)
+
+    def _barriers_per_round(self):
+        return 2                                   # start + end
+
+    def _round(self, body):
+        """Run one round's body; if the context is (or becomes) failed, still issue
+        the round's remaining collectives, then raise ExchangeFailed."""
+        self._nbar = 0
+        st = capi.phub_check(self.hub.ctx)
+        if not st:
+            try:
+                body()
+                return
+            except capi.PhubError as e:
+                st = e.status
+        for _ in range(self._barriers_per_round() - self._nbar):
+            self.barrier()
+        raise ExchangeFailed(f"rank {self.rank}: {capi.STATUS_NAMES[st]} "
+                             f"({capi.phub_last_error(self.hub.ctx)})")
+
+    def check(self):
+        """Collective: wait for this rank's work and raise ExchangeFailed on EVERY
+        rank if any rank's context failed (its round results are incomplete)."""
+        import torch
+        import torch.distributed as dist
+        try:
+            self.hub.synchronize()
+            st = 0
+        except capi.PhubError as e:
+            st = e.status
+        t = torch.tensor([st], dtype=torch.int32, device=f"cuda:{self.device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        worst = int(t.item())
+        if worst:
+            raise ExchangeFailed(f"an exchange failed on some rank: {capi.STATUS_NAMES[worst]}")
+
+    def sync_timeouts(self) -> int:
+        return capi.phub_sync_timeouts(self.hub.ctx)
+
+
+class ChainShardedPHub(_DeviceWaitExchange):
     """Chained exchange.
 
     Workers are hosted in rank order, so the worker-order sum can be built
@@ -388,18 +445,15 @@ class ChainShardedPHub:
 
     sync="blocks" (default): ONE persistent launch per rank and round; the
       model is cut into blocks of `block` elements with one device flag each,
-      so rank p+1 starts on block b as soon as rank p has raised its flag
-      (streaming).  With pull=True (default) each rank keeps its partial
-      in its own HBM and the next rank reads it over NVLink inside its kernel,
-      so the incoming partial never costs the consumer an HBM write + read.
+      so rank p+1 starts on block b as soon as rank p has stored it into its
+      inbox over NVLink and raised the flag (streaming).
     sync="flags": the model is split into `pieces`, one launch per piece, each
       waiting for a per-piece flag (device-side) -- the previous design.
     sync="barrier": per-piece launches separated by NCCL barriers.
     """
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, pieces=8, sync="blocks", nslots=2, block=0,
-                 pull=False, consume=True, window=0, per_warp=False, oneshot=False):
+                 device=None, group=None, pieces=8, sync="blocks", nslots=2, block=0):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -410,14 +464,6 @@ class ChainShardedPHub:
             raise ValueError("sync must be 'blocks', 'flags' or 'barrier'")
         self.sync = sync
         self.block = int(block)          # 0: chosen from the model size below
-        self.pull = bool(pull) and sync == "blocks"
-        self.consume = bool(consume)
-        # back-pressure (blocks only): a producer runs at most `window` blocks ahead
-        self.window = int(window) if sync == "blocks" else 0
-        # per_warp: warps (not CTAs) take and signal blocks (block a multiple of 256)
-        self.per_warp = bool(per_warp) and sync == "blocks"
-        # oneshot: the last rank's fused launch is one CTA per 2048 elements
-        self.oneshot = bool(oneshot) and sync == "blocks" and not self.window
         self._epoch = 0
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
@@ -441,32 +487,23 @@ class ChainShardedPHub:
                        for key, p in self._own.items()}
         for t in self._grads.values():
             t.zero_()
-        # partial-sum buffers: push style -> an inbox on the consumer (rank > 0);
-        # pull style -> an outbox on the producer (rank < world - 1)
-        self._pin = capi.phub_alloc_shared(dev, 4 * Ep) if rank > 0 and not self.pull else None
-        self._pout = capi.phub_alloc_shared(dev, 4 * Ep) if not self.last and self.pull else None
+        # the incoming partial sum: an inbox on every rank > 0, stored into by rank - 1
+        self._pin = capi.phub_alloc_shared(dev, 4 * Ep) if rank > 0 else None
         self.pieces = chain_pieces(Ep, pieces)
         nflags = -(-Ep // self.block) if sync == "blocks" else len(self.pieces)
         # one uint32 "ready" flag per block (or piece), raised by the previous rank
         self._flags = capi.phub_alloc_shared(dev, 4 * nflags) if rank > 0 else None
         if self._flags:
             torch.as_tensor(_CudaArray(self._flags, nflags, self), device=f"cuda:{dev}").zero_()
-        # consumer-progress counter on every producer (rank < world - 1)
-        self._credit = capi.phub_alloc_shared(dev, 4) if self.window and not self.last else None
-        if self._credit:
-            torch.as_tensor(_CudaArray(self._credit, 1, self), device=f"cuda:{dev}").zero_()
-        self._nblk = -(-Ep // self.block)
         h = capi.phub_ipc_get_handle
         mine = (rank, h(dev, self._pin) if self._pin else None,
                 h(dev, self.hub.weights_ptr()),
-                h(dev, self._flags) if self._flags else None,
-                h(dev, self._pout) if self._pout else None,
-                h(dev, self._credit) if self._credit else None)
+                h(dev, self._flags) if self._flags else None)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         allh.sort(key=lambda x: x[0])
         self._opened = []
-        self._next_in = self._next_flags = self._prev_out = self._prev_credit = None
+        self._next_in = self._next_flags = None
 
         def open_(hd):
             p_ = capi.phub_ipc_open(dev, hd)
@@ -475,16 +512,11 @@ class ChainShardedPHub:
 
         err = None
         try:
-            if rank > 0 and self.window:
-                self._prev_credit = open_(allh[rank - 1][5])
             if not self.last:
-                if not self.pull:
-                    self._next_in = open_(allh[rank + 1][1])
+                self._next_in = open_(allh[rank + 1][1])
                 self._next_flags = open_(allh[rank + 1][3])
-            if rank > 0 and self.pull:
-                self._prev_out = open_(allh[rank - 1][4])
             if self.last:
-                reps = [open_(wh) for r, _pin, wh, _fl, _po, _cr in allh if r != rank]
+                reps = [open_(wh) for r, _pin, wh, _fl in allh if r != rank]
                 capi.phub_set_replicas(self.hub.ctx, reps)
         except capi.PhubError as ex:
             err = ex
@@ -498,8 +530,7 @@ class ChainShardedPHub:
                 except capi.PhubError:
                     pass
             self._grads = {}
-            for p_ in list(self._own.values()) + [x for x in (self._pin, self._pout, self._flags,
-                                                              self._credit) if x]:
+            for p_ in list(self._own.values()) + [x for x in (self._pin, self._flags) if x]:
                 capi.phub_free_shared(dev, p_)
             self.hub.close()
             raise PeerMappingError(f"peer mapping failed on some rank ({err or 'other rank'})")
@@ -515,25 +546,27 @@ class ChainShardedPHub:
     def gradients(self, slot: int = 0) -> dict:
         return {w: self._grads[(slot, w)] for w in self.hosted}
 
-    def barrier(self):
-        import torch.distributed as dist
-        dist.all_reduce(self._flag, group=self.group)
+    def _barriers_per_round(self):
+        return 2 if self.sync != "barrier" else len(self.pieces) + self.world - 1
 
     def exchange(self, slot: int = 0):
+        """One round: push -> aggregate + Nesterov -> replicas.  Raises
+        ExchangeFailed if this rank's context failed."""
+        self._round(lambda: self._exchange(slot))
+
+    def _exchange(self, slot):
         Ep = self.hub.E_padded
         hosted = self.hosted
-        # start barrier: the last rank's kernel stores w' into every other rank's
-        # replica, so every rank must be done reading its replica (e.g. the
-        # previous round's pull, enqueued after that round's end barrier) first
-        self.barrier()
-        upstream = self._prev_out if self.pull else self._pin     # partial of ranks 0..p-1
+        upstream = self._pin                                       # partial of ranks 0..p-1
+        if self.sync != "barrier":
+            # start barrier: the last rank's kernel stores w' into every other rank's
+            # replica, so every rank must be done reading its replica (e.g. the
+            # previous round's pull, enqueued after that round's end barrier) first
+            self.barrier()
         if self.last:
             w0 = 0
             if self.world > 1:
-                # the pushed-in partial is a transient inbox: the block kernel may
-                # drop it from L2 after reading (no HBM write-back, PHUB_CONSUME)
-                consume = self.sync == "blocks" and not self.pull and self.consume
-                self.hub.push(0, upstream, mode="consume" if consume else "borrow", n=Ep)
+                self.hub.push(0, upstream, mode="borrow", n=Ep)
                 w0 = 1
             for i, w in enumerate(hosted):
                 self.hub.push(w0 + i, self._own[(slot, w)], mode="borrow", n=Ep)
@@ -545,17 +578,11 @@ class ChainShardedPHub:
             self._epoch += 1
             ep = self._epoch
             wait = (self._flags, ep) if self._flags else None
-            credit = (self._credit, (ep - 1) * self._nblk, self.window) if self._credit else None
             if self.last:
-                capi.phub_aggregate_range(self.hub.ctx, 0, Ep, stream, wait=wait, block=self.block,
-                                          credit_return=self._prev_credit, per_warp=self.per_warp,
-                                          oneshot=self.oneshot and self.world > 1)
+                capi.phub_aggregate_range(self.hub.ctx, 0, Ep, stream, wait=wait, block=self.block)
             else:
-                dst = self._pout if self.pull else self._next_in
-                capi.phub_partial_sum(self.hub.ctx, srcs, dst, 0, Ep, stream, wait=wait,
-                                      signal=(self._next_flags, ep), block=self.block,
-                                      credit=credit, credit_return=self._prev_credit,
-                                      per_warp=self.per_warp)
+                capi.phub_partial_sum(self.hub.ctx, srcs, self._next_in, 0, Ep, stream, wait=wait,
+                                      signal=(self._next_flags, ep), block=self.block)
             self.barrier()                   # replicas complete; buffers free for the next round
             return
         if self.sync == "flags":
@@ -590,9 +617,6 @@ class ChainShardedPHub:
         for w in self.hosted:
             host_out[w].copy_(self.replica, non_blocking=True)
 
-    def sync_timeouts(self) -> int:
-        return capi.phub_sync_timeouts(self.hub.ctx)
-
     def weights(self):
         return self.replica
 
@@ -611,10 +635,6 @@ class ChainShardedPHub:
             capi.phub_free_shared(self.device, p)
         if self._pin:
             capi.phub_free_shared(self.device, self._pin)
-        if self._pout:
-            capi.phub_free_shared(self.device, self._pout)
-        if self._credit:
-            capi.phub_free_shared(self.device, self._credit)
         if self._flags:
             capi.phub_free_shared(self.device, self._flags)
         self._own = {}
@@ -639,7 +659,7 @@ def hier_nvlink_bytes(ranges, E_padded: int, rank: int):
     return out, inn
 
 
-class HierPHub:
+class HierPHub(_DeviceWaitExchange):
     """Hierarchical reduction across racks (PAPER.md
     P:746-763, emulated in P:1002-1012).
 
@@ -658,13 +678,14 @@ class HierPHub:
 
     def __init__(self, key_sizes, workers_per_rack=8, chunk_size_bytes=32768, lr=0.1,
                  momentum=0.9, device=None, group=None, block=32768, nslots=2,
-                 worker_order=False, double_replica=False):
+                 worker_order=False):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
         self.group = group
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         self.R, self.rack, self.P = world, rank, int(workers_per_rack)
+        self.rank = rank
         self.block = int(block)
         # worker_order: the flat worker-order sum of one job's R x P workers (raw
         # slices pushed to the owners) instead of the rack-grouped sum
@@ -690,15 +711,9 @@ class HierPHub:
         nblk = max(1, -(-L // self.block))
         self._flags = capi.phub_alloc_shared(dev, 4 * nblk * world)
         torch.as_tensor(_CudaArray(self._flags, nblk * world, self), device=f"cuda:{dev}").zero_()
-        # double_replica: a second replica buffer; round k stores w' into slot k % 2
-        # (slot 0 = the context's w), so a pull of round k may overlap round k+1
-        self.double_replica = bool(double_replica)
-        self._r1 = capi.phub_alloc_shared(dev, 4 * Ep) if self.double_replica else None
-        self._r1_t = (torch.as_tensor(_CudaArray(self._r1, Ep, self), device=f"cuda:{dev}")
-                      if self._r1 else None)
         h = capi.phub_ipc_get_handle
         mine = (rank, b, e, h(dev, self._inbox), h(dev, self._flags),
-                h(dev, self.hub.weights_ptr()), h(dev, self._r1) if self._r1 else None)
+                h(dev, self.hub.weights_ptr()))
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         allh.sort(key=lambda x: x[0])
@@ -706,19 +721,16 @@ class HierPHub:
         self.inbox = [[0] * world for _ in range(2)]
         self.peer_inbox = [[0] * world for _ in range(2)]
         self.peer_flags = [0] * world
-        reps, reps1 = [], []
+        reps = []
         err = None
         try:
-            for o, ob, oe, ih, fh, wh, r1h in allh:
+            for o, ob, oe, ih, fh, wh in allh:
                 if o == rank:
                     continue
                 for hd in (ih, fh, wh):
                     self._opened.append(capi.phub_ipc_open(dev, hd))
                 pin, pfl, pw = self._opened[-3:]
                 reps.append(pw)
-                if r1h is not None:
-                    self._opened.append(capi.phub_ipc_open(dev, r1h))
-                    reps1.append(self._opened[-1])
                 self.peer_flags[o] = pfl
                 for sl in range(2):
                     # padded-based: ptr + 4x addresses element x of o's range in o's slot for us
@@ -728,9 +740,6 @@ class HierPHub:
             capi.phub_set_replicas(self.hub.ctx, reps)
         except capi.PhubError as ex:
             err = ex
-        # slot 1 replicas: the peers' second buffers plus this rank's own (its
-        # owned range; slot 0's own copy is the context's w, always written)
-        self._reps = (reps, reps1 + ([self._r1] if self._r1 else []))
         # every rank must agree before anyone relies on peer mappings
         ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=f"cuda:{dev}")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
@@ -741,22 +750,15 @@ class HierPHub:
                 except capi.PhubError:
                     pass
             self._grads = {}
-            self._r1_t = None
-            for p_ in list(self._own.values()) + [self._inbox, self._flags] + \
-                    ([self._r1] if self._r1 else []):
+            for p_ in list(self._own.values()) + [self._inbox, self._flags]:
                 capi.phub_free_shared(dev, p_)
             self.hub.close()
             raise PeerMappingError(f"peer mapping failed on some rank ({err or 'other rank'})")
         self.epoch = 0
         self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
-        self._w0 = self.hub.weights()
+        self.replica = self.hub.weights()      # this rank's full replica (padded layout)
         torch.cuda.synchronize(dev)
         dist.barrier(group=group)
-
-    @property
-    def replica(self):
-        """This rank's full replica of the weights of the latest round."""
-        return self._r1_t if self.double_replica and self.epoch % 2 == 1 else self._w0
 
     @property
     def num_workers(self):
@@ -779,11 +781,12 @@ class HierPHub:
         """This rack's gradient buffers (padded layout), keyed by local worker index."""
         return {k: self._grads[(slot, k)] for k in range(self.P)}
 
-    def barrier(self):
-        import torch.distributed as dist
-        dist.all_reduce(self._flag, group=self.group)
-
     def exchange(self, slot: int = 0):
+        """One round in one launch per GPU.  Raises ExchangeFailed if this rank's
+        context failed."""
+        self._round(lambda: self._exchange(slot))
+
+    def _exchange(self, slot):
         Ep = self.hub.E_padded
         # start barrier: this round's kernels store w' into every rank's replica,
         # so every rank must be done reading its replica from the previous round
@@ -793,15 +796,10 @@ class HierPHub:
             self.hub.push(k, self._own[(slot, k)], mode="borrow", n=Ep)
         self.epoch += 1
         par = self.epoch % 2
-        if self.double_replica:
-            capi.phub_set_replicas(self.hub.ctx, self._reps[par])
         capi.phub_hier_exchange(self.hub.ctx, self.R, self.block, self.inbox[par],
                                 self.peer_inbox[par], self._flags, self.peer_flags, self.epoch,
                                 self.hub._stream(None), worker_order=self.worker_order)
         self.barrier()                       # every rack's w' stores into this replica are done
-
-    def sync_timeouts(self) -> int:
-        return capi.phub_sync_timeouts(self.hub.ctx)
 
     def weights(self):
         return self.replica
@@ -816,11 +814,8 @@ class HierPHub:
             capi.phub_ipc_close(self.device, p)
         dist.barrier(group=self.group)
         self._grads = {}
-        self._r1_t = None
         for p in self._own.values():
             capi.phub_free_shared(self.device, p)
-        if self._r1:
-            capi.phub_free_shared(self.device, self._r1)
         capi.phub_free_shared(self.device, self._inbox)
         capi.phub_free_shared(self.device, self._flags)
         self._own = {}
@@ -839,7 +834,7 @@ class PushShardedPHub(HierPHub):
     P2PShardedPHub (gradients() keyed by global worker id)."""
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, block=12288, nslots=2, double_replica=False):
+                 device=None, group=None, block=12288, nslots=2):
         import torch.distributed as dist
         world = dist.get_world_size(group)
         if num_workers % world:
@@ -847,7 +842,7 @@ class PushShardedPHub(HierPHub):
         super().__init__(key_sizes, workers_per_rack=num_workers // world,
                          chunk_size_bytes=chunk_size_bytes, lr=lr, momentum=momentum,
                          device=device, group=group, block=block, nslots=nslots,
-                         worker_order=True, double_replica=double_replica)
+                         worker_order=True)
         self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, self.rack, world)
 
     @property

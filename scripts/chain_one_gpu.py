@@ -51,7 +51,7 @@ def main():
         capi.phub_partial_sum(head.ctx, [x.data_ptr() for x in g[:4]], part.data_ptr(), 0, Ep,
                               st.cuda_stream, signal=(flags.data_ptr(), r), block=args.block)
         e1.record(st)
-        tail.push(0, part, mode="consume")
+        tail.push(0, part)
         for k in range(4):
             tail.push(1 + k, g[4 + k])
         capi.phub_aggregate_range(tail.ctx, 0, Ep, st.cuda_stream, wait=(flags.data_ptr(), r),

@@ -24,7 +24,7 @@ import oracle  # noqa: E402
 from paper_1805_07891_b200.sharded import (  # noqa: E402
     ChainShardedPHub, P2PShardedPHub, PushShardedPHub)
 from workloads import grad_stream, manifest  # noqa: E402
-from workloads.generate import values_at_np, values_torch  # noqa: E402
+from workloads.generate import fullmant_at_np, fullmant_np, fullmant_torch  # noqa: E402
 
 
 def sample(sizes, E, ranges, block, rng):
@@ -56,25 +56,25 @@ def main():
     sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
     hub = sh.hub
     idx = torch.as_tensor(hub.padded_index(), device=dev)
-    hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
+    hub.load_state(fullmant_torch(1, 0, E, dev), fullmant_torch(2, 0, E, dev))
     for r in range(rounds):
         g = sh.gradients(slot=r % 2)
         for w in sh.hosted:
             g[w].fill_(float("nan"))
-            g[w][idx] = values_torch(grad_stream(w) + 37 * r, 0, E, 25, dev)
+            g[w][idx] = fullmant_torch(grad_stream(w) + 37 * r, 0, E, dev)
         sh.exchange(slot=r % 2)
     torch.cuda.synchronize()
     rng = np.random.default_rng(7 + rank)
     samp = sample(sizes, E, None, None, rng)
     got = sh.weights()[idx[torch.as_tensor(samp, device=dev)]].cpu().numpy()
-    w_ref = values_at_np(1, samp, 20)
-    v_ref = values_at_np(2, samp, 25)
+    w_ref = fullmant_at_np(1, samp)
+    v_ref = fullmant_at_np(2, samp)
     for r in range(rounds):
-        gs = np.stack([values_at_np(grad_stream(w) + 37 * r, samp, 25) for w in range(N)])
+        gs = np.stack([fullmant_at_np(grad_stream(w) + 37 * r, samp) for w in range(N)])
         w_ref, v_ref, _ = oracle.elems(gs, w_ref, v_ref, 0.1, 0.9)
+    if mode in ("chain", "push"):
+        sh.check()                   # collective: raises on every rank if a device wait expired
     ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
-    if mode in ("chain", "push") and sh.sync_timeouts() != 0:
-        ok = False
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)

@@ -19,8 +19,8 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
 from paper_1805_07891_b200.sharded import HierPHub  # noqa: E402
-from workloads import grad_stream, manifest, values_np  # noqa: E402
-from workloads.generate import values_at_np, values_torch  # noqa: E402
+from workloads import grad_stream, manifest  # noqa: E402
+from workloads.generate import fullmant_at_np, fullmant_np, fullmant_torch  # noqa: E402
 
 SPECIAL = {"small": [3, 3, 9408, 64, 64, 4096, 20000, 1000, 7], "one": [5]}
 SAMPLED = ("vgg19", "alexnet", "resnet269")
@@ -39,7 +39,7 @@ def main():
     sh = HierPHub(sizes, workers_per_rack=P, chunk_size_bytes=cb, device=local, block=block)
     hub = sh.hub
     idx = torch.as_tensor(hub.padded_index(), device=dev)
-    hub.load_state(values_torch(1, 0, E, 20, dev), values_torch(2, 0, E, 25, dev))
+    hub.load_state(fullmant_torch(1, 0, E, dev), fullmant_torch(2, 0, E, dev))
 
     def stream(r, k, rnd):                     # worker k of rack r, round rnd
         return grad_stream(r * P + k) + 37 * rnd
@@ -48,7 +48,7 @@ def main():
         g = sh.gradients(slot=rnd % 2)
         for k in range(P):
             g[k].fill_(float("nan"))
-            g[k][idx] = values_torch(stream(rack, k, rnd), 0, E, 25, dev)
+            g[k][idx] = fullmant_torch(stream(rack, k, rnd), 0, E, dev)
         sh.exchange(slot=rnd % 2)
     torch.cuda.synchronize()
     if name in SAMPLED:
@@ -57,19 +57,27 @@ def main():
         samp = np.unique(np.concatenate([rng.integers(0, E, 20000), starts[:-1],
                                          starts[1:] - 1])).astype(np.int64)
         got = sh.weights()[idx[torch.as_tensor(samp, device=dev)]].cpu().numpy()
-        w_ref, v_ref = values_at_np(1, samp, 20), values_at_np(2, samp, 25)
+        w_ref, v_ref = fullmant_at_np(1, samp), fullmant_at_np(2, samp)
         for rnd in range(rounds):
-            gs = np.stack([np.stack([values_at_np(stream(r, k, rnd), samp, 25) for k in range(P)])
+            gs = np.stack([np.stack([fullmant_at_np(stream(r, k, rnd), samp) for k in range(P)])
                            for r in range(R)])
             w_ref, v_ref, _ = oracle.hier_elems(gs, w_ref, v_ref, 0.1, 0.9)
     else:
         got = sh.weights()[idx].cpu().numpy()
-        w_ref, v_ref = values_np(1, 0, E, 20), values_np(2, 0, E, 25)
+        w_ref, v_ref = fullmant_np(1, 0, E), fullmant_np(2, 0, E)
+        w_flat, v_flat = w_ref, v_ref
         for rnd in range(rounds):
-            racks = [[values_np(stream(r, k, rnd), 0, E, 25) for k in range(P)] for r in range(R)]
+            racks = [[fullmant_np(stream(r, k, rnd), 0, E) for k in range(P)] for r in range(R)]
             w_ref, v_ref, _ = oracle.hier_round(sizes, racks, w_ref, v_ref, 0.1, 0.9,
                                                 chunk_bytes=cb)
-    ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32)) and sh.sync_timeouts() == 0
+            w_flat, v_flat, _ = oracle.round_(sizes, [g for rk in racks for g in rk], w_flat,
+                                              v_flat, 0.1, 0.9, chunk_bytes=cb)
+        if P > 1 and E > 100:        # rack grouping must be visible (else parity proves nothing)
+            diff = int(np.sum(got.view(np.uint32) != w_flat.view(np.uint32)))
+            print(f"rank {rack}: hierarchical differs from the flat worker order on {diff}/{E}")
+            assert diff > 0
+    sh.check()                       # collective: raises on every rank if a device wait expired
+    ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))
     flag = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(flag)

@@ -9,8 +9,8 @@ from conftest import ROOT
 
 def test_reference_arm_json_line():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                        "--config", "tiny", "--steps", "1", "--warmup", "1",
-                        "--cpu-seconds", "0.5"], capture_output=True, text=True, timeout=300,
+                        "--config", "tiny", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=300,
                        cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
@@ -23,6 +23,7 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["value"] > 0
+    assert d["config"]["E"] == 288768 and "full" in d["cpu_baseline"]["sample"]   # no sampling
 
 
 def test_reference_arm_nonzero_rank_is_silent():

@@ -1,0 +1,207 @@
+"""Summation order on the GPU (-m gpu): the kernels sum the workers in
+worker-id order, and the parity inputs can tell.  VERDICT r1 "next" #1.
+
+* Adversarial worker-order case (R3): workers pushing
+  1, 2^-24, 2^-24 give ((+0 + 1) + 2^-24) + 2^-24 = 1 in worker order (ties
+  to even twice) but 1 + 2^-23 in reverse order.  Checked through every kernel
+  (k_flat 256/128-bit, k_tiles, k_bulk, k_wide, the k_blocks chain), with the
+  reversed push as the control that must give the other value.
+* Negative controls on full-mantissa inputs: a reversed-worker push and a
+  collective-style (pairwise tree / torch) sum must FAIL bit-exactness
+  against the oracle -- proving a wrong order cannot pass the parity tests.
+* Cache policy (NEXT-2): the cache-bypass instantiations of
+  the flat kernel are bit-exact too (a policy changes placement, not values).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import grad_stream, manifest
+from workloads.generate import fullmant_np
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+f32 = np.float32
+DEV = "cuda:0"
+E24 = float(2.0 ** -24)
+ONE = 0x3F800000
+ONE_PLUS = 0x3F800001          # 1 + 2^-23
+
+
+def bits(a):
+    return np.asarray(a, dtype=f32).view(np.uint32)
+
+
+def _hub(sizes, N, **kw):
+    from paper_1805_07891_b200 import PHub
+    return PHub(sizes, N, device=0, **kw)
+
+
+def _adversarial(hub, order):
+    """Padded device buffers: every real element of worker order[k] holds the
+    k-th value of (1, 2^-24, 2^-24)."""
+    vals = [1.0, E24, E24]
+    idx = torch.as_tensor(hub.padded_index(), device=DEV)
+    bufs = [None] * 3
+    for k, w in enumerate(order):
+        b = torch.zeros(hub.E_padded, device=DEV)
+        b[idx] = vals[k]
+        bufs[w] = b
+    return bufs
+
+
+SIZES = [5, 4096, 1000, 70000]          # short keys, a ragged tail, several tiles
+
+
+@pytest.mark.parametrize("kernel", ["FLAT", "FLAT128", "TILES", "BULK", "WIDE"])
+def test_worker_order_adversarial_every_kernel(kernel):
+    from paper_1805_07891_b200 import capi
+    for order, want in (((0, 1, 2), ONE), ((2, 1, 0), ONE_PLUS)):
+        hub = _hub(SIZES, 3, keep_aggregate=True, lr=0.0, momentum=0.0)
+        hub.set_option(capi.PHUB_OPT_KERNEL, getattr(capi, f"PHUB_KERNEL_{kernel}"))
+        bufs = _adversarial(hub, order)       # order (2,1,0): worker 0 holds 2^-24 ...
+        for w, b in enumerate(bufs):
+            hub.push(w, b)
+        hub.aggregate_optimize()
+        _, _, s = hub.read_state()
+        assert np.all(bits(s) == want), (kernel, order, np.unique(bits(s)))
+        hub.close()
+    # the oracle agrees on both (its own pin is tests/test_oracle_round.py::test_worker_order)
+    g = [np.full(1, v, f32) for v in (1.0, E24, E24)]
+    _, _, s = oracle.round_([1], g, np.zeros(1, f32), np.zeros(1, f32), 0.0, 0.0)
+    assert bits(s)[0] == ONE
+
+
+def test_worker_order_adversarial_block_chain():
+    """k_blocks: the producer sums worker 0 (= 1) into the partial; the consumer
+    adds workers 1, 2 (2^-24 each) in order -> 1.  Starting the chain with the
+    small workers instead gives 1 + 2^-23."""
+    from paper_1805_07891_b200 import PHub, capi
+    for first, rest, want in (((1.0,), (E24, E24), ONE), ((E24, E24), (1.0,), ONE_PLUS)):
+        head = _hub(SIZES, len(first))
+        Ep = head.E_padded
+        idx = torch.as_tensor(head.padded_index(), device=DEV)
+
+        def buf(v):
+            b = torch.zeros(Ep, device=DEV)
+            b[idx] = v
+            return b
+
+        src = [buf(v) for v in first]
+        part = torch.empty(Ep, device=DEV)
+        nblk = -(-Ep // 2048)
+        flags = torch.zeros(nblk, dtype=torch.int32, device=DEV)
+        st = head._stream(None)
+        capi.phub_partial_sum(head.ctx, [b.data_ptr() for b in src], part.data_ptr(), 0, Ep, st,
+                              signal=(flags.data_ptr(), 1), block=2048)
+        tail = PHub(SIZES, 1 + len(rest), device=0, lr=0.0, momentum=0.0, keep_aggregate=True)
+        tail.push(0, part)
+        rb = [buf(v) for v in rest]
+        for k, b in enumerate(rb):
+            tail.push(1 + k, b)
+        capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 1), block=2048)
+        _, _, s = tail.read_state()
+        assert np.all(bits(s) == want)
+        assert capi.phub_sync_timeouts(tail.ctx) == 0
+        head.close()
+        tail.close()
+
+
+def _full(hub, N, seed):
+    from workloads.generate import fullmant_torch
+    idx = torch.as_tensor(hub.padded_index(), device=DEV)
+    out = []
+    for w in range(N):
+        b = torch.zeros(hub.E_padded, device=DEV)
+        b[idx] = fullmant_torch(grad_stream(w) + 37 * seed, 0, hub.E, DEV)
+        out.append(b)
+    return out
+
+
+def _mismatch(got, ref):
+    return float(np.mean(bits(got) != bits(ref)))
+
+
+@pytest.mark.parametrize("N", [3, 8])
+def test_negative_control_reversed_push_fails_parity(N):
+    """Pushing the workers in reverse order is a different (valid) sum: the
+    kernel reproduces the REVERSED oracle bit for bit and fails the
+    worker-order oracle on many elements."""
+    sizes = manifest("tiny")
+    hub = _hub(sizes, N, keep_aggregate=True)
+    E = hub.E
+    w0, v0 = fullmant_np(1 + 37 * 50, 0, E), fullmant_np(2 + 37 * 50, 0, E)
+    hub.load_state(w0, v0)
+    gd = _full(hub, N, 50)
+    for w in range(N):
+        hub.push(w, gd[N - 1 - w])
+    hub.aggregate_optimize()
+    w, v, s = hub.read_state()
+    hg = [fullmant_np(grad_stream(k) + 37 * 50, 0, E) for k in range(N)]
+    rw, rv, rs = oracle.round_(sizes, hg, w0, v0, 0.1, 0.9)
+    assert _mismatch(s, rs) > (0.15 if N < 8 else 0.25)
+    assert _mismatch(w, rw) > 0.05
+    ow, ov, os_ = oracle.round_(sizes, hg[::-1], w0, v0, 0.1, 0.9)
+    assert np.array_equal(bits(s), bits(os_)) and np.array_equal(bits(w), bits(ow))
+    hub.close()
+
+
+def test_negative_control_collective_order_fails_parity():
+    """Collective-style reductions -- a pairwise tree (tree all-reduce /
+    in-switch reduction shape) and a rotated ring order (a ring all-reduce's
+    chunk on rank r starts at rank r+1) -- followed by the same Nesterov step
+    are within rounding of the oracle but NOT bit-exact (AllReduceBaseline is
+    the multi-GPU instance, tests/test_gpu_multi.py)."""
+    sizes = manifest("tiny")
+    N = 8
+    probe = _hub(sizes, 1)
+    E = probe.E
+    w0, v0 = fullmant_np(1 + 37 * 51, 0, E), fullmant_np(2 + 37 * 51, 0, E)
+    gd = _full(probe, N, 51)
+    xs = list(gd)
+    while len(xs) > 1:
+        xs = [xs[i] + xs[i + 1] for i in range(0, len(xs), 2)]
+    tree = xs[0]
+    ring = torch.zeros_like(gd[0])
+    for k in list(range(1, N)) + [0]:
+        ring = ring + gd[k]
+    hg = [fullmant_np(grad_stream(k) + 37 * 51, 0, E) for k in range(N)]
+    _, _, rs = oracle.round_(sizes, hg, w0, v0, 0.1, 0.9)
+    for agg in (tree, ring):
+        hub = _hub(sizes, 1, rescale=1.0 / N, keep_aggregate=True)
+        hub.load_state(w0, v0)
+        hub.push(0, agg)
+        hub.aggregate_optimize()
+        _, _, s = hub.read_state()
+        assert _mismatch(s, rs) > 0.1
+        rel = np.abs(s.astype(np.float64) - rs) / np.maximum(np.abs(rs.astype(np.float64)), 1e-30)
+        assert np.median(rel) < 1e-6                      # "within rounding", not exact
+        hub.close()
+    probe.close()
+
+
+@pytest.mark.parametrize("kernel", ["FLAT", "FLAT128"])
+@pytest.mark.parametrize("N", [3, 8])
+def test_cache_bypass_bit_exact(kernel, N):
+    """PHUB_CACHE_BYPASS (every stream evict-first: the paper's cache-bypassed
+    Opt/Agg) computes the same bits as the cache-enabled default."""
+    from paper_1805_07891_b200 import capi
+    sizes = [3, 4096, 9408, 20000, 262144, 7]
+    hub = _hub(sizes, N, keep_aggregate=True)
+    hub.set_option(capi.PHUB_OPT_KERNEL, getattr(capi, f"PHUB_KERNEL_{kernel}"))
+    hub.set_option(capi.PHUB_OPT_CACHE, capi.PHUB_CACHE_BYPASS)
+    E = hub.E
+    w0, v0 = fullmant_np(1 + 37 * 52, 0, E), fullmant_np(2 + 37 * 52, 0, E)
+    hub.load_state(w0, v0)
+    for r in range(2):
+        gd = _full(hub, N, 52 + r)
+        for w in range(N):
+            hub.push(w, gd[w])
+        hub.aggregate_optimize()
+        hg = [fullmant_np(grad_stream(k) + 37 * (52 + r), 0, E) for k in range(N)]
+        w0, v0, rs = oracle.round_(sizes, hg, w0, v0, 0.1, 0.9)
+    w, v, s = hub.read_state()
+    assert np.array_equal(bits(s), bits(rs))
+    assert np.array_equal(bits(w), bits(w0)) and np.array_equal(bits(v), bits(v0))
+    hub.close()

@@ -1,10 +1,14 @@
 """GPU parity: the sm_100a path vs the CPU oracle, through the C ABI (-m gpu).
 
 Inputs are generated independently on each side from the same seeded
-counter-based streams (workloads.generate): on the device by values_torch into
-the padded layout (padding filled with NaN so any read of padding would show),
-on the host by values_np for the oracle.  Nothing the CUDA path writes is ever
-fed to the oracle.
+counter-based streams (workloads.generate): on the device by fullmant_torch
+into the padded layout (padding filled with NaN so any read of padding would
+show), on the host by fullmant_np for the oracle.  Nothing the CUDA path
+writes is ever fed to the oracle.  The values are FULL-MANTISSA (random 24-bit
+significands over 31 binades, both signs), so summing the workers in any
+order other than worker-id order changes most results (tests/test_generate.py
+pins that, tests/test_gpu_order.py shows the kernels fail it when the order
+is wrong): bit-exactness here is evidence of the worker-order sum itself.
 
 Bar (BASELINE.json north_star): chunk table and the worker-order sum
 bit-exact; w' and v' within 1e-6 relative -- this build asserts bit-exact for
@@ -16,7 +20,7 @@ import pytest
 
 import oracle
 from workloads import manifest, values_np, grad_stream
-from workloads.generate import values_at_np
+from workloads.generate import fullmant_at_np, fullmant_np
 from conftest import read_golden
 
 torch = pytest.importorskip("torch")
@@ -49,24 +53,25 @@ def _pad_index(hub):
     return torch.as_tensor(hub.padded_index(), device=DEV)
 
 
-def device_grads(hub, N, seed=0, shift=25):
-    """N padded device buffers with stream values at real elements, NaN in padding."""
-    from workloads.generate import values_torch
+def device_grads(hub, N, seed=0):
+    """N padded device buffers with full-mantissa stream values at real
+    elements, NaN in padding."""
+    from workloads.generate import fullmant_torch
     idx = _pad_index(hub)
     out = []
     for w in range(N):
         buf = torch.full((hub.E_padded,), float("nan"), dtype=torch.float32, device=DEV)
-        buf[idx] = values_torch(grad_stream(w) + 37 * seed, 0, hub.E, shift, DEV)
+        buf[idx] = fullmant_torch(grad_stream(w) + 37 * seed, 0, hub.E, DEV)
         out.append(buf)
     return out
 
 
-def host_grads(E, N, seed=0, shift=25):
-    return [values_np(grad_stream(w) + 37 * seed, 0, E, shift) for w in range(N)]
+def host_grads(E, N, seed=0):
+    return [fullmant_np(grad_stream(w) + 37 * seed, 0, E) for w in range(N)]
 
 
 def host_state(E, seed=0):
-    return values_np(1 + 37 * seed, 0, E, 20), values_np(2 + 37 * seed, 0, E, 25)
+    return fullmant_np(1 + 37 * seed, 0, E), fullmant_np(2 + 37 * seed, 0, E)
 
 
 def run_round(hub, grads_dev, mode="borrow"):
@@ -221,7 +226,7 @@ def test_errors_leave_state_unchanged():
 
 def test_pull_semantics():
     sizes = SMALL
-    init = values_np(5, 0, sum(sizes), 20)
+    init = fullmant_np(5, 0, sum(sizes))
     hub = _hub(sizes, 3, init_weights=init)
     starts = np.concatenate([[0], np.cumsum(sizes)])
     dst = np.empty(sizes[2], f32)
@@ -391,19 +396,19 @@ def _sample_indices(sizes, chunk_bytes, rng, n_random=20000):
     *[("resnet269", 8, 4096 << i) for i in range(9)],        # BJ configs[4] sweep
 ])
 def test_full_size_sampled(name, N, cb):
-    from workloads.generate import values_torch
+    from workloads.generate import fullmant_torch
     sizes = manifest(name)
     hub = _hub(sizes, N, chunk_size_bytes=cb)                # bench launch config (AUTO)
     E = hub.E
     idx_pad = _pad_index(hub)
-    w0 = values_torch(1, 0, E, 20, DEV)
-    v0 = values_torch(2, 0, E, 25, DEV)
+    w0 = fullmant_torch(1, 0, E, DEV)
+    v0 = fullmant_torch(2, 0, E, DEV)
     hub.load_state(w0, v0)
     del w0, v0
     gd = []
     for w in range(N):
         b = torch.full((hub.E_padded,), float("nan"), device=DEV)
-        b[idx_pad] = values_torch(grad_stream(w), 0, E, 25, DEV)
+        b[idx_pad] = fullmant_torch(grad_stream(w), 0, E, DEV)
         gd.append(b)
     run_round(hub, gd)
     del gd
@@ -411,8 +416,8 @@ def test_full_size_sampled(name, N, cb):
     samp = _sample_indices(sizes, cb, rng)
     w_all, v_all, _ = hub.read_state()
     # oracle on independently generated inputs at the sampled elements
-    g = np.stack([values_at_np(grad_stream(w), samp, 25) for w in range(N)])
-    rw, rv, _ = oracle.elems(g, values_at_np(1, samp, 20), values_at_np(2, samp, 25), 0.1, 0.9)
+    g = np.stack([fullmant_at_np(grad_stream(w), samp) for w in range(N)])
+    rw, rv, _ = oracle.elems(g, fullmant_at_np(1, samp), fullmant_at_np(2, samp), 0.1, 0.9)
     assert_bits_equal(w_all[samp], rw, f"{name}@{cb} sampled w'")
     assert_bits_equal(v_all[samp], rv, f"{name}@{cb} sampled v'")
     hub.close()
@@ -661,26 +666,45 @@ def test_stage_flags_signal_and_bounded_wait():
     w, _, _ = tail.read_state()
     rw, _, _ = oracle.round_(sizes, host_grads(E, 4, 9), w0, v0, 0.1, 0.9)
     assert_bits_equal(w, rw, "flag-ordered chain on one GPU")
-    # a flag that is never raised: the wait expires (~2 s), the work is skipped
+    # a flag that is never raised: the wait expires (~2 s), the work is skipped, and
+    # the context turns sticky-failed: the NEXT call reports it, never a stale w'
     for k in range(3):
         tail.push(k, gd[k])
     capi.phub_aggregate_range(tail.ctx, 0, tail.E_padded, st, wait=(flags.data_ptr() + 4, 1))
     torch.cuda.synchronize()
     assert capi.phub_sync_timeouts(tail.ctx) >= 1
+    assert_sticky_timeout(tail, gd)
     head.close()
     tail.close()
 
 
-@pytest.mark.parametrize("block,mode,per_warp,oneshot", [
-    (2048, "borrow", False, False), (32768, "borrow", False, False),
-    (16384, "consume", False, False), (768, "borrow", True, False), (4096, "consume", True, False),
-    (12288, "borrow", False, True), (2048, "consume", False, True)])
-def test_block_streaming_flags_chain_on_one_gpu(block, mode, per_warp, oneshot):
+def assert_sticky_timeout(hub, gd):
+    """After an expired device wait every data call on the context fails with
+    PHUB_ERR_SYNC_TIMEOUT (header conventions; VERDICT r1 #3)."""
+    from paper_1805_07891_b200 import PhubError, capi
+
+    def status(fn):
+        with pytest.raises(PhubError) as e:
+            fn()
+        return capi.STATUS_NAMES[e.value.status]
+
+    assert capi.STATUS_NAMES[capi.phub_check(hub.ctx)] == "PHUB_ERR_SYNC_TIMEOUT"
+    assert status(lambda: hub.push(0, gd[0])) == "PHUB_ERR_SYNC_TIMEOUT"
+    assert status(lambda: hub.read_state()) == "PHUB_ERR_SYNC_TIMEOUT"
+    assert status(lambda: hub.pull(torch.empty(hub.E_padded, device=DEV))) == \
+        "PHUB_ERR_SYNC_TIMEOUT"
+    assert status(lambda: hub.weights_ptr()) == "PHUB_ERR_SYNC_TIMEOUT"
+    assert status(lambda: hub.synchronize()) == "PHUB_ERR_SYNC_TIMEOUT"
+
+
+@pytest.mark.parametrize("block", [2048, 12288, 16384, 32768])
+def test_block_streaming_flags_chain_on_one_gpu(block):
     """phub_sync block form: a partial sum raises one flag per block and a
     range aggregate waits on them block by block (same stream here: the
-    producer finishes first, so no kernel waits on a co-resident one) --
-    bit-identical to the 6-worker oracle round; every flag raised exactly
-    to the epoch; a bad block size is refused; an unraised flag times out."""
+    producer finishes first; tests/test_gpu_emulated_ranks.py runs them
+    concurrently) -- bit-identical to the 6-worker oracle round; every flag
+    raised exactly to the epoch; a bad block size is refused; an unraised
+    flag times out and makes the context sticky-failed."""
     from paper_1805_07891_b200 import PHub, PhubError, capi
     sizes = manifest("resnet50")
     E = sum(sizes)
@@ -694,16 +718,15 @@ def test_block_streaming_flags_chain_on_one_gpu(block, mode, per_warp, oneshot):
     st = head._stream(None)
     with pytest.raises(PhubError):
         capi.phub_partial_sum(head.ctx, [g.data_ptr() for g in gd[:3]], part.data_ptr(), 0, Ep,
-                              st, signal=(flags.data_ptr(), 3), block=1000, per_warp=per_warp)
+                              st, signal=(flags.data_ptr(), 3), block=1000)
     capi.phub_partial_sum(head.ctx, [g.data_ptr() for g in gd[:3]], part.data_ptr(), 0, Ep, st,
-                          signal=(flags.data_ptr(), 3), block=block, per_warp=per_warp)
+                          signal=(flags.data_ptr(), 3), block=block)
     tail = PHub(sizes, 4, device=0, rescale=1.0 / 6, keep_aggregate=True)
     tail.load_state(w0, v0)
-    tail.push(0, part, mode=mode)          # consume: its L2 lines may be discarded after reading
+    tail.push(0, part)
     for k in range(3):
         tail.push(1 + k, gd[3 + k])
-    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 3), block=block,
-                              per_warp=per_warp, oneshot=oneshot)
+    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 3), block=block)
     torch.cuda.synchronize()
     assert tail.iteration == 1
     f = flags.cpu().numpy()
@@ -717,32 +740,22 @@ def test_block_streaming_flags_chain_on_one_gpu(block, mode, per_warp, oneshot):
     # flags never raised for epoch 4: the waits expire once (~2 s), the work is skipped
     for k in range(4):
         tail.push(k, gd[k])
-    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 4), block=block,
-                              per_warp=per_warp, oneshot=oneshot)
+    capi.phub_aggregate_range(tail.ctx, 0, Ep, st, wait=(flags.data_ptr(), 4), block=block)
     torch.cuda.synchronize()
     assert capi.phub_sync_timeouts(tail.ctx) >= 1
+    assert_sticky_timeout(tail, gd)
     head.close()
     tail.close()
 
 
-def test_consume_push_outside_block_streaming_is_a_borrow():
-    """PHUB_CONSUME on the flat (non-block) kernel reads like PHUB_BORROW and
-    leaves the buffer intact; per-key CONSUME pushes are plain borrows."""
-    hub = _hub(SMALL, 3, keep_aggregate=True)
-    w0, v0 = host_state(hub.E, 13)
-    hub.load_state(w0, v0)
-    gd = device_grads(hub, 3, 13)
-    keep = gd[0].clone()
-    hub.push(0, gd[0], mode="consume")
-    for w in (1, 2):
-        hub.push(w, gd[w], mode="consume" if w == 1 else "borrow")
-    hub.aggregate_optimize()
-    torch.cuda.synchronize()
-    w, v, s = hub.read_state()
-    rw, rv, rs = oracle.round_(SMALL, host_grads(hub.E, 3, 13), w0, v0, 0.1, 0.9)
-    assert_bits_equal(s, rs, "consume (flat) aggregate")
-    assert_bits_equal(w, rw, "consume (flat) w")
-    assert torch.equal(gd[0].nan_to_num(7.0), keep.nan_to_num(7.0))
+def test_removed_push_mode_is_refused():
+    """Round 2 removed PHUB_CONSUME (mode 2): it is an invalid mode now."""
+    from paper_1805_07891_b200 import PhubError, capi
+    hub = _hub(SMALL, 2)
+    gd = device_grads(hub, 1)
+    with pytest.raises(PhubError) as e:
+        capi.phub_push(hub.ctx, 0, capi.PHUB_ALL_KEYS, gd[0].data_ptr(), hub.E_padded, 2, 0)
+    assert capi.STATUS_NAMES[e.value.status] == "PHUB_ERR_INVALID_ARGUMENT"
     hub.close()
 
 

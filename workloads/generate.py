@@ -16,6 +16,20 @@ bit for bit):
 The std of (isum - 131070) is ~2**15.21, so ``shift=25`` gives gradients with
 std ~2**-10 (SURVEY.md 8(d) "g ~ 2^-10 N(0,1)"), ``shift=20`` weights with
 std ~0.036.
+
+Those values carry at most 17 significant bits at one fixed scale, so any sum
+of <= 128 of them is exact in fp32 in ANY order: they cannot tell a
+worker-order sum from a reversed or tree-ordered one.  The parity tests
+therefore use the *full-mantissa* recipe (``fullmant_*``), built bit by bit:
+
+    bits  = sign << 31 | (127 - e) << 23 | mantissa23
+    sign  = bit 63 of z,  e = (z >> 23) % 31,  mantissa23 = z & 0x7FFFFF
+
+i.e. a random 24-bit significand with a random binade 2^-e, e in [0, 30]
+(magnitudes in [2^-30, 2)), random sign.  Nearly every fp32 addition of two
+such values rounds, so summing the same workers in another order changes the
+result on most elements (tests/test_generate.py pins this).  Integer
+construction only: numpy and torch produce identical bits.
 """
 from __future__ import annotations
 
@@ -94,6 +108,29 @@ def dyadic_np(stream: int, count: int, start: int = 0) -> np.ndarray:
     return (k.astype(np.float32) / np.float32(256.0)).astype(np.float32)
 
 
+FULLMANT_BINADES = 31          # e in [0, 30]: magnitudes in [2^-30, 2)
+
+
+def _fullmant_bits_np(z: np.ndarray) -> np.ndarray:
+    sign = (z >> np.uint64(63)) << np.uint64(31)
+    e = (z >> np.uint64(23)) % np.uint64(FULLMANT_BINADES)
+    bits = sign | ((np.uint64(127) - e) << np.uint64(23)) | (z & np.uint64(0x7FFFFF))
+    return bits.astype(np.uint32)
+
+
+def fullmant_at_np(stream: int, index: np.ndarray) -> np.ndarray:
+    """Full-mantissa fp32 values of ``stream`` at arbitrary element indices."""
+    idx = np.asarray(index, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = _splitmix64_np(idx + np.uint64(stream_key(stream)))
+    return _fullmant_bits_np(z).view(np.float32)
+
+
+def fullmant_np(stream: int, start: int, count: int) -> np.ndarray:
+    """Full-mantissa fp32 values of ``stream`` at indices start .. start+count-1."""
+    return fullmant_at_np(stream, np.arange(start, start + count, dtype=np.uint64))
+
+
 # ------------------------------------------------------------- torch (device)
 def _s64(c: int) -> int:
     return c - (1 << 64) if c >= (1 << 63) else c
@@ -125,4 +162,23 @@ def values_torch(stream: int, start: int, count: int, shift: int, device, out=No
         z = _splitmix64_torch(idx + key)
         isum = (z & 0xFFFF) + ((z >> 16) & 0xFFFF) + ((z >> 32) & 0xFFFF) + ((z >> 48) & 0xFFFF)
         out[b:b + n] = (isum - 131070).to(torch.float32) * scale
+    return out
+
+
+def fullmant_torch(stream: int, start: int, count: int, device, out=None, block: int = 1 << 25):
+    """Same values as :func:`fullmant_np`, generated on ``device`` (blocked)."""
+    import torch
+    if out is None:
+        out = torch.empty(count, dtype=torch.float32, device=device)
+    key = _s64(stream_key(stream))
+    ov = out.view(torch.int32)
+    for b in range(0, count, block):
+        n = min(block, count - b)
+        idx = torch.arange(start + b, start + b + n, dtype=torch.int64, device=device)
+        z = _splitmix64_torch(idx + key)
+        sign = _lsr(z, 63) << 31
+        e = torch.remainder(_lsr(z, 23), FULLMANT_BINADES)
+        bits = sign | ((127 - e) << 23) | (z & 0x7FFFFF)
+        # low 32 bits as a signed int32 (two's complement) -> the fp32 pattern
+        ov[b:b + n] = (bits - ((bits >> 31) & 1) * (1 << 32)).to(torch.int32)
     return out
