@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--chunk-bytes", type=int, default=None)
     ap.add_argument("--kernel", default="auto", choices=["auto", "flat", "flat128", "tiles", "wide", "bulk"])
     ap.add_argument("--cache", default="enabled", choices=["enabled", "bypass"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=8,
+                    help="e2e rounds timed (the pipeline's fill + drain is amortised over them)")
     ap.add_argument("--e2e-streams", type=int, default=1,
                     help="copy streams per direction in the 1-GPU e2e measurement")
     ap.add_argument("--grid", type=int, default=0, help="CTAs for the flat kernel (0 = auto)")

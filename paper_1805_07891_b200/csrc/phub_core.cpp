@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -377,6 +378,21 @@ phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
         return PHUB_ERR_INVALID_ARGUMENT;
     }
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+    {
+        // every kernel loaded before any flag protocol can spin (lazy loading), once per device
+        static std::mutex mu;
+        static std::vector<int> loaded;
+        std::lock_guard<std::mutex> lk(mu);
+        if (std::find(loaded.begin(), loaded.end(), c->device) == loaded.end()) {
+            if ((e = phub::preload_kernels()) != cudaSuccess) {
+                cudaGetLastError();
+                delete c;
+                why = std::string("kernel preload: ") + cudaGetErrorString(e);
+                return PHUB_ERR_CUDA;
+            }
+            loaded.push_back(c->device);
+        }
+    }
     const size_t bytes = c->E_pad * sizeof(float);
     if ((e = cudaMalloc(&c->d_w, bytes)) != cudaSuccess ||
         (e = cudaMalloc(&c->d_v, bytes)) != cudaSuccess ||

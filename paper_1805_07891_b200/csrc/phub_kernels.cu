@@ -33,6 +33,8 @@
 //   k_wide_* ablation of MXNet-style wide aggregation: N-1
 //            pairwise passes then a separate optimizer pass; same arithmetic,
 //            12(N-1)+20 B/elt instead of 4N+16.
+#include <vector>
+
 #include "phub_kernels.cuh"
 #include "phub.h"
 
@@ -1033,6 +1035,41 @@ cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launch
                                      dim3(kThreads), args, 0, s);
     ++*launches;
     return e;
+}
+
+// Load every kernel of the library into the context now.  Under CUDA's lazy
+// loading (the CUDA 12 default) a kernel's code is loaded on its first use,
+// and a load can wait for the device -- including for a kernel spinning on a
+// device flag that only the not-yet-loaded kernel would raise (a producer and
+// consumer of one chain on two streams of one GPU, or any first exchange
+// round): a deadlock until the bounded wait expires.  phub_init calls this
+// once per device, before any flag protocol can run.
+cudaError_t preload_kernels() {
+    std::vector<const void*> fns;
+    for (int nw = 0; nw <= 9; ++nw) {
+        fns.push_back(pick_blocks<true>(nw));
+        fns.push_back(pick_blocks<false>(nw));
+        fns.push_back(pick_hier(nw, true));
+        fns.push_back(pick_hier(nw, false));
+        for (int vec : {4, 8})
+            for (int cache : {PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS})
+                for (bool agg : {false, true})
+                    fns.push_back(reinterpret_cast<const void*>(pick_flat(vec, nw, agg, cache)));
+        fns.push_back(reinterpret_cast<const void*>(pick_tiles_nw<false>(nw)));
+        fns.push_back(reinterpret_cast<const void*>(pick_tiles_nw<true>(nw)));
+        if (void* b = pick_bulk<false>(nw)) fns.push_back(b);
+        if (void* b = pick_bulk<true>(nw)) fns.push_back(b);
+    }
+    for (const void* f : {(const void*)k_prefix<0>, (const void*)k_prefix<1>, (const void*)k_prefix<2>,
+                          (const void*)k_prefix<3>, (const void*)k_prefix<4>, (const void*)k_prefix<5>,
+                          (const void*)k_wide_first, (const void*)k_wide_add, (const void*)k_wide_nag})
+        fns.push_back(f);
+    for (const void* f : fns) {
+        cudaFuncAttributes at;
+        cudaError_t e = cudaFuncGetAttributes(&at, f);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 size_t bulk_smem_bytes(int nw) { return (size_t)kBulkStages * (nw + 2) * kBulkTile * sizeof(float); }

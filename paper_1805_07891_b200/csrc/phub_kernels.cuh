@@ -109,6 +109,10 @@ cudaError_t launch_bulk(const FlatArgs& a, int grid, cudaStream_t s, int* launch
 size_t bulk_smem_bytes(int nw);
 cudaError_t launch_wide(const WideArgs& a, int grid, cudaStream_t s, int* launches);
 
+// Load every kernel into the current device's context (lazy-loading safety for
+// the flag protocols; see phub_kernels.cu).
+cudaError_t preload_kernels();
+
 // Resident CTAs per SM of the flat kernel for (vec, nw, agg) -- grid sizing.
 int flat_blocks_per_sm(int vec, int nw, bool agg, int cache);
 

@@ -134,7 +134,7 @@ SMALL = [3, 3, 9408, 64, 64, 4096, 20000, 1000, 262144, 7]
 
 @pytest.mark.parametrize("R,P,name,block,rounds", [
     (2, 4, "small", 2048, 2), (4, 2, "small", 2048, 2), (2, 4, "resnet50", 12288, 2),
-    (4, 2, "resnet50", 12288, 2), (4, 1, "tiny", 2048, 3)])
+    (4, 2, "resnet50", 12288, 2), (4, 1, "tiny", 2048, 3), (8, 1, "resnet50", 12288, 2)])
 def test_push_exchange_emulated(R, P, name, block, rounds):
     """k_hier worker_order=1 == PushShardedPHub's round: bit-exact vs the
     worker-order oracle over all R*P workers; every rank holds the full w'."""
@@ -169,7 +169,7 @@ def _owned_mask(h, sizes):
 
 @pytest.mark.parametrize("R,P,name,block", [
     (2, 4, "small", 2048), (4, 2, "small", 2048), (2, 8, "resnet50", 32768),
-    (4, 3, "resnet50", 16384)])
+    (4, 3, "resnet50", 16384), (8, 2, "small", 2048)])
 def test_hierarchical_exchange_emulated(R, P, name, block):
     """k_hier worker_order=0 == HierPHub's round: bit-exact vs
     oracle.hier_round (rack-order sum of rack aggregates, reading R17), and
@@ -291,6 +291,7 @@ def test_piece_flags_chain_concurrent_streams():
     cons.push(0, inbox)
     for k in range(P):
         cons.push(1 + k, gd[P + k])
+    torch.cuda.synchronize()         # the zero-fills above ran on torch's stream, not s_*
     for p, (b, e) in enumerate(pieces):
         capi.phub_aggregate_range(cons.ctx, b, e, s_cons.cuda_stream,
                                   wait=(flags.data_ptr() + 4 * p, 1))
