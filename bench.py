@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--chunk-bytes", type=int, default=None)
     ap.add_argument("--kernel", default="auto", choices=["auto", "flat", "flat128", "tiles", "wide", "bulk"])
-    ap.add_argument("--cache", default="enabled", choices=["enabled", "bypass"])
+    ap.add_argument("--cache", default="bypass", choices=["enabled", "bypass"],
+                    help="L2 policy: bypass = every stream evict-first (default, measured "
+                         "fastest); enabled = w' evict-last for the pull (P:911)")
     ap.add_argument("--e2e-steps", type=int, default=8,
                     help="e2e rounds timed (the pipeline's fill + drain is amortised over them)")
     ap.add_argument("--e2e-streams", type=int, default=1,
@@ -659,7 +661,7 @@ def bench_multi(args, mname, N, cb):
         t = torch.tensor([a.elapsed_time(b) / args.e2e_steps], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item()) / 1e3
-        if p2p:
+        if chain:
             sh.check()
         del host_g, host_o
         probe = pcie_probe(dev)

@@ -92,7 +92,8 @@ struct phub_ctx_s {
     int flat_oneshot = -1;            // -1 auto: one-shot for local HBM streams (profiles/
                                       // r01_tune2), persistent grid when peer replicas are
                                       // registered (NVLink latency; profiles/r01_multi2)
-    int cache = PHUB_CACHE_ENABLED;
+    int cache = PHUB_CACHE_BYPASS;    // every stream evict-first: measured fastest on B200,
+                                      // alone and with the pull (R14, NEXT-2)
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     int blocks_occ[2][phub::kMaxWorkers + 1] = {};      // resident CTAs/SM [nag][nw]
     int hier_occ[2] = {0, 0};                          // resident CTAs/SM of k_hier [worker_order]

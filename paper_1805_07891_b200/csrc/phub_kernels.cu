@@ -707,8 +707,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ Hi
                                 for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], rv.x[e]);
                             }
                         }
-                        V8 wv = ld_state<PHUB_CACHE_ENABLED>(w + i);
-                        V8 vv = ld_state<PHUB_CACHE_ENABLED>(v + i);
+                        V8 wv = ld_state<PHUB_CACHE_BYPASS>(w + i);   // read once: evict-first
+                        V8 vv = ld_state<PHUB_CACHE_BYPASS>(v + i);
                         V8 sv;
 #pragma unroll
                         for (int e = 0; e < 8; ++e) {
