@@ -1,0 +1,163 @@
+// l2_residue2.cu (derived from cache_sweep.cu) -- L2 policy sweep of the fused aggregate + Nesterov step
+// (k_flat's one-shot 256-bit schedule, N = 8, VGG-19 size) on one B200.
+//
+// Scratch experiment for NEXT-2 (P:691 / P:908-935 "cache-enabled vs
+// cache-bypass"): which L2 eviction hints on which stream make the streaming
+// kernel fastest, alone and followed by the pull of w' (a D2D copy)?
+//   G: gradient loads   0 = .nc L1::no_allocate L2::evict_first (k_flat)
+//                       1 = .nc L1::no_allocate (no L2 hint)
+//                       2 = .nc L1::no_allocate L2::evict_first L2::256B prefetch
+//   S: w, v loads       0 = L1::no_allocate            1 = + L2::evict_first
+//   W: w' store         0 = L2::evict_last (k_flat "cache enabled")
+//                       1 = L2::evict_first (k_flat "bypass")   2 = no hint
+//   V: v' store         0 = L2::evict_first (k_flat)   1 = no hint
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o cache_sweep cache_sweep.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+struct alignas(32) V8 { float x[8]; };
+
+template <int G> __device__ __forceinline__ V8 ldg(const V8* p) {
+    V8 r;
+    if (G == 0)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]), "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7]) : "l"(p));
+    else if (G == 1)
+        asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]), "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7]) : "l"(p));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]), "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7]) : "l"(p));
+    return r;
+}
+template <int S> __device__ __forceinline__ V8 lds(const V8* p) {
+    V8 r;
+    if (S == 0)
+        asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]), "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7]) : "l"(p));
+    else
+        asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]), "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7]) : "l"(p));
+    return r;
+}
+template <int W> __device__ __forceinline__ void stw(V8* p, const V8& r) {
+    if (W == 0)
+        asm volatile("st.global.L1::no_allocate.L2::evict_last.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+            :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]), "f"(r.x[5]), "f"(r.x[6]), "f"(r.x[7]) : "memory");
+    else if (W == 1)
+        asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+            :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]), "f"(r.x[5]), "f"(r.x[6]), "f"(r.x[7]) : "memory");
+    else
+        asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+            :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]), "f"(r.x[5]), "f"(r.x[6]), "f"(r.x[7]) : "memory");
+}
+
+struct Args { const float* g[8]; float* w; float* v; uint64_t nvec; float lr, mu, resc; };
+
+template <int G, int S, int W, int V>
+__global__ void __launch_bounds__(256) k(const __grid_constant__ Args a) {
+    const uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    if (i >= a.nvec) return;
+    V8 gv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) gv[q] = ldg<G>(reinterpret_cast<const V8*>(a.g[q]) + i);
+    V8 wv = lds<S>(reinterpret_cast<const V8*>(a.w) + i);
+    V8 vv = lds<S>(reinterpret_cast<const V8*>(a.v) + i);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float s = __fadd_rn(0.0f, gv[0].x[j]);
+#pragma unroll
+        for (int q = 1; q < 8; ++q) s = __fadd_rn(s, gv[q].x[j]);
+        const float g = __fmul_rn(s, a.resc);
+        const float vn = __fadd_rn(__fmul_rn(a.mu, vv.x[j]), g);
+        wv.x[j] = __fsub_rn(wv.x[j], __fmul_rn(a.lr, __fadd_rn(g, __fmul_rn(a.mu, vn))));
+        vv.x[j] = vn;
+    }
+    stw<W>(reinterpret_cast<V8*>(a.w) + i, wv);
+    if (V == 0) stw<1>(reinterpret_cast<V8*>(a.v) + i, vv);
+    else stw<2>(reinterpret_cast<V8*>(a.v) + i, vv);
+}
+
+
+// fill with full-mantissa-like random bits (finite, normal)
+__global__ void fill(float* p, uint64_t n, uint64_t seed) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t z = (i + seed) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        uint32_t b = (uint32_t)((z >> 63) << 31) | (uint32_t)((127 - (z >> 23) % 20) << 23) | (uint32_t)(z & 0x7FFFFF);
+        p[i] = __uint_as_float(b) * 1e-3f;
+    }
+}
+// pollute: store `n` floats with L2::evict_last (what PHUB_CACHE_ENABLED does to w')
+__global__ void pollute(float* p, uint64_t nvec) {
+    const uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    if (i < nvec) { V8 r; for (int j = 0; j < 8; ++j) r.x[j] = 1.0f; stw<0>(reinterpret_cast<V8*>(p) + i, r); }
+}
+
+int main() {
+    const uint64_t E = 143667264, nvec = E / 8;
+    std::vector<float*> bufs(11);
+    for (int b = 0; b < 11; ++b) { cudaMalloc(&bufs[b], E * 4); fill<<<4096, 256>>>(bufs[b], E, 1000003ull * b); }
+    float* junk; cudaMalloc(&junk, 256u << 20);
+    Args a{};
+    for (int q = 0; q < 8; ++q) a.g[q] = bufs[q];
+    a.w = bufs[8]; a.v = bufs[9]; a.nvec = nvec; a.lr = 0.1f; a.mu = 0.9f; a.resc = 0.125f;
+    const unsigned grid = (unsigned)((nvec + 255) / 256);
+    cudaStream_t st; cudaStreamCreate(&st);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    auto bypass = k<0, 1, 1, 0>;
+    auto enabled = k<0, 0, 0, 0>;
+    auto time = [&](void (*fn)(Args), const char* what) {
+        for (int t = 0; t < 3; ++t) fn<<<grid, 256, 0, st>>>(a);
+        cudaEventRecord(e0, st);
+        for (int t = 0; t < 20; ++t) fn<<<grid, 256, 0, st>>>(a);
+        cudaEventRecord(e1, st); cudaEventSynchronize(e1);
+        float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
+        printf("{\"step\": \"%s\", \"ms\": %.4f}\n", what, ms / 20); fflush(stdout);
+    };
+    int maxwin = 0, maxpers = 0;
+    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, 0);
+    cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, 0);
+    printf("{\"max_window_bytes\": %d, \"max_persisting_l2_bytes\": %d}\n", maxwin, maxpers);
+    cudaDeviceSynchronize();
+    time(bypass, "bypass fresh");
+    time(bypass, "bypass fresh again");
+    for (int which = 0; which < 2; ++which)
+        for (int mb : {32, 64, 96, 128}) {
+            float* base = which == 0 ? a.w : a.v;
+            uint64_t n = ((uint64_t)mb << 20) / 4;
+            pollute<<<(unsigned)(n / 8 / 256 + 1), 256, 0, st>>>(base + E - n, n / 8);
+            char b[96]; snprintf(b, sizeof b, "bypass after last %d MB of %s stored evict_last", mb, which ? "v" : "w");
+            time(bypass, b);
+            time(bypass, "  ... again");
+            cudaCtxResetPersistingL2Cache();
+            time(bypass, "  ... after reset");
+        }
+    // the CUDA L2 persistence API: a persisting access-policy window over the tail of w
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, maxpers);
+    for (int mb : {16, 32, 64}) {
+        if (((uint64_t)mb << 20) > (uint64_t)maxwin) break;
+        cudaStreamAttrValue attr = {};
+        uint64_t n = ((uint64_t)mb << 20) / 4;
+        attr.accessPolicyWindow.base_ptr = a.w + E - n;
+        attr.accessPolicyWindow.num_bytes = (size_t)mb << 20;
+        attr.accessPolicyWindow.hitRatio = 1.0f;
+        attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr);
+        char b[96]; snprintf(b, sizeof b, "bypass with a %d MB persisting window on w's tail", mb);
+        time(bypass, b);
+        time(bypass, "  ... again");
+        attr.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr);
+        cudaCtxResetPersistingL2Cache();
+        time(bypass, "  ... window off + reset");
+    }
+    cudaError_t err = cudaGetLastError();
+    printf("{\"status\": \"%s\"}\n", cudaGetErrorString(err));
+    return err == cudaSuccess ? 0 : 1;
+}
