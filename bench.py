@@ -47,9 +47,10 @@ def parse():
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--chunk-bytes", type=int, default=None)
     ap.add_argument("--kernel", default="auto", choices=["auto", "flat", "flat128", "tiles", "wide", "bulk"])
-    ap.add_argument("--cache", default="bypass", choices=["enabled", "bypass"],
-                    help="L2 policy: bypass = every stream evict-first (default, measured "
-                         "fastest); enabled = w' evict-last for the pull (P:911)")
+    ap.add_argument("--cache", default="resident", choices=["enabled", "bypass", "resident"],
+                    help="L2 policy: resident = a fixed 32 MiB slice of w stays in L2 across "
+                         "rounds, the rest evict-first (default, measured fastest); bypass = "
+                         "every stream evict-first; enabled = all of w' evict-last (P:911)")
     ap.add_argument("--e2e-steps", type=int, default=8,
                     help="e2e rounds timed (the pipeline's fill + drain is amortised over them)")
     ap.add_argument("--e2e-streams", type=int, default=1,
@@ -800,8 +801,9 @@ def bench_single(args, mname, N, cb):
         hub.close()
         hub = PHub(sizes, N, chunk_size_bytes=cb, device=0, keep_aggregate=True)
     hub.set_option(capi.PHUB_OPT_KERNEL, kern)
-    hub.set_option(capi.PHUB_OPT_CACHE, capi.PHUB_CACHE_BYPASS if args.cache == "bypass"
-                   else capi.PHUB_CACHE_ENABLED)
+    hub.set_option(capi.PHUB_OPT_CACHE, {"bypass": capi.PHUB_CACHE_BYPASS,
+                                         "enabled": capi.PHUB_CACHE_ENABLED,
+                                         "resident": capi.PHUB_CACHE_RESIDENT}[args.cache])
     if args.grid:
         hub.set_option(capi.PHUB_OPT_GRID, args.grid)
     if args.tile_elems:
@@ -943,12 +945,15 @@ def bench_graph(hub, grads, N, E, stream, steps, rounds_per_graph=20):
 
 def bench_cache_table(hub, grads, N, E, stream, args, reps=20):
     """The caching table of P:913-935 (S 5, "Caching Effectiveness") on B200: the
-    fused aggregate + Nesterov kernel with the cache-enabled policy (w' stored
-    L2 evict-last so the pull that follows reads it from L2) vs all
-    streams evict-first (the cache-bypass analog), each timed alone and followed
-    by the pull of the whole model (phub_pull ALL_KEYS into a device buffer),
-    plus the pull alone ("Opt/Agg Off").  Mean ms over `reps` (CUDA events on
-    the launching stream); DRAM bytes come from the committed ncu capture."""
+    fused aggregate + Nesterov kernel under each L2 policy -- cache-enabled (all
+    of w' stored evict-last so the pull that follows reads it from L2),
+    cache-bypass (every stream evict-first) and resident (a fixed slice of w
+    kept in L2 across rounds, the default) -- each timed alone and followed by
+    the pull of the whole model (phub_pull ALL_KEYS into a device buffer), plus
+    the pull alone ("Opt/Agg Off").  Mean ms over `reps` (CUDA events on the
+    launching stream).  The L2 state a policy leaves behind changes the next
+    policy's time (profiles/r02_l2/), so each policy is measured after its own
+    `settle` rounds; fresh-process numbers are in profiles/r02_l2/."""
     import torch
     from paper_1805_07891_b200 import capi
     dst = torch.empty(hub.E_padded, dtype=torch.float32, device=grads[0].device)
@@ -978,13 +983,17 @@ def bench_cache_table(hub, grads, N, E, stream, args, reps=20):
         pull()
 
     rows = {"pull_only_ms": timed(pull)}
-    for mode, val in (("cached", capi.PHUB_CACHE_ENABLED), ("bypass", capi.PHUB_CACHE_BYPASS)):
+    modes = (("resident", capi.PHUB_CACHE_RESIDENT), ("cached", capi.PHUB_CACHE_ENABLED),
+             ("bypass", capi.PHUB_CACHE_BYPASS))
+    for mode, val in modes:
         hub.set_option(capi.PHUB_OPT_CACHE, val)
+        for _ in range(10):                       # settle: the previous policy's L2 state
+            agg()
         rows[f"{mode}_kernel_ms"] = timed(agg)
         rows[f"{mode}_kernel_pull_ms"] = timed(agg_pull)
-    hub.set_option(capi.PHUB_OPT_CACHE, capi.PHUB_CACHE_ENABLED)
+    hub.set_option(capi.PHUB_OPT_CACHE, capi.PHUB_CACHE_RESIDENT)
     out = {k: round(v, 4) for k, v in rows.items()}
-    for mode in ("cached", "bypass"):
+    for mode, _ in modes:
         out[f"{mode}_exchanges_per_s"] = round(N / (rows[f"{mode}_kernel_pull_ms"] / 1e3), 1)
     out["how"] = ("mean of %d rounds each; pull = phub_pull(ALL_KEYS) D2D of the padded model "
                   "(cudaMemcpyAsync: %.0f MB read + written)" % (reps, 4 * hub.E_padded / 1e6))

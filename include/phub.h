@@ -418,6 +418,8 @@ enum {
     PHUB_OPT_TILE_ELEMS = 3,  /* max elements per CTA tile in the chunk-tile kernel (1024) */
     PHUB_OPT_CACHE = 4,       /* PHUB_CACHE_*: L2 policy of the pulled weights   */
                               /* (5, 6: removed in round 2 -- measured without gain)     */
+    PHUB_OPT_L2_RESIDENT = 8, /* PHUB_CACHE_RESIDENT: bytes of w kept L2-resident across  */
+                              /* rounds (the tail of the owned range; default 32 MiB)    */
     PHUB_OPT_FLAT_ONESHOT = 7 /* flat kernels: 1 = one vector per thread, grid covering */
                               /* the range (the hardware CTA scheduler balances like     */
                               /* PHub's chunk -> core map); 0 = persistent grid (SMs x   */
@@ -436,12 +438,17 @@ enum {
                               /* async copies (TMA engine, mbarrier ring); N <= 8        */
 };
 enum {
-    PHUB_CACHE_ENABLED = 0,   /* w' stored evict-last (kept in L2 for the pull), grads   */
-                              /* evict-first ("cache-enabled")              */
-    PHUB_CACHE_BYPASS = 1     /* DEFAULT: every stream evict-first (non-temporal analog): */
-                              /* on B200 the model (>> 126 MB L2) never fits, so keeping  */
-                              /* w' only crowds L2 -- measured 0.952 vs 1.009 ms (VGG-19,  */
-                              /* N = 8), also faster with the pull (R14)        */
+    PHUB_CACHE_ENABLED = 0,   /* all of w' stored evict-last (kept in L2 for the pull),  */
+                              /* grads evict-first ("cache-enabled")        */
+    PHUB_CACHE_BYPASS = 1,    /* every stream evict-first (the cache-bypass analog)     */
+    PHUB_CACHE_RESIDENT = 2   /* DEFAULT: a FIXED slice of w (the last                 */
+                              /* PHUB_OPT_L2_RESIDENT bytes of the owned range) is loaded */
+                              /* and stored evict-last, so it stays in L2 from round to  */
+                              /* round; everything else evict-first.  VGG-19, N = 8:     */
+                              /* 0.978 vs 1.003 (BYPASS) vs 1.009 ms (ENABLED): the model */
+                              /* (>> 126 MB of L2) never fits, so caching all of w' only */
+                              /* crowds L2, a fixed resident slice is hit every round    */
+                              /* (R14, profiles/r02_l2/)                       */
 };
 phub_status phub_set_option(phub_ctx ctx, int32_t option, int64_t value);
 

@@ -92,8 +92,9 @@ struct phub_ctx_s {
     int flat_oneshot = -1;            // -1 auto: one-shot for local HBM streams (profiles/
                                       // r01_tune2), persistent grid when peer replicas are
                                       // registered (NVLink latency; profiles/r01_multi2)
-    int cache = PHUB_CACHE_BYPASS;    // every stream evict-first: measured fastest on B200,
-                                      // alone and with the pull (R14, NEXT-2)
+    int cache = PHUB_CACHE_RESIDENT;  // a fixed L2-resident slice of w, the rest evict-first:
+                                      // measured fastest on B200 (R14, NEXT-2)
+    uint64_t resident_bytes = 32ull << 20;   // PHUB_OPT_L2_RESIDENT (profiles/r02_l2/: 32 MiB best)
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     int blocks_occ[2][phub::kMaxWorkers + 1] = {};      // resident CTAs/SM [nag][nw]
     int hier_occ[2] = {0, 0};                          // resident CTAs/SM of k_hier [worker_order]
@@ -634,6 +635,16 @@ static cudaError_t launch_keys(phub_ctx c, cudaStream_t s, const std::vector<uin
     return e;
 }
 
+// PHUB_CACHE_RESIDENT: first vector (relative to `lo`, in `vec`-element units)
+// of the kept slice -- the last resident_bytes of this context's owned range
+// [ob, oe) -- for a launch over [lo, hi); UINT64_MAX when the launch holds none.
+static uint64_t keep_from(phub_ctx c, uint64_t ob, uint64_t oe, uint64_t lo, uint64_t hi, int vec) {
+    const uint64_t keep = std::min<uint64_t>(oe - ob, c->resident_bytes / 4) / vec * vec;
+    const uint64_t ks = oe - keep;                    // first kept element
+    if (keep == 0 || ks >= hi) return UINT64_MAX;
+    return ks > lo ? (ks - lo + vec - 1) / vec : 0;
+}
+
 static void end_iteration(phub_ctx c) {
     std::fill(c->got.begin(), c->got.end(), 0);
     c->got_count = 0;
@@ -875,6 +886,7 @@ phub_status phub_aggregate_range(phub_ctx c, uint64_t begin, uint64_t end,
                              ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
                              : c->flat_grid[1][c->keep_agg];
             grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, cover));
+            a.keep_from = keep_from(c, ob, oe, lo, e_, 8);
             e = phub::launch_flat(a, 8, c->cache, grid, static_cast<cudaStream_t>(stream),
                                   &c->launches);
         }
@@ -970,6 +982,7 @@ phub_status phub_aggregate_optimize(phub_ctx c, void* stream) {
                          ? (int)std::min<uint64_t>(cover, 0x7fffffffULL)
                                      : c->flat_grid[vec == 8][c->keep_agg];
         grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(grid, cover));
+        a.keep_from = keep_from(c, b, eend, b, eend, vec);
         if (variant == PHUB_KERNEL_BULK)
             e = phub::launch_bulk(a, c->grid_override ? c->grid_override : c->num_sms, s,
                                   &c->launches);
@@ -1314,8 +1327,13 @@ phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
             if (value < 0 || value > (1 << 30)) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "bad grid");
             c->grid_override = (int)value;
             return PHUB_OK;
+        case PHUB_OPT_L2_RESIDENT:
+            if (value < 0) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "resident bytes must be >= 0");
+            c->resident_bytes = (uint64_t)value;
+            return PHUB_OK;
         case PHUB_OPT_CACHE: {
-            if (value != PHUB_CACHE_ENABLED && value != PHUB_CACHE_BYPASS)
+            if (value != PHUB_CACHE_ENABLED && value != PHUB_CACHE_BYPASS &&
+                value != PHUB_CACHE_RESIDENT)
                 return c->fail(PHUB_ERR_INVALID_ARGUMENT, "unknown cache mode");
             c->cache = (int)value;
             DeviceGuard g(c->device);

@@ -68,11 +68,18 @@ __device__ __forceinline__ V4 ld_grad(const V4* p) {
     return r;
 }
 
-// Model state (w, v): read then rewritten by the same thread.
+// Model state (w, v): read then rewritten by the same thread.  ENABLED: no
+// L2 hint; BYPASS: evict-first; RESIDENT: evict-last (the kept slice of w,
+// re-read from L2 next round).
 template <int CACHE>
 __device__ __forceinline__ V8 ld_state(const V8* p) {
     V8 r;
-    if (CACHE == PHUB_CACHE_BYPASS)
+    if (CACHE == PHUB_CACHE_RESIDENT)
+        asm volatile("ld.global.L1::no_allocate.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
+                       "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
+                     : "l"(p));
+    else if (CACHE == PHUB_CACHE_BYPASS)
         asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
                        "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
@@ -93,9 +100,10 @@ __device__ __forceinline__ V4 ld_state(const V4* p) {
     return r;
 }
 
-// Updated weights: under PHUB_CACHE_ENABLED they are stored L2 evict-last so
-// a pull / all-gather that follows is served from L2 ("models can be sent
-// directly from cache after being updated"); under BYPASS they stream.
+// Updated weights: under PHUB_CACHE_ENABLED (and for the kept slice under
+// RESIDENT) they are stored L2 evict-last so a pull / the next round is served
+// from L2 ("models can be sent directly from cache after being updated",
+// P:911); under BYPASS (and outside the kept slice) they stream.
 template <int CACHE>
 __device__ __forceinline__ void st_w(V8* p, const V8& r) {
     if (CACHE == PHUB_CACHE_BYPASS)
@@ -226,6 +234,8 @@ __device__ __forceinline__ void flat_body(const FlatArgs& a, uint64_t i) {
     V* __restrict__ v = reinterpret_cast<V*>(a.v + a.begin);
     V* __restrict__ sa = AGG ? reinterpret_cast<V*>(a.agg + a.begin) : nullptr;
     {
+        // RESIDENT: the last keep vectors of the range are the L2-kept slice of w
+        const bool keep = CACHE == PHUB_CACHE_RESIDENT && i >= a.keep_from;
         float acc[VEC];
         if constexpr (NW > 0) {
             V gv[NW];
@@ -256,15 +266,19 @@ __device__ __forceinline__ void flat_body(const FlatArgs& a, uint64_t i) {
                     }
             }
         }
-        V wv = ld_state<CACHE>(w + i);
-        V vv = ld_state<CACHE>(v + i);
+        constexpr int C_OUT = CACHE == PHUB_CACHE_RESIDENT ? PHUB_CACHE_BYPASS : CACHE;
+        V wv = keep ? ld_state<PHUB_CACHE_RESIDENT>(w + i) : ld_state<C_OUT>(w + i);
+        V vv = ld_state<C_OUT>(v + i);
         V sv;
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
             sv.x[j] = acc[j];
             nag(acc[j], wv.x[j], vv.x[j], a.lr, a.mu, a.rescale);
         }
-        st_w<CACHE>(w + i, wv);
+        if (keep)
+            st_w<PHUB_CACHE_ENABLED>(w + i, wv);         // evict-last: stays resident
+        else
+            st_w<C_OUT>(w + i, wv);
         st_stream(v + i, vv);
         if constexpr (AGG) st_stream(sa + i, sv);
         // fused pull: w' straight into every registered (peer) replica over NVLink
@@ -939,6 +953,9 @@ FlatFn pick_flat_nw(int nw) {
 
 FlatFn pick_flat(int vec, int nw, bool agg, int cache) {
     if (vec == 8) {
+        if (cache == PHUB_CACHE_RESIDENT)
+            return agg ? pick_flat_nw<8, PHUB_CACHE_RESIDENT, true>(nw)
+                       : pick_flat_nw<8, PHUB_CACHE_RESIDENT, false>(nw);
         if (cache == PHUB_CACHE_BYPASS)
             return agg ? pick_flat_nw<8, PHUB_CACHE_BYPASS, true>(nw)
                        : pick_flat_nw<8, PHUB_CACHE_BYPASS, false>(nw);
@@ -1052,7 +1069,7 @@ cudaError_t preload_kernels() {
         fns.push_back(pick_hier(nw, true));
         fns.push_back(pick_hier(nw, false));
         for (int vec : {4, 8})
-            for (int cache : {PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS})
+            for (int cache : {PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS, PHUB_CACHE_RESIDENT})
                 for (bool agg : {false, true})
                     fns.push_back(reinterpret_cast<const void*>(pick_flat(vec, nw, agg, cache)));
         fns.push_back(reinterpret_cast<const void*>(pick_tiles_nw<false>(nw)));

@@ -39,6 +39,8 @@ struct FlatArgs {
                                       // host turns it into a sticky PHUB_ERR_SYNC_TIMEOUT
     uint64_t block;                   // > 0: block-streaming flags (one per `block` elements)
     uint32_t* ticket;                 // [0] next block, [1] CTAs done (block streaming, zeroed)
+    uint64_t keep_from;               // PHUB_CACHE_RESIDENT: vectors >= keep_from (relative to
+                                      // begin) are the L2-kept slice of w
 };
 
 // Hierarchical reduction: one GPU = one rack's PBox with its P

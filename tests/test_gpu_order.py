@@ -181,19 +181,22 @@ def test_negative_control_collective_order_fails_parity():
     probe.close()
 
 
-@pytest.mark.parametrize("cache", ["ENABLED", "BYPASS"])
+@pytest.mark.parametrize("cache", ["ENABLED", "BYPASS", "RESIDENT"])
 @pytest.mark.parametrize("kernel", ["FLAT", "FLAT128"])
 @pytest.mark.parametrize("N", [3, 8])
 def test_cache_policies_bit_exact(kernel, N, cache):
-    """Both L2 policies -- PHUB_CACHE_BYPASS (every stream evict-first: the
-    paper's cache-bypassed Opt/Agg; the default since round 2) and
-    PHUB_CACHE_ENABLED (w' evict-last for the pull) -- compute the
-    oracle's bits (a policy changes placement, not values)."""
+    """Every L2 policy -- PHUB_CACHE_RESIDENT (the default: a fixed slice of w
+    kept in L2, here 100 KB so the range splits mid-key), PHUB_CACHE_BYPASS
+    (every stream evict-first: the paper's cache-bypassed Opt/Agg,
+    P:913-935) and PHUB_CACHE_ENABLED (all of w' evict-last for the pull,
+    P:911) -- computes the oracle's bits (a policy changes placement, not
+    values)."""
     from paper_1805_07891_b200 import capi
     sizes = [3, 4096, 9408, 20000, 262144, 7]
     hub = _hub(sizes, N, keep_aggregate=True)
     hub.set_option(capi.PHUB_OPT_KERNEL, getattr(capi, f"PHUB_KERNEL_{kernel}"))
     hub.set_option(capi.PHUB_OPT_CACHE, getattr(capi, f"PHUB_CACHE_{cache}"))
+    hub.set_option(capi.PHUB_OPT_L2_RESIDENT, 100000)
     E = hub.E
     w0, v0 = fullmant_np(1 + 37 * 52, 0, E), fullmant_np(2 + 37 * 52, 0, E)
     hub.load_state(w0, v0)
