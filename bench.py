@@ -51,6 +51,8 @@ def parse():
                     help="L2 policy: resident = a fixed 32 MiB slice of w stays in L2 across "
                          "rounds, the rest evict-first (default, measured fastest); bypass = "
                          "every stream evict-first; enabled = all of w' evict-last (P:911)")
+    ap.add_argument("--resident-mb", type=int, default=-1,
+                    help="resident policy: MiB of w kept in L2 across rounds (-1: library default)")
     ap.add_argument("--e2e-steps", type=int, default=8,
                     help="e2e rounds timed (the pipeline's fill + drain is amortised over them)")
     ap.add_argument("--e2e-streams", type=int, default=1,
@@ -804,6 +806,8 @@ def bench_single(args, mname, N, cb):
     hub.set_option(capi.PHUB_OPT_CACHE, {"bypass": capi.PHUB_CACHE_BYPASS,
                                          "enabled": capi.PHUB_CACHE_ENABLED,
                                          "resident": capi.PHUB_CACHE_RESIDENT}[args.cache])
+    if args.resident_mb >= 0:
+        hub.set_option(capi.PHUB_OPT_L2_RESIDENT, args.resident_mb << 20)
     if args.grid:
         hub.set_option(capi.PHUB_OPT_GRID, args.grid)
     if args.tile_elems:
@@ -885,6 +889,8 @@ def bench_single(args, mname, N, cb):
                    "workers": N, "chunk_bytes": cb, "grid": args.grid, "tile_elems": args.tile_elems, "oneshot": args.oneshot,
                    "mode": "M1 (1 GPU, pushes resident, "
                    "zero-copy BORROW)", "kernel": kname, "cache": args.cache,
+                   "l2_resident_mib": (None if args.cache != "resident" else
+                                       args.resident_mb if args.resident_mb >= 0 else 32),
                    "l2": f"no flush: inputs exceed L2 ({(4 * N + 16) * E / 1e9:.2f} GB/round "
                          f"vs 126 MB L2)" if (4 * N + 16) * E > 4 * 126e6 else
                          "inputs fit in L2 (reported as us/round)",

@@ -642,7 +642,9 @@ static uint64_t keep_from(phub_ctx c, uint64_t ob, uint64_t oe, uint64_t lo, uin
     const uint64_t keep = std::min<uint64_t>(oe - ob, c->resident_bytes / 4) / vec * vec;
     const uint64_t ks = oe - keep;                    // first kept element
     if (keep == 0 || ks >= hi) return UINT64_MAX;
-    return ks > lo ? (ks - lo + vec - 1) / vec : 0;
+    // rounded up to a whole warp of vectors: the kernel's L2 policy operand is
+    // warp-uniform (it is moved into a uniform register, R2UR)
+    return ks > lo ? ((ks - lo + vec - 1) / vec + 31) / 32 * 32 : 0;
 }
 
 static void end_iteration(phub_ctx c) {

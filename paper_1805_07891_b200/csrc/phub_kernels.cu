@@ -100,6 +100,45 @@ __device__ __forceinline__ V4 ld_state(const V4* p) {
     return r;
 }
 
+// PHUB_CACHE_RESIDENT: w is loaded and stored with a run-time L2 policy
+// operand (createpolicy + .L2::cache_hint), evict-last on the kept slice and
+// evict-first elsewhere -- one instruction form for both, so the choice costs
+// no registers (a branch between two qualifier forms cost 20).  The policy must
+// be warp-uniform: the host rounds keep_from to a whole warp of vectors.
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+    uint64_t p;
+    if (keep)
+        asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else
+        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+template <int VEC>
+__device__ __forceinline__ VecT<VEC> ld_state_pol(const VecT<VEC>* p, uint64_t pol) {
+    VecT<VEC> r;
+    if constexpr (VEC == 8)
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                     : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
+                       "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
+                     : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3])
+                     : "l"(p), "l"(pol));
+    return r;
+}
+template <int VEC>
+__device__ __forceinline__ void st_state_pol(VecT<VEC>* p, const VecT<VEC>& r, uint64_t pol) {
+    if constexpr (VEC == 8)
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;"
+                     :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "f"(r.x[4]),
+                        "f"(r.x[5]), "f"(r.x[6]), "f"(r.x[7]), "l"(pol) : "memory");
+    else
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                     :: "l"(p), "f"(r.x[0]), "f"(r.x[1]), "f"(r.x[2]), "f"(r.x[3]), "l"(pol)
+                     : "memory");
+}
+
 // Updated weights: under PHUB_CACHE_ENABLED (and for the kept slice under
 // RESIDENT) they are stored L2 evict-last so a pull / the next round is served
 // from L2 ("models can be sent directly from cache after being updated",
@@ -234,8 +273,8 @@ __device__ __forceinline__ void flat_body(const FlatArgs& a, uint64_t i) {
     V* __restrict__ v = reinterpret_cast<V*>(a.v + a.begin);
     V* __restrict__ sa = AGG ? reinterpret_cast<V*>(a.agg + a.begin) : nullptr;
     {
-        // RESIDENT: the last keep vectors of the range are the L2-kept slice of w
-        const bool keep = CACHE == PHUB_CACHE_RESIDENT && i >= a.keep_from;
+        // RESIDENT: vectors >= keep_from are the L2-kept slice of w (warp-uniform)
+        const uint64_t wpol = CACHE == PHUB_CACHE_RESIDENT ? l2_policy(i >= a.keep_from) : 0;
         float acc[VEC];
         if constexpr (NW > 0) {
             V gv[NW];
@@ -267,7 +306,7 @@ __device__ __forceinline__ void flat_body(const FlatArgs& a, uint64_t i) {
             }
         }
         constexpr int C_OUT = CACHE == PHUB_CACHE_RESIDENT ? PHUB_CACHE_BYPASS : CACHE;
-        V wv = keep ? ld_state<PHUB_CACHE_RESIDENT>(w + i) : ld_state<C_OUT>(w + i);
+        V wv = CACHE == PHUB_CACHE_RESIDENT ? ld_state_pol<VEC>(w + i, wpol) : ld_state<C_OUT>(w + i);
         V vv = ld_state<C_OUT>(v + i);
         V sv;
 #pragma unroll
@@ -275,8 +314,8 @@ __device__ __forceinline__ void flat_body(const FlatArgs& a, uint64_t i) {
             sv.x[j] = acc[j];
             nag(acc[j], wv.x[j], vv.x[j], a.lr, a.mu, a.rescale);
         }
-        if (keep)
-            st_w<PHUB_CACHE_ENABLED>(w + i, wv);         // evict-last: stays resident
+        if constexpr (CACHE == PHUB_CACHE_RESIDENT)
+            st_state_pol<VEC>(w + i, wv, wpol);           // kept slice: evict-last, stays resident
         else
             st_w<C_OUT>(w + i, wv);
         st_stream(v + i, vv);
