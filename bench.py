@@ -78,12 +78,20 @@ def parse():
                     help="hier mode: elements per block flag")
     ap.add_argument("--push-block", type=int, default=12288,
                     help="push mode: elements per block flag")
+    ap.add_argument("--sched-block", type=int, default=16384,
+                    help="sched mode: elements per item block")
+    ap.add_argument("--sched-lag", type=int, default=0,
+                    help="sched mode: blocks of progress each chain stage / consumer lags")
+    ap.add_argument("--sched-weights", default="",
+                    help="sched mode: comma-separated owner shares (default: sharded.SCHED_TABLE)")
+    ap.add_argument("--sched-raw", default="",
+                    help="sched mode: comma-separated RAW fraction per owner (with --sched-weights)")
     ap.add_argument("--chain-producer-grid", type=int, default=0,
                     help="chain mode: CTAs of the partial-sum launch on non-last ranks")
     ap.add_argument("--chain-consumer-grid", type=int, default=0,
                     help="chain mode: CTAs of the fused launch on the last rank")
     ap.add_argument("--mode", default="auto",
-                    choices=["auto", "p2p", "push", "chain", "nccl", "allreduce", "hier"],
+                    choices=["auto", "p2p", "push", "sched", "chain", "nccl", "allreduce", "hier"],
                     help="N>1 exchange of the 8-worker job: chained (chain), owner-sharded "
                          "all-store (push) or peer-load (p2p) kernels, NCCL send/recv (nccl), "
                          "NCCL all-reduce baseline (allreduce); hier: hierarchical reduction, "
@@ -466,7 +474,8 @@ def bench_multi(args, mname, N, cb):
     import torch
     import torch.distributed as dist
     from paper_1805_07891_b200.sharded import (AllReduceBaseline, ChainShardedPHub, HierPHub,
-                                               P2PShardedPHub, PushShardedPHub, ShardedPHub)
+                                               P2PShardedPHub, PushShardedPHub, SchedShardedPHub,
+                                               ShardedPHub)
     from workloads import grad_stream, manifest
     from workloads.generate import values_torch
 
@@ -480,8 +489,9 @@ def bench_multi(args, mname, N, cb):
         args.mode = "chain" if G == 2 else "push"
     hier = args.mode == "hier"
     push = args.mode == "push"
-    chain = args.mode in ("chain", "hier", "push")   # the whole round is one exchange() call
-    p2p = args.mode in ("p2p", "chain", "hier", "push")
+    sched = args.mode == "sched"
+    chain = args.mode in ("chain", "hier", "push", "sched")   # the round is one exchange() call
+    p2p = args.mode in ("p2p", "chain", "hier", "push", "sched")
     ar = args.mode == "allreduce"
     NT = N * G if hier else N                   # workers in the job
     try:
@@ -491,6 +501,11 @@ def bench_multi(args, mname, N, cb):
         elif push:
             sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local,
                                  block=args.push_block)
+        elif sched:
+            fl = lambda x: [float(v) for v in x.split(",")] if x else None  # noqa: E731
+            sh = SchedShardedPHub(sizes, N, chunk_size_bytes=cb, device=local,
+                                  block=args.sched_block, lag=args.sched_lag,
+                                  weights=fl(args.sched_weights), raw_frac=fl(args.sched_raw))
         elif chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
                                   sync=args.chain_sync, block=args.chain_block)
@@ -598,6 +613,8 @@ def bench_multi(args, mname, N, cb):
             [hub.owner_range(o) for o in range(G)], Ep, rank)
     elif push:   # same bytes as the owner-sharded P2P exchange (plan), all as stores
         pass
+    elif sched:  # RAW slices + CHAIN partials + final sums + replica stores (byte model)
+        mine["out"], mine["in"] = sh.nvlink_bytes()
     elif chain:  # one partial per link per round; the last rank stores w' into G-1 replicas
         from paper_1805_07891_b200.sharded import chain_nvlink_bytes
         mine["out"], mine["in"] = chain_nvlink_bytes(Ep, G, rank)
@@ -715,6 +732,15 @@ def bench_multi(args, mname, N, cb):
                                 "over NVLink and sums its own range over all workers in worker "
                                 "order -> Nesterov -> w' into every replica (all NVLink traffic "
                                 "as stores)") if push else
+                               (f"M3 (full exchange) sched: one ticket-ordered launch per GPU "
+                                f"executes its item program -- per owner range a RAW part "
+                                f"(raw worker slices stored into the owner) and a CHAIN part "
+                                f"(rank-by-rank worker-order partials, finished sum stored into "
+                                f"the owner), mixed per owner so the busiest NVLink port moves "
+                                f"the fewest bytes; owner shares {[round(x, 4) for x in sh.weights]}"
+                                f", RAW fractions {[round(x, 4) for x in sh.raw_frac]}, "
+                                f"{args.sched_block}-element blocks, lag {args.sched_lag}")
+                               if sched else
                                (f"M3 (full exchange) chain: rank-ordered partial sums over "
                                 f"NVLink, last rank fused Nesterov + replica stores, " +
                                 (f"one launch per rank streamed by per-block device flags "
@@ -750,6 +776,8 @@ def bench_multi(args, mname, N, cb):
                                      "end barrier)") if hier else
                                     ("push exchange round (k_hier worker-order, incl. the end "
                                      "barrier)") if push else
+                                    ("scheduled exchange round (k_sched, incl. the end "
+                                     "barrier)") if sched else
                                     ("chained exchange round (partial-sum + fused kernels, "
                                      "incl. barriers)") if chain else
                                     ("fused exchange kernel (k_flat with peer loads/stores), "

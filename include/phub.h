@@ -397,6 +397,99 @@ phub_status phub_hier_beneficial(int32_t workers_per_rack, int32_t racks, double
                                  double b_wkr, double b_core, int32_t cross_rack,
                                  int32_t* beneficial, double* lhs, double* rhs);
 
+/* ---------------------------------------------------------------------------
+ * Scheduled owner-sharded exchange ("chunks ...
+ * assigned to owners", P:698 streaming aggregation; reading R3 worker order)
+ *
+ * One persistent launch per GPU executes a host-built ITEM PROGRAM for the
+ * N-worker job whose workers are hosted in rank order (rank p hosts global
+ * workers [p*W, (p+1)*W)).  The padded model is cut into owner ranges
+ * [bounds[o], bounds[o+1]); each owner range into a RAW part [bounds[o],
+ * split[o]) and a CHAIN part [split[o], bounds[o+1]):
+ *   RAW part:   every other rank stores its W workers' raw slices into the
+ *               owner's raw inbox; the owner sums all N workers in worker
+ *               order (CONSUME_RAW) -- the push exchange;
+ *   CHAIN part: the worker-order sum is built rank by rank: rank 0 sums its
+ *               workers from +0 and stores the partial into rank 1's inbox,
+ *               rank p adds its workers to the incoming partial and stores it
+ *               into rank p+1's, the last rank completes the sum and either
+ *               runs the Nesterov step itself (owner == last rank) or stores
+ *               s into the owner's inbox (CONSUME_FINAL).
+ * Both give the flat worker-order sum s = ((+0 + g_0) + g_1) + ... bit for
+ * bit (R3, R4).  The split of each owner range trades NVLink bytes between
+ * ports: all-RAW is the push exchange (byte-optimal at W = 1), all-CHAIN on
+ * the last owner the chained exchange (byte-optimal at G = 2); in between a
+ * mix lowers the busiest port's bytes (G = 4, W = 2: 1.79 vs 2.25 model sizes,
+ * scripts/sched_lp.py).  Every NAG item stores w' locally and into every
+ * replica registered with phub_set_replicas.
+ * ------------------------------------------------------------------------- */
+enum {
+    PHUB_ITEM_RAW_PUSH = 1,      /* store local workers' raw slices of [lo,hi) into rank dst's
+                                    raw inbox, raise dst's flag signal_flag                   */
+    PHUB_ITEM_CHAIN = 2,         /* [wait flag] partial(inbox or +0) + local workers; dst >= 0:
+                                    store into rank dst's inbox and raise its signal_flag;
+                                    dst < 0: Nesterov here                                   */
+    PHUB_ITEM_CONSUME_RAW = 3,   /* wait flags wait_flag + q (q != rank); worker-order sum of
+                                    local workers and raw inbox slots; Nesterov              */
+    PHUB_ITEM_CONSUME_FINAL = 4  /* wait flag; s = inbox; Nesterov                            */
+};
+typedef struct {
+    uint64_t lo, hi;             /* padded-layout element range, multiples of 8              */
+    uint64_t base, len;          /* RAW items: the owner's raw part [base, base + len)       */
+    uint32_t type;               /* PHUB_ITEM_*                                              */
+    int32_t dst;                 /* destination rank, or -1                                  */
+    uint32_t wait_flag;          /* index into this rank's flags, UINT32_MAX = none          */
+    uint32_t signal_flag;        /* index into dst's flags                                   */
+} phub_sched_item;
+
+/* Host-only planner: the item program of `rank` (ticket order) for `ranks`
+ * GPUs with `workers_per_rank` workers each.  bounds[ranks+1] (bounds[0] = 0,
+ * non-decreasing, bounds[ranks] = E_padded), split[ranks] (bounds[o] <=
+ * split[o] <= bounds[o+1]); every bound and split a multiple of 8.  Parts are
+ * cut into blocks of block_elems (multiple of 2048).  Items are ordered by a
+ * key every rank shares -- (normalized progress of the block in its part +
+ * stage * lag, stage) -- so each item waits only on items with strictly
+ * smaller keys on other ranks: deadlock-free with any number of co-resident
+ * CTAs taking tickets in order.  lag_blocks shifts the chain
+ * stages and consumers by that many blocks of progress (pipeline fill).
+ * Flag layout (identical on every rank, *num_flags entries, zero initially):
+ * chain block c: [c] partial arrival, [C + c] final arrival; raw block j
+ * (numbered owner-major): [2C + j*ranks + q] slices of rank q arrived.
+ * *count receives the item count (cap may be 0: count query; LENGTH_MISMATCH
+ * if cap < count).  INVALID_ARGUMENT on bad geometry. */
+phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_rank,
+                            const uint64_t* bounds, const uint64_t* split, uint64_t block_elems,
+                            uint64_t lag_blocks, phub_sched_item* out, uint64_t cap,
+                            uint64_t* count, uint32_t* num_flags);
+
+/* Upload an item program (host array) to the context's device; validated
+ * (types, ranges within E_padded and multiples of 8, dst < ranks, flag
+ * indices < num_flags).  Replaces the previous program. */
+phub_status phub_sched_load(phub_ctx ctx, int32_t ranks, int32_t rank, const phub_sched_item* items,
+                            uint64_t count, uint32_t num_flags);
+
+/* One round of the loaded program (one launch on `stream`).  Requires the
+ * context's W = N workers pushed whole-model (PHUB_ALL_KEYS, BORROW, 32-B
+ * aligned) and num_owners == 1 (the items, not the context's owner table,
+ * say which ranges this rank optimizes; v is meaningful on those ranges).
+ *   inbox[q]     rank q's partial/sum inbox (E_padded floats, 32-B aligned;
+ *                peer-mapped for q != rank), addressed by padded element.
+ *   raw_inbox[q] rank q's raw inbox: slot (src rank s, worker k) of owner q's
+ *                raw part at raw_inbox[q] + ((s*W + k)*len + (x - base)).
+ *   flags[q]     rank q's flags (num_flags uint32, never reset).
+ *   epoch        1, 2, 3, ... strictly increasing per round (flags hold it).
+ * Bounded waits as phub_sync (sticky PHUB_ERR_SYNC_TIMEOUT; a skipped item
+ * never raises its flag).  The caller orders rounds (a barrier before: every
+ * replica and inbox free; after: replicas complete).  Completes the
+ * iteration. */
+typedef struct {
+    float* const* inbox;
+    float* const* raw_inbox;
+    uint32_t* const* flags;
+    uint32_t epoch;
+} phub_sched;
+phub_status phub_sched_exchange(phub_ctx ctx, const phub_sched* s, void* stream);
+
 /* Shared device allocations that can be exported to peer processes.
  * phub_alloc_shared: cudaMalloc of `bytes` on `device` (whole allocation, so an
  * IPC handle maps exactly this buffer).  phub_free_shared releases it. */

@@ -34,6 +34,9 @@ PHUB_CROSS_RACK_SHARDED, PHUB_CROSS_RACK_RING = 0, 1
 (PHUB_KERNEL_AUTO, PHUB_KERNEL_FLAT, PHUB_KERNEL_TILES, PHUB_KERNEL_FLAT128,
  PHUB_KERNEL_WIDE, PHUB_KERNEL_BULK) = range(6)
 PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS, PHUB_CACHE_RESIDENT = 0, 1, 2
+(PHUB_ITEM_RAW_PUSH, PHUB_ITEM_CHAIN, PHUB_ITEM_CONSUME_RAW,
+ PHUB_ITEM_CONSUME_FINAL) = 1, 2, 3, 4
+PHUB_NO_FLAG = 0xFFFFFFFF
 
 
 class phub_chunk(C.Structure):
@@ -52,6 +55,17 @@ class phub_hier(C.Structure):
                 ("inbox", C.POINTER(C.c_void_p)), ("peer_inbox", C.POINTER(C.c_void_p)),
                 ("flags", C.c_void_p), ("peer_flags", C.POINTER(C.c_void_p)),
                 ("epoch", C.c_uint32), ("worker_order", C.c_int32)]
+
+
+class phub_sched_item(C.Structure):
+    _fields_ = [("lo", C.c_uint64), ("hi", C.c_uint64), ("base", C.c_uint64), ("len", C.c_uint64),
+                ("type", C.c_uint32), ("dst", C.c_int32), ("wait_flag", C.c_uint32),
+                ("signal_flag", C.c_uint32)]
+
+
+class phub_sched(C.Structure):
+    _fields_ = [("inbox", C.POINTER(C.c_void_p)), ("raw_inbox", C.POINTER(C.c_void_p)),
+                ("flags", C.POINTER(C.c_void_p)), ("epoch", C.c_uint32)]
 
 
 class phub_config(C.Structure):
@@ -117,6 +131,12 @@ _SIGS = {
     "phub_set_option": (C.c_int, [phub_ctx, C.c_int32, C.c_int64]),
     "phub_set_replicas": (C.c_int, [phub_ctx, C.POINTER(C.c_void_p), C.c_int32]),
     "phub_hier_exchange": (C.c_int, [phub_ctx, C.c_void_p, C.c_void_p]),
+    "phub_sched_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _u64p, _u64p, C.c_uint64,
+                                  C.c_uint64, C.c_void_p, C.c_uint64, _u64p,
+                                  C.POINTER(C.c_uint32)]),
+    "phub_sched_load": (C.c_int, [phub_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_uint64,
+                                  C.c_uint32]),
+    "phub_sched_exchange": (C.c_int, [phub_ctx, C.c_void_p, C.c_void_p]),
     "phub_alloc_shared": (C.c_int, [C.c_int32, C.c_uint64, C.POINTER(C.c_void_p)]),
     "phub_free_shared": (C.c_int, [C.c_int32, C.c_void_p]),
     "phub_ipc_get_handle": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p]),
@@ -364,6 +384,33 @@ def phub_hier_exchange(ctx, num_racks: int, block: int, inbox, peer_inbox, flags
     ib, pib, pf = arr(inbox), arr(peer_inbox), arr(peer_flags)     # alive across the call
     h = phub_hier(R, int(block), ib, pib, flags or None, pf, int(epoch), int(bool(worker_order)))
     _check(_lib.phub_hier_exchange(ctx, C.byref(h), stream), "phub_hier_exchange", ctx)
+
+
+def phub_sched_plan(ranks: int, rank: int, workers_per_rank: int, bounds, split,
+                    block_elems: int, lag_blocks: int = 0):
+    """Item program of `rank` (phub.h phub_sched_plan): (items array, num_flags)."""
+    b = (C.c_uint64 * len(bounds))(*[int(x) for x in bounds])
+    sp = (C.c_uint64 * len(split))(*[int(x) for x in split])
+    n, nf = C.c_uint64(), C.c_uint32()
+    args = (ranks, rank, workers_per_rank, b, sp, int(block_elems), int(lag_blocks))
+    _check(_lib.phub_sched_plan(*args, None, 0, C.byref(n), C.byref(nf)), "phub_sched_plan", None)
+    items = (phub_sched_item * n.value)()
+    _check(_lib.phub_sched_plan(*args, items, n.value, C.byref(n), C.byref(nf)),
+           "phub_sched_plan", None)
+    return items, nf.value
+
+
+def phub_sched_load(ctx, ranks: int, rank: int, items, num_flags: int):
+    _check(_lib.phub_sched_load(ctx, ranks, rank, items, len(items), num_flags),
+           "phub_sched_load", ctx)
+
+
+def phub_sched_exchange(ctx, inbox, raw_inbox, flags, epoch: int, stream: int = 0):
+    """One scheduled round (phub.h phub_sched_exchange); pointer lists per rank."""
+    R = len(inbox)
+    arr = lambda xs: (C.c_void_p * R)(*[x or None for x in xs])  # noqa: E731
+    s = phub_sched(arr(inbox), arr(raw_inbox), arr(flags), int(epoch))
+    _check(_lib.phub_sched_exchange(ctx, C.byref(s), stream), "phub_sched_exchange", ctx)
 
 
 def phub_alloc_shared(device: int, nbytes: int) -> int:

@@ -98,6 +98,12 @@ struct phub_ctx_s {
     int flat_grid[2][2] = {{0, 0}, {0, 0}};   // [vec8?][agg]
     int blocks_occ[2][phub::kMaxWorkers + 1] = {};      // resident CTAs/SM [nag][nw]
     int hier_occ[2] = {0, 0};                          // resident CTAs/SM of k_hier [worker_order]
+    // scheduled exchange (phub_sched_load / phub_sched_exchange)
+    phub::SchedItem* d_items = nullptr;
+    uint64_t n_items = 0;
+    int sched_ranks = 0, sched_rank = -1;
+    uint32_t sched_flags = 0;
+    int sched_occ = 0;
     uint64_t iteration = 0;
     int launches = 0;
     uint64_t launches_total = 0;
@@ -319,6 +325,7 @@ static void free_ctx(phub_ctx c) {
     cudaFree(c->d_tiles);
     cudaFree(c->d_base);
     cudaFree(c->d_sync);
+    cudaFree(c->d_items);
     if (c->h_err) cudaFreeHost(c->h_err);
     delete c;
 }
@@ -1247,6 +1254,220 @@ phub_status phub_hier_exchange(phub_ctx c, const phub_hier* h, void* stream) {
     cudaError_t e = phub::launch_hier(a, grid, static_cast<cudaStream_t>(stream), &c->launches);
     c->launches_total += (uint64_t)c->launches;
     if (e != cudaSuccess) return c->cuda_fail(e, "hierarchical exchange launch");
+    end_iteration(c);
+    return PHUB_OK;
+}
+
+// ------------------------------------------- scheduled exchange (DESIGN 8.6)
+static_assert(sizeof(phub_sched_item) == sizeof(phub::SchedItem), "item layout");
+static_assert(offsetof(phub_sched_item, type) == offsetof(phub::SchedItem, type), "item layout");
+static_assert(offsetof(phub_sched_item, signal_flag) == offsetof(phub::SchedItem, signal_flag),
+              "item layout");
+
+phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_rank,
+                            const uint64_t* bounds, const uint64_t* split, uint64_t block_elems,
+                            uint64_t lag_blocks, phub_sched_item* out, uint64_t cap,
+                            uint64_t* count, uint32_t* num_flags) {
+    const int G = ranks, p = rank, W = workers_per_rank;
+    if (G < 1 || G > phub::kMaxRacks || p < 0 || p >= G || W < 1 || W > phub::kMaxWorkers ||
+        !bounds || !split || !count || !block_elems || block_elems % 2048 || (cap && !out))
+        return PHUB_ERR_INVALID_ARGUMENT;
+    if (bounds[0] != 0) return PHUB_ERR_INVALID_ARGUMENT;
+    for (int o = 0; o < G; ++o)
+        if (bounds[o + 1] < bounds[o] || bounds[o] % 8 || bounds[o + 1] % 8 || split[o] % 8 ||
+            split[o] < bounds[o] || split[o] > bounds[o + 1])
+            return PHUB_ERR_INVALID_ARGUMENT;
+    struct Blk { int o; uint64_t lo, hi; uint64_t j, J; };
+    std::vector<Blk> chain, raw;
+    for (int o = 0; o < G; ++o) {                     // chain parts, address order
+        const uint64_t b = split[o], e = bounds[o + 1];
+        for (uint64_t lo = b; lo < e; lo += block_elems)
+            chain.push_back({o, lo, std::min(lo + block_elems, e), 0, 0});
+    }
+    for (int o = 0; o < G; ++o) {                     // raw parts, owner-major
+        const uint64_t b = bounds[o], e = split[o];
+        const uint64_t J = (e - b + block_elems - 1) / block_elems;
+        for (uint64_t j = 0; j < J; ++j)
+            raw.push_back({o, b + j * block_elems, std::min(b + (j + 1) * block_elems, e), j, J});
+    }
+    const uint64_t C = chain.size(), R = raw.size();
+    const uint64_t nflags = 2 * C + R * (uint64_t)G;
+    if (nflags >= 0xffffffffull) return PHUB_ERR_INVALID_ARGUMENT;
+    // (progress key, stage, item): progress = fraction of the block's part done
+    // before it, plus stage * lag; the same doubles on every rank
+    struct Keyed { double t; int stage; phub_sched_item it; };
+    std::vector<Keyed> v;
+    const double lag_c = C ? (double)lag_blocks / (double)C : 0.0;
+    for (uint64_t c = 0; c < C; ++c) {
+        const Blk& b = chain[c];
+        const double t = (double)c / (double)C;
+        phub_sched_item it{};
+        it.lo = b.lo;
+        it.hi = b.hi;
+        it.type = PHUB_ITEM_CHAIN;
+        it.wait_flag = p > 0 ? (uint32_t)c : phub::kNoFlag;
+        if (p < G - 1) {
+            it.dst = p + 1;                           // partial into the next rank's inbox
+            it.signal_flag = (uint32_t)c;
+        } else if (b.o == G - 1) {
+            it.dst = -1;                              // sum complete here: Nesterov
+            it.signal_flag = phub::kNoFlag;
+        } else {
+            it.dst = b.o;                             // s into the owner's inbox
+            it.signal_flag = (uint32_t)(C + c);
+        }
+        v.push_back({t + p * lag_c, p, it});
+        if (p == b.o && b.o != G - 1) {
+            phub_sched_item f{};
+            f.lo = b.lo;
+            f.hi = b.hi;
+            f.type = PHUB_ITEM_CONSUME_FINAL;
+            f.dst = -1;
+            f.wait_flag = (uint32_t)(C + c);
+            f.signal_flag = phub::kNoFlag;
+            v.push_back({t + G * lag_c, G, f});
+        }
+    }
+    for (uint64_t jg = 0; jg < R; ++jg) {
+        const Blk& b = raw[jg];
+        const double t = (double)b.j / (double)b.J;
+        phub_sched_item it{};
+        it.lo = b.lo;
+        it.hi = b.hi;
+        it.base = bounds[b.o];
+        it.len = split[b.o] - bounds[b.o];
+        if (p != b.o) {
+            it.type = PHUB_ITEM_RAW_PUSH;
+            it.dst = b.o;
+            it.wait_flag = phub::kNoFlag;
+            it.signal_flag = (uint32_t)(2 * C + jg * G + p);
+            v.push_back({t, 0, it});
+        } else {
+            it.type = PHUB_ITEM_CONSUME_RAW;
+            it.dst = -1;
+            it.wait_flag = (uint32_t)(2 * C + jg * G);
+            it.signal_flag = phub::kNoFlag;
+            v.push_back({t + (double)lag_blocks / (double)b.J, 1, it});
+        }
+    }
+    std::stable_sort(v.begin(), v.end(), [](const Keyed& a, const Keyed& b) {
+        return a.t < b.t || (a.t == b.t && a.stage < b.stage);
+    });
+    *count = v.size();
+    if (num_flags) *num_flags = (uint32_t)nflags;
+    if (cap == 0) return PHUB_OK;
+    if (cap < v.size()) return PHUB_ERR_LENGTH_MISMATCH;
+    for (size_t i = 0; i < v.size(); ++i) out[i] = v[i].it;
+    return PHUB_OK;
+}
+
+phub_status phub_sched_load(phub_ctx c, int32_t ranks, int32_t rank, const phub_sched_item* items,
+                            uint64_t count, uint32_t num_flags) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (phub_status st0 = c->guard()) return st0;
+    if (ranks < 1 || ranks > phub::kMaxRacks || rank < 0 || rank >= ranks || (count && !items))
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "bad ranks / rank / items");
+    for (uint64_t t = 0; t < count; ++t) {
+        const phub_sched_item& it = items[t];
+        const bool raw = it.type == PHUB_ITEM_RAW_PUSH || it.type == PHUB_ITEM_CONSUME_RAW;
+        bool ok = it.type >= PHUB_ITEM_RAW_PUSH && it.type <= PHUB_ITEM_CONSUME_FINAL &&
+                  it.lo % 8 == 0 && it.hi % 8 == 0 && it.lo < it.hi && it.hi <= c->E_pad &&
+                  it.dst >= -1 && it.dst < ranks;
+        if (raw) ok = ok && it.base % 8 == 0 && it.lo >= it.base && it.hi <= it.base + it.len;
+        if (it.type == PHUB_ITEM_RAW_PUSH)
+            ok = ok && it.dst >= 0 && it.dst != rank && it.signal_flag < num_flags;
+        if (it.type == PHUB_ITEM_CHAIN)
+            ok = ok && (it.wait_flag == phub::kNoFlag || it.wait_flag < num_flags) &&
+                 (it.dst < 0 || (it.dst != rank && it.signal_flag < num_flags));
+        if (it.type == PHUB_ITEM_CONSUME_RAW)
+            ok = ok && it.dst == -1 && (uint64_t)it.wait_flag + ranks <= num_flags;
+        if (it.type == PHUB_ITEM_CONSUME_FINAL) ok = ok && it.dst == -1 && it.wait_flag < num_flags;
+        if (!ok)
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "item %llu: invalid (type %u, [%llu, %llu), "
+                           "dst %d)", (unsigned long long)t, it.type, (unsigned long long)it.lo,
+                           (unsigned long long)it.hi, it.dst);
+    }
+    DeviceGuard g(c->device);
+    phub::SchedItem* d = nullptr;
+    if (count) {
+        cudaError_t e = cudaMalloc(&d, count * sizeof(phub::SchedItem));
+        if (e == cudaSuccess) e = cudaMemcpy(d, items, count * sizeof(phub::SchedItem),
+                                             cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(d);
+            return c->cuda_fail(e, "sched item upload");
+        }
+    }
+    cudaFree(c->d_items);
+    c->d_items = d;
+    c->n_items = count;
+    c->sched_ranks = ranks;
+    c->sched_rank = rank;
+    c->sched_flags = num_flags;
+    return PHUB_OK;
+}
+
+phub_status phub_sched_exchange(phub_ctx c, const phub_sched* s, void* stream) {
+    if (!c) return PHUB_ERR_INVALID_ARGUMENT;
+    if (phub_status st0 = c->guard()) return st0;
+    if (!s || s->epoch == 0) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "epoch must be >= 1");
+    if (c->sched_rank < 0) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "no item program loaded");
+    if (c->G != 1 || c->N > phub::kMaxWorkers || c->ce % 8)
+        return c->fail(PHUB_ERR_UNSUPPORTED, "scheduled exchange needs num_owners == 1, chunks of "
+                       "a multiple of 32 B and <= %d local workers", phub::kMaxWorkers);
+    const int R = c->sched_ranks, me = c->sched_rank;
+    if (!s->inbox || !s->raw_inbox || !s->flags)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "inbox / raw_inbox / flags arrays required");
+    for (int q = 0; q < R; ++q)
+        if (reinterpret_cast<uintptr_t>(s->inbox[q]) % 32 ||
+            reinterpret_cast<uintptr_t>(s->raw_inbox[q]) % 32 ||
+            reinterpret_cast<uintptr_t>(s->flags[q]) % 4 || (R > 1 && !s->flags[q]))
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "rank %d: inboxes must be 32-B aligned, "
+                           "flags 4-B aligned and non-null", q);
+    if (c->got_count != (uint64_t)c->K * c->N)
+        return c->fail(PHUB_ERR_INCOMPLETE, "%llu of %llu (worker,key) pushes received (S:181)",
+                       (unsigned long long)c->got_count,
+                       (unsigned long long)((uint64_t)c->K * c->N));
+    if (c->range_cursor != UINT64_MAX || c->done_count)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "iteration is being aggregated otherwise");
+    phub::SchedArgs a{};
+    for (int w = 0; w < c->N; ++w) {
+        const uintptr_t b0 = c->base[(size_t)w * c->K];
+        for (int k = 1; k < c->K; ++k)
+            if (c->base[(size_t)w * c->K + k] != b0 || b0 % 32)
+                return c->fail(PHUB_ERR_UNSUPPORTED, "worker %d: whole-model 32-B aligned push "
+                               "required", w);
+        a.g[w] = reinterpret_cast<const float*>(b0);
+    }
+    a.nw = c->N;
+    a.R = R;
+    a.rank = me;
+    a.w = c->d_w;
+    a.v = c->d_v;
+    a.agg = c->keep_agg ? c->d_agg : nullptr;
+    a.lr = c->lr;
+    a.mu = c->mu;
+    a.rescale = c->rescale;
+    a.nrep = (int)c->replicas.size();
+    for (int r = 0; r < a.nrep; ++r) a.rep[r] = c->replicas[r];
+    a.items = c->d_items;
+    a.nitems = c->n_items;
+    for (int q = 0; q < R; ++q) {
+        a.inbox[q] = s->inbox[q];
+        a.raw_inbox[q] = s->raw_inbox[q];
+        a.flags[q] = s->flags[q];
+    }
+    a.epoch = s->epoch;
+    a.ticket = c->d_sync + 3;
+    a.timeouts = c->d_sync + 1;
+    a.err_host = c->d_err;
+    DeviceGuard g(c->device);
+    c->launches = 0;
+    if (!c->sched_occ) c->sched_occ = phub::sched_blocks_per_sm(c->N);
+    const int grid = c->grid_override ? c->grid_override : c->num_sms * c->sched_occ;
+    cudaError_t e = phub::launch_sched(a, grid, static_cast<cudaStream_t>(stream), &c->launches);
+    c->launches_total += (uint64_t)c->launches;
+    if (e != cudaSuccess) return c->cuda_fail(e, "scheduled exchange launch");
     end_iteration(c);
     return PHUB_OK;
 }

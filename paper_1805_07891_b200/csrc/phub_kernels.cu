@@ -797,6 +797,192 @@ void* pick_hier_wo(int nw) {
 }
 void* pick_hier(int nw, bool wo) { return wo ? pick_hier_wo<true>(nw) : pick_hier_wo<false>(nw); }
 
+// ------------------------------------------------ scheduled exchange (8.6)
+// One persistent launch per GPU walks the host-built item program in ticket
+// order (phub_sched_plan): RAW_PUSH, CHAIN (first / middle / last stage of the
+// rank-by-rank worker-order partial sum), CONSUME_RAW, CONSUME_FINAL.  Every
+// item waits only on items of other ranks with strictly smaller keys in the
+// shared order, and tickets are taken in that order, so a waited-on item has
+// always been taken by a running CTA: no deadlock with co-resident CTAs (the
+// k_hier argument).  Waits are bounded; a skipped item never
+// raises its flag, so downstream stages time out too.
+
+// acc += g_0, g_1, ... (this rank's workers, in order), batches of 4 loads
+template <int NW>
+__device__ __forceinline__ void sched_local(const SchedArgs& a, uint64_t i, float acc[8]) {
+    const int nw = NW > 0 ? NW : a.nw;
+#pragma unroll
+    for (int k0 = 0; k0 < (NW > 0 ? NW : kMaxWorkers); k0 += 4) {
+        if (k0 >= nw) break;
+        V8 gv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k0 + k < nw) gv[k] = ld_grad(reinterpret_cast<const V8*>(a.g[k0 + k]) + i);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k0 + k < nw) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], gv[k].x[j]);
+            }
+    }
+}
+
+// s = acc: Nesterov on vector i, w' stored locally and into every replica
+__device__ __forceinline__ void sched_nag(const SchedArgs& a, uint64_t i, const float acc[8]) {
+    V8* w = reinterpret_cast<V8*>(a.w);
+    V8* v = reinterpret_cast<V8*>(a.v);
+    V8 wv = ld_state<PHUB_CACHE_BYPASS>(w + i);
+    V8 vv = ld_state<PHUB_CACHE_BYPASS>(v + i);
+    V8 sv;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        sv.x[e] = acc[e];
+        float s = acc[e];
+        nag(s, wv.x[e], vv.x[e], a.lr, a.mu, a.rescale);
+    }
+    st_stream(w + i, wv);
+    st_stream(v + i, vv);
+    if (a.agg) st_stream(reinterpret_cast<V8*>(a.agg) + i, sv);
+    for (int r = 0; r < a.nrep; ++r) reinterpret_cast<V8*>(a.rep[r])[i] = wv;
+}
+
+// Thread 0: bounded wait for flags[f] >= epoch (0 = gave up or abandoned)
+__device__ __forceinline__ int sched_wait(const SchedArgs& a, const uint32_t* f, const uint64_t t0) {
+    volatile uint32_t* abandoned = a.timeouts + 1;
+    while (ld_acquire_sys(f) < a.epoch) {
+        if (*abandoned >= a.epoch) return 0;
+        if (globaltimer_ns() - t0 > 2000000000ull) {
+            record_timeout(a.timeouts, a.err_host, a.epoch);
+            return 0;
+        }
+        __nanosleep(100);
+    }
+    return 1;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ SchedArgs a) {
+    __shared__ uint64_t s_t;
+    __shared__ int s_ok;
+    const uint32_t* my_flags = a.flags[a.rank];
+    for (;;) {
+        if (threadIdx.x == 0) s_t = atomicAdd(a.ticket, 1u);
+        __syncthreads();
+        const uint64_t t = s_t;
+        if (t >= a.nitems) break;
+        const SchedItem it = a.items[t];
+        if (threadIdx.x == 0) {
+            int good = 1;
+            const uint64_t t0 = globaltimer_ns();
+            if (it.type == PHUB_ITEM_CONSUME_RAW) {
+                for (int q = 0; q < a.R && good; ++q)
+                    if (q != a.rank) good = sched_wait(a, my_flags + it.wait_flag + q, t0);
+            } else if (it.wait_flag != kNoFlag) {
+                good = sched_wait(a, my_flags + it.wait_flag, t0);
+            }
+            s_ok = good;
+        }
+        __syncthreads();
+        const bool ok = s_ok != 0;
+        const uint64_t lo = it.lo / 8, hi = it.hi / 8;
+        if (ok) {
+            if (it.type == PHUB_ITEM_RAW_PUSH) {
+                // worker k of this rank -> slot (rank, k) of owner dst's raw part
+                float* dst = a.raw_inbox[it.dst];
+                const int nw = NW > 0 ? NW : a.nw;
+                for (uint64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+                    const uint64_t x = 8 * i - it.base;
+                    for (int k0 = 0; k0 < nw; k0 += 4) {
+                        V8 gv[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (k0 + k < nw) gv[k] = ld_grad(reinterpret_cast<const V8*>(a.g[k0 + k]) + i);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (k0 + k < nw)
+                                *reinterpret_cast<V8*>(
+                                    dst + ((uint64_t)(a.rank * nw + k0 + k) * it.len + x)) = gv[k];
+                    }
+                }
+            } else if (it.type == PHUB_ITEM_CHAIN) {
+                const bool first = it.wait_flag == kNoFlag;
+                const V8* in = reinterpret_cast<const V8*>(a.inbox[a.rank]);
+                for (uint64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+                    float acc[8];
+                    if (first) {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc[e] = 0.0f;           // +0 (R4)
+                    } else {
+                        const V8 p = ld_coherent(in + i);                      // ranks 0..p-1
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) acc[e] = p.x[e];
+                    }
+                    sched_local<NW>(a, i, acc);
+                    if (it.dst >= 0) {
+                        V8 out;
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) out.x[e] = acc[e];
+                        reinterpret_cast<V8*>(a.inbox[it.dst])[i] = out;
+                    } else {
+                        sched_nag(a, i, acc);
+                    }
+                }
+            } else if (it.type == PHUB_ITEM_CONSUME_RAW) {
+                const int nw = NW > 0 ? NW : a.nw;
+                const float* rin = a.raw_inbox[a.rank];
+                for (uint64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+                    const uint64_t x = 8 * i - it.base;
+                    float acc[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+                    for (int q = 0; q < a.R; ++q) {                        // worker order (R3)
+                        if (q == a.rank) {
+                            sched_local<NW>(a, i, acc);
+                        } else {
+                            for (int k = 0; k < nw; ++k) {
+                                const V8 r = ld_coherent(reinterpret_cast<const V8*>(
+                                    rin + ((uint64_t)(q * nw + k) * it.len + x)));
+#pragma unroll
+                                for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], r.x[e]);
+                            }
+                        }
+                    }
+                    sched_nag(a, i, acc);
+                }
+            } else {                                                   // CONSUME_FINAL
+                const V8* in = reinterpret_cast<const V8*>(a.inbox[a.rank]);
+                for (uint64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
+                    const V8 p = ld_coherent(in + i);
+                    float acc[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[e] = p.x[e];
+                    sched_nag(a, i, acc);
+                }
+            }
+        }
+        __syncthreads();                               // bar.sync + one fence (cumulative)
+        if (threadIdx.x == 0 && ok && it.dst >= 0 && it.signal_flag != kNoFlag) {
+            __threadfence_system();
+            st_release_sys(a.flags[it.dst] + it.signal_flag, a.epoch);
+        }
+    }
+    if (a.nrep) __threadfence_system();
+    if (threadIdx.x == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x - 1) {
+        a.ticket[0] = 0;
+        a.ticket[1] = 0;
+    }
+}
+
+void* pick_sched(int nw) {
+    switch (nw) {
+        case 1: return (void*)k_sched<1>;
+        case 2: return (void*)k_sched<2>;
+        case 4: return (void*)k_sched<4>;
+        case 8: return (void*)k_sched<8>;
+        default: return (void*)k_sched<0>;
+    }
+}
+
 // ------------------------------------------------ bulk-copy (TMA) staging
 // Variant with the loads taken off the register file: one producer thread per
 // CTA streams each tile's N gradient slices and the w, v slices into a
@@ -1085,6 +1271,20 @@ int hier_blocks_per_sm(int nw, bool worker_order) {
     return nb > 0 ? nb : 1;
 }
 
+int sched_blocks_per_sm(int nw) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pick_sched(nw), kThreads, 0) != cudaSuccess)
+        return 1;
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_sched(const SchedArgs& a, int grid, cudaStream_t s, int* launches) {
+    void* args[] = {const_cast<SchedArgs*>(&a)};
+    cudaError_t e = cudaLaunchKernel(pick_sched(a.nw), dim3(grid), dim3(kThreads), args, 0, s);
+    ++*launches;
+    return e;
+}
+
 cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launches) {
     void* args[] = {const_cast<HierArgs*>(&a)};
     cudaError_t e = cudaLaunchKernel(pick_hier(a.nw, a.worker_order != 0), dim3(grid),
@@ -1107,6 +1307,7 @@ cudaError_t preload_kernels() {
         fns.push_back(pick_blocks<false>(nw));
         fns.push_back(pick_hier(nw, true));
         fns.push_back(pick_hier(nw, false));
+        fns.push_back(pick_sched(nw));
         for (int vec : {4, 8})
             for (int cache : {PHUB_CACHE_ENABLED, PHUB_CACHE_BYPASS, PHUB_CACHE_RESIDENT})
                 for (bool agg : {false, true})

@@ -71,6 +71,39 @@ struct HierArgs {
 cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launches);
 int hier_blocks_per_sm(int nw, bool worker_order);
 
+// Scheduled exchange (phub_sched_exchange): one persistent
+// launch per GPU executes a host-built item program in ticket order.  The item
+// layout is phub_sched_item's (static_assert in phub_core.cpp).
+struct SchedItem {
+    uint64_t lo, hi, base, len;
+    uint32_t type;
+    int32_t dst;
+    uint32_t wait_flag, signal_flag;
+};
+constexpr uint32_t kNoFlag = 0xffffffffu;
+struct SchedArgs {
+    const float* g[kMaxWorkers];      // this rank's workers (padded-layout bases)
+    int nw;                           // W
+    int R, rank;
+    float* w;
+    float* v;
+    float* agg;                       // nullptr unless keep_aggregate
+    float lr, mu, rescale;
+    int nrep;
+    float* rep[kMaxReplicas];         // peer replicas receiving w' of every NAG item
+    const SchedItem* items;
+    uint64_t nitems;
+    float* inbox[kMaxRacks];          // rank q's partial/sum inbox (padded-based)
+    float* raw_inbox[kMaxRacks];      // rank q's raw inbox
+    uint32_t* flags[kMaxRacks];       // rank q's flags
+    uint32_t epoch;
+    uint32_t* ticket;                 // [0] next item, [1] CTAs done
+    uint32_t* timeouts;               // [0] expired waits, [1] abandoned epoch
+    volatile uint32_t* err_host;
+};
+cudaError_t launch_sched(const SchedArgs& a, int grid, cudaStream_t s, int* launches);
+int sched_blocks_per_sm(int nw);
+
 struct TileArgs {
     const Tile* tiles;
     uint64_t ntiles;

@@ -859,3 +859,237 @@ class PushShardedPHub(HierPHub):
         self.exchange(slot)
         for w in self.hosted:
             host_out[w].copy_(self.replica, non_blocking=True)
+
+
+# ------------------------------------------------- scheduled exchange (8.6)
+# Owner weights and RAW fractions per G (W = 8/G workers per GPU) from the
+# byte-balancing model of scripts/sched_lp.py: the busiest NVLink port moves
+# 1.000 / 1.769 / 1.789 / 1.750 model sizes at G = 2 / 3 / 4 / 8, vs 2.500 /
+# 2.667 / 2.250 / 1.750 for the push exchange (all RAW).
+SCHED_TABLE = {
+    2: ([0.0, 1.0], [0.0, 0.0]),
+    3: ([0.3846, 0.1538, 0.4616], [0.4, 0.0, 0.1667]),
+    4: ([0.2982, 0.193, 0.193, 0.3158], [0.5294, 0.0, 0.0, 0.1667]),
+    8: ([0.125] * 8, [1.0] * 8),
+}
+
+
+def sched_port_bytes(G: int, W: int, weights, raw_frac):
+    """Busiest-direction bytes (in model sizes) of every GPU's NVLink port for
+    owner shares `weights` and RAW fractions `raw_frac` (scripts/sched_lp.py's
+    byte model, plain Python): RAW -- W raw slices from every other rank into
+    the owner; CHAIN -- one partial per hop 0 -> 1 -> ... -> G-1, plus the
+    finished sum into the owner unless it is the last rank; w' of every share
+    into every other replica."""
+    inn, out = [0.0] * G, [0.0] * G
+    for o in range(G):
+        raw, ch = weights[o] * raw_frac[o], weights[o] * (1.0 - raw_frac[o])
+        for q in range(G):
+            if q != o:
+                inn[o] += W * raw
+                out[q] += W * raw
+                out[o] += weights[o]          # replica stores
+                inn[q] += weights[o]
+        for p in range(G - 1):
+            out[p] += ch
+            inn[p + 1] += ch
+        if o != G - 1:
+            out[G - 1] += ch
+            inn[o] += ch
+    return [max(i, x) for i, x in zip(inn, out)]
+
+
+def sched_geometry(key_sizes, chunk_size_bytes: int, G: int, weights, raw_frac):
+    """Owner bounds and RAW/CHAIN splits in the padded layout, snapped to chunk
+    starts so every chunk has exactly one owner."""
+    import bisect
+    Ep, offs, _ = capi.phub_plan_ranges(key_sizes, chunk_size_bytes, 1)
+    chunks, n = capi.phub_plan_chunks(key_sizes, chunk_size_bytes, 1, capi.PHUB_OWNER_CONTIG)
+    starts = sorted(int(offs[chunks[i].key_id]) + int(chunks[i].offset) for i in range(n)) + [Ep]
+
+    def snap(x, lo, hi):
+        i = bisect.bisect_left(starts, x)
+        cand = [s for s in starts[max(0, i - 1):i + 1] if lo <= s <= hi] or [lo]
+        return min(cand, key=lambda s: abs(s - x))
+
+    tot = float(sum(weights))
+    bounds, acc = [0], 0.0
+    for o in range(G - 1):
+        acc += weights[o]
+        bounds.append(snap(int(round(Ep * acc / tot)), bounds[-1], Ep))
+    bounds.append(Ep)
+    split = [snap(bounds[o] + int(round((bounds[o + 1] - bounds[o]) * raw_frac[o])),
+                  bounds[o], bounds[o + 1]) for o in range(G)]
+    return Ep, bounds, split
+
+
+class SchedShardedPHub(_DeviceWaitExchange):
+    """Scheduled owner-sharded exchange of the N-worker job (DESIGN.md 8.6;
+    phub_sched_plan / phub_sched_exchange): per owner range, a RAW part
+    exchanged like the push exchange and a CHAIN part summed rank by rank like
+    the chained exchange, mixed per SCHED_TABLE so that the busiest NVLink port
+    moves the fewest bytes.  One persistent launch per GPU executes this rank's
+    item program; every transfer is an NVLink store; the sum is the flat
+    worker-order sum (R3), bit-identical to the one-GPU result.  Workers are
+    hosted in rank order (rank r: global workers [r*W, (r+1)*W))."""
+
+    def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
+                 device=None, group=None, block=16384, lag=0, weights=None, raw_frac=None,
+                 nslots=2, keep_aggregate=False):
+        import torch
+        import torch.distributed as dist
+        from .phub import PHub, _CudaArray
+        self.group = group
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if num_workers % world:
+            raise ValueError(f"{num_workers} workers cannot be hosted evenly on {world} ranks")
+        self.rank, self.world, self.W = rank, world, num_workers // world
+        self.block, self.lag = int(block), int(lag)
+        if weights is None or raw_frac is None:
+            if world in SCHED_TABLE:
+                weights, raw_frac = SCHED_TABLE[world]
+            else:                                      # no table entry: the push exchange
+                weights, raw_frac = [1.0 / world] * world, [1.0] * world
+        self.weights, self.raw_frac = list(weights), list(raw_frac)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        dev = self.device
+        Ep, self.bounds, self.split = sched_geometry(key_sizes, chunk_size_bytes, world,
+                                                     self.weights, self.raw_frac)
+        self.hub = PHub(key_sizes, self.W, chunk_size_bytes=chunk_size_bytes, lr=lr,
+                        momentum=momentum, rescale=1.0 / num_workers, device=dev,
+                        keep_aggregate=keep_aggregate)
+        assert self.hub.E_padded == Ep
+        items, self.num_flags = capi.phub_sched_plan(world, rank, self.W, self.bounds, self.split,
+                                                     self.block, self.lag)
+        capi.phub_sched_load(self.hub.ctx, world, rank, items, self.num_flags)
+        self.nslots = int(nslots)
+        self._own = {(sl, k): capi.phub_alloc_shared(dev, 4 * Ep)
+                     for sl in range(self.nslots) for k in range(self.W)}
+        self._grads = {key: torch.as_tensor(_CudaArray(p, Ep, self), device=f"cuda:{dev}")
+                       for key, p in self._own.items()}
+        for t in self._grads.values():
+            t.zero_()
+        raw_len = self.split[rank] - self.bounds[rank]
+        self._inbox = capi.phub_alloc_shared(dev, 4 * Ep)
+        self._raw = capi.phub_alloc_shared(dev, 4 * world * self.W * max(raw_len, 8))
+        self._flags = capi.phub_alloc_shared(dev, 4 * max(self.num_flags, 1))
+        torch.as_tensor(_CudaArray(self._flags, max(self.num_flags, 1), self),
+                        device=f"cuda:{dev}").zero_()
+        h = capi.phub_ipc_get_handle
+        mine = (rank, h(dev, self._inbox), h(dev, self._raw), h(dev, self._flags),
+                h(dev, self.hub.weights_ptr()))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        allh.sort(key=lambda x: x[0])
+        self._opened = []
+        self.inbox, self.raw_inbox, self.flags = [0] * world, [0] * world, [0] * world
+        self.inbox[rank], self.raw_inbox[rank], self.flags[rank] = self._inbox, self._raw, self._flags
+        reps, err = [], None
+        try:
+            for q, ih, rh, fh, wh in allh:
+                if q == rank:
+                    continue
+                for hd in (ih, rh, fh, wh):
+                    self._opened.append(capi.phub_ipc_open(dev, hd))
+                self.inbox[q], self.raw_inbox[q], self.flags[q], pw = self._opened[-4:]
+                reps.append(pw)
+            capi.phub_set_replicas(self.hub.ctx, reps)
+        except capi.PhubError as ex:
+            err = ex
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32, device=f"cuda:{dev}")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            for p_ in self._opened:
+                try:
+                    capi.phub_ipc_close(dev, p_)
+                except capi.PhubError:
+                    pass
+            self._grads = {}
+            for p_ in list(self._own.values()) + [self._inbox, self._raw, self._flags]:
+                capi.phub_free_shared(dev, p_)
+            self.hub.close()
+            raise PeerMappingError(f"peer mapping failed on some rank ({err or 'other rank'})")
+        self.epoch = 0
+        self._flag = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
+        self.replica = self.hub.weights()
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+    @property
+    def hosted(self):
+        return [self.rank * self.W + k for k in range(self.W)]
+
+    def owned(self):
+        """[begin, end) of the padded layout this rank runs Nesterov on."""
+        return self.bounds[self.rank], self.bounds[self.rank + 1]
+
+    def gradients(self, slot: int = 0) -> dict:
+        return {self.rank * self.W + k: self._grads[(slot, k)] for k in range(self.W)}
+
+    def nvlink_bytes(self):
+        """(out, in) bytes of this rank per round under the byte model."""
+        G, W, Ep = self.world, self.W, self.hub.E_padded
+        sh = [(self.bounds[o + 1] - self.bounds[o]) / Ep for o in range(G)]
+        rf = [(self.split[o] - self.bounds[o]) / max(self.bounds[o + 1] - self.bounds[o], 1)
+              for o in range(G)]
+        inn = out = 0.0
+        me = self.rank
+        for o in range(G):
+            raw, ch = sh[o] * rf[o], sh[o] * (1 - rf[o])
+            if o == me:
+                inn += W * raw * (G - 1)
+                out += sh[o] * (G - 1)
+            else:
+                out += W * raw
+                inn += sh[o]
+            if me < G - 1:
+                out += ch
+            if me > 0:
+                inn += ch
+            if o != G - 1:
+                if me == G - 1:
+                    out += ch
+                if me == o:
+                    inn += ch
+        return int(4 * Ep * out), int(4 * Ep * inn)
+
+    def exchange(self, slot: int = 0):
+        """One round in one launch per GPU.  Raises ExchangeFailed if this rank's
+        context failed."""
+        self._round(lambda: self._exchange(slot))
+
+    def _exchange(self, slot):
+        Ep = self.hub.E_padded
+        self.barrier()                       # every replica and inbox free (previous round read)
+        for k in range(self.W):
+            self.hub.push(k, self._own[(slot, k)], mode="borrow", n=Ep)
+        self.epoch += 1
+        capi.phub_sched_exchange(self.hub.ctx, self.inbox, self.raw_inbox, self.flags, self.epoch,
+                                 self.hub._stream(None))
+        self.barrier()                       # every rank's w' stores into this replica are done
+
+    def exchange_host(self, host_grads: dict, host_out: dict, slot: int = 0):
+        g = self.gradients(slot)
+        for w in self.hosted:
+            g[w].copy_(host_grads[w], non_blocking=True)
+        self.exchange(slot)
+        for w in self.hosted:
+            host_out[w].copy_(self.replica, non_blocking=True)
+
+    def weights(self):
+        return self.replica
+
+    def close(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        capi.phub_set_replicas(self.hub.ctx, [])
+        for p in self._opened:
+            capi.phub_ipc_close(self.device, p)
+        dist.barrier(group=self.group)
+        self._grads = {}
+        for p in list(self._own.values()) + [self._inbox, self._raw, self._flags]:
+            capi.phub_free_shared(self.device, p)
+        self._own = {}
+        self.hub.close()

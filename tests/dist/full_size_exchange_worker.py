@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
 from paper_1805_07891_b200.sharded import (  # noqa: E402
-    ChainShardedPHub, P2PShardedPHub, PushShardedPHub)
+    ChainShardedPHub, P2PShardedPHub, PushShardedPHub, SchedShardedPHub)
 from workloads import grad_stream, manifest  # noqa: E402
 from workloads.generate import fullmant_at_np, fullmant_np, fullmant_torch  # noqa: E402
 
@@ -52,7 +52,8 @@ def main():
         mode = "chain" if G == 2 else "push"
     sizes = manifest(name)
     E = sum(sizes)
-    cls = {"chain": ChainShardedPHub, "p2p": P2PShardedPHub, "push": PushShardedPHub}[mode]
+    cls = {"chain": ChainShardedPHub, "p2p": P2PShardedPHub, "push": PushShardedPHub,
+           "sched": SchedShardedPHub}[mode]
     sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
     hub = sh.hub
     idx = torch.as_tensor(hub.padded_index(), device=dev)
@@ -72,7 +73,7 @@ def main():
     for r in range(rounds):
         gs = np.stack([fullmant_at_np(grad_stream(w) + 37 * r, samp) for w in range(N)])
         w_ref, v_ref, _ = oracle.elems(gs, w_ref, v_ref, 0.1, 0.9)
-    if mode in ("chain", "push"):
+    if mode in ("chain", "push", "sched"):
         sh.check()                   # collective: raises on every rank if a device wait expired
     ok = np.array_equal(got.view(np.uint32), w_ref.view(np.uint32))
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))

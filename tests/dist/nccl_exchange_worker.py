@@ -20,7 +20,8 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
 from paper_1805_07891_b200.sharded import (  # noqa: E402
-    AllReduceBaseline, ChainShardedPHub, P2PShardedPHub, PushShardedPHub, ShardedPHub)
+    AllReduceBaseline, ChainShardedPHub, P2PShardedPHub, PushShardedPHub, SchedShardedPHub,
+    ShardedPHub)
 from workloads import grad_stream, manifest  # noqa: E402
 from workloads.generate import fullmant_np, fullmant_torch  # noqa: E402
 
@@ -43,12 +44,14 @@ def main():
                               block=2048)
     elif mode == "push":
         sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048)
+    elif mode == "sched":
+        sh = SchedShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048, lag=1)
     elif mode == "allreduce":
         sh = AllReduceBaseline(sizes, N, chunk_size_bytes=cb, device=local)
     else:
         cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
         sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
-    fused = mode in ("p2p", "push") or mode.startswith("chain")
+    fused = mode in ("p2p", "push", "sched") or mode.startswith("chain")
     w_ref, v_ref = fullmant_np(1, 0, E), fullmant_np(2, 0, E)
     sh.hub.load_state(w_ref, v_ref)
     idx = torch.as_tensor(sh.hub.padded_index(), device=dev)
@@ -66,7 +69,7 @@ def main():
         hg = [fullmant_np(grad_stream(w) + 37 * r, 0, E) for w in range(N)]
         w_ref, v_ref, _ = oracle.round_(sizes, hg, w_ref, v_ref, 0.1, 0.9, chunk_bytes=cb)
     torch.cuda.synchronize()
-    if mode.startswith("chain") or mode == "push":
+    if mode.startswith("chain") or mode in ("push", "sched"):
         sh.check()                   # collective: raises on every rank if a device wait expired
     got = sh.weights()[idx].cpu().numpy()
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))

@@ -307,3 +307,125 @@ def test_piece_flags_chain_concurrent_streams():
     assert_bits_equal(gv, v, "piece-chain v'")
     prod.close()
     cons.close()
+
+
+# ---------------------------------------------- scheduled exchange (8.6)
+class EmulatedSched:
+    """R rank contexts of SchedShardedPHub on one GPU: each rank's item program
+    (phub_sched_plan) loaded into its own context, launched on its own stream;
+    local buffers stand in for the peer-mapped inboxes, raw inboxes, flags and
+    replicas."""
+
+    def __init__(self, sizes, R, W, weights, raw_frac, block, lag, grid, seed, cb=32768):
+        from paper_1805_07891_b200 import PHub, capi
+        from paper_1805_07891_b200.sharded import sched_geometry
+        self.capi, self.R, self.W, self.seed = capi, R, W, seed
+        self.Ep, self.bounds, self.split = sched_geometry(sizes, cb, R, weights, raw_frac)
+        self.hubs = [PHub(sizes, W, chunk_size_bytes=cb, device=0, rescale=1.0 / (R * W),
+                          keep_aggregate=True) for _ in range(R)]
+        h0 = self.hubs[0]
+        self.E = h0.E
+        self.nflags = None
+        for r, h in enumerate(self.hubs):
+            items, nf = capi.phub_sched_plan(R, r, W, self.bounds, self.split, block, lag)
+            capi.phub_sched_load(h.ctx, R, r, items, nf)
+            self.nflags = nf
+            h.set_option(capi.PHUB_OPT_GRID, grid)
+            capi.phub_set_replicas(h.ctx, [self.hubs[q].weights_ptr() for q in range(R) if q != r])
+        self.inbox = [torch.zeros(self.Ep, device=DEV) for _ in range(R)]
+        self.raw = [torch.zeros(R * W * max(self.split[r] - self.bounds[r], 8), device=DEV)
+                    for r in range(R)]
+        self.flags = [torch.zeros(max(self.nflags, 1), dtype=torch.int32, device=DEV)
+                      for _ in range(R)]
+        self.streams = [torch.cuda.Stream() for _ in range(R)]
+        self.epoch = 0
+        idx = torch.as_tensor(h0.padded_index(), device=DEV)
+        self.pidx = h0.padded_index()
+        from workloads.generate import fullmant_torch
+        self.grads = []
+        for q in range(R):
+            rank = []
+            for k in range(W):
+                b = torch.full((self.Ep,), float("nan"), device=DEV)
+                b[idx] = fullmant_torch(grad_stream(q * W + k) + 37 * seed, 0, self.E, DEV)
+                rank.append(b)
+            self.grads.append(rank)
+
+    def host_grads(self):
+        return [fullmant_np(grad_stream(w) + 37 * self.seed, 0, self.E)
+                for w in range(self.R * self.W)]
+
+    def owned_mask(self, r):
+        return (self.pidx >= self.bounds[r]) & (self.pidx < self.bounds[r + 1])
+
+    def round(self, order=None):
+        self.epoch += 1
+        torch.cuda.synchronize()                     # start barrier
+        ptr = lambda ts: [t.data_ptr() for t in ts]  # noqa: E731
+        for r in (order or range(self.R)):
+            h = self.hubs[r]
+            for k in range(self.W):
+                h.push(k, self.grads[r][k])
+            self.capi.phub_sched_exchange(h.ctx, ptr(self.inbox), ptr(self.raw), ptr(self.flags),
+                                          self.epoch, self.streams[r].cuda_stream)
+        torch.cuda.synchronize()                     # end barrier
+
+    def close(self):
+        for h in self.hubs:
+            h.close()
+
+
+SCHED_CASES = [
+    # R, W, weights, raw fractions, manifest, block, lag, rounds
+    (2, 4, [0.0, 1.0], [0.0, 0.0], "resnet50", 16384, 0, 2),                  # = the chain
+    (2, 4, [0.45, 0.55], [0.5, 0.3], "small", 2048, 1, 2),
+    (4, 2, [0.2982, 0.193, 0.193, 0.3158], [0.5294, 0.0, 0.0, 0.1667], "resnet50", 16384, 0, 2),
+    (4, 2, [0.2982, 0.193, 0.193, 0.3158], [0.5294, 0.0, 0.0, 0.1667], "small", 2048, 4, 3),
+    (4, 2, [0.125, 0.25, 0.25, 0.375], [1.0, 0.0, 0.0, 0.0], "tiny", 2048, 2, 2),
+    (8, 1, [0.125] * 8, [1.0] * 8, "resnet50", 16384, 0, 2),                  # = push exchange
+    (3, 3, [0.3846, 0.1538, 0.4616], [0.4, 0.0, 0.1667], "small", 2048, 0, 2),  # N = 9
+]
+
+
+@pytest.mark.parametrize("R,W,wts,rf,name,block,lag,rounds", SCHED_CASES)
+def test_sched_exchange_emulated(R, W, wts, rf, name, block, lag, rounds):
+    """k_sched == SchedShardedPHub's round: bit-exact vs the worker-order oracle
+    over all R*W workers on every replica; v' and s bit-exact on each rank's
+    Nesterov range."""
+    sizes = SMALL if name == "small" else manifest(name)
+    em = EmulatedSched(sizes, R, W, wts, rf, block, lag, grid=max(1, 360 // R), seed=100 + R)
+    w, v = fullmant_np(1 + 37 * 100, 0, em.E), fullmant_np(2 + 37 * 100, 0, em.E)
+    for h in em.hubs:
+        h.load_state(w, v)
+    flat = em.host_grads()
+    for _ in range(rounds):
+        em.round(order=list(reversed(range(R))))
+        w, v, s = oracle.round_(sizes, flat, w, v, 0.1, 0.9)
+    for r, h in enumerate(em.hubs):
+        assert em.capi.phub_sync_timeouts(h.ctx) == 0
+        gw, gv, gs = h.read_state()
+        assert_bits_equal(gw, w, f"rank {r} replica w'")
+        own = em.owned_mask(r)
+        assert_bits_equal(gv[own], v[own], f"rank {r} owned v'")
+        assert_bits_equal(gs[own], s[own], f"rank {r} owned s")
+    em.close()
+
+
+def test_sched_exchange_missing_rank_times_out_loudly():
+    """Rank 1 never launches: rank 0's chain/consume waits expire, the context
+    is sticky-failed and the next call reports PHUB_ERR_SYNC_TIMEOUT."""
+    from paper_1805_07891_b200 import PhubError
+    em = EmulatedSched(manifest("tiny"), 2, 2, [0.5, 0.5], [0.5, 0.5], 2048, 0, grid=64, seed=81)
+    em.epoch += 1
+    h = em.hubs[0]
+    for k in range(2):
+        h.push(k, em.grads[0][k])
+    ptr = lambda ts: [t.data_ptr() for t in ts]  # noqa: E731
+    em.capi.phub_sched_exchange(h.ctx, ptr(em.inbox), ptr(em.raw), ptr(em.flags), em.epoch,
+                                em.streams[0].cuda_stream)
+    torch.cuda.synchronize()
+    assert em.capi.phub_sync_timeouts(h.ctx) >= 1
+    with pytest.raises(PhubError) as e:
+        h.read_state()
+    assert em.capi.STATUS_NAMES[e.value.status] == "PHUB_ERR_SYNC_TIMEOUT"
+    em.close()

@@ -27,7 +27,7 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("mode", ["nccl", "p2p", "push", "chain", "chain_flags",
+@pytest.mark.parametrize("mode", ["nccl", "p2p", "push", "sched", "chain", "chain_flags",
                                   "chain_barrier", "allreduce"])
 @pytest.mark.parametrize("G,name,N,cb,rounds", [
     (2, "small", 8, 32768, 2), (2, "tiny", 4, 4096, 1), (4, "resnet50", 8, 32768, 2),
@@ -54,7 +54,8 @@ FULL = os.path.join(ROOT, "tests", "dist", "full_size_exchange_worker.py")
 
 
 @pytest.mark.parametrize("G,mode", [(2, "auto"), (2, "p2p"), (4, "auto"), (4, "chain"),
-                                    (4, "push"), (4, "p2p"), (8, "auto")])
+                                    (4, "push"), (4, "p2p"), (8, "auto"), (2, "sched"),
+                                    (4, "sched"), (8, "sched")])
 def test_full_size_vgg19_exchange_sampled(G, mode):
     """bench.py's N > 1 launch configuration at BASELINE.json's full VGG-19
     size (2 rounds), every rank's replica checked against the oracle on

@@ -1,0 +1,196 @@
+"""Host logic of the scheduled exchange (phub_sched_plan), on
+CPU: the item programs every rank gets for a geometry are checked by
+simulation, without any arithmetic of the method:
+
+  * ownership: the Nesterov items of rank o cover exactly [bounds[o],
+    bounds[o+1]) and the ranks together cover the padded model once;
+  * order: every Nesterov input is the sum of all N workers in worker-id order
+    from +0 -- the programs are executed symbolically (each buffer block holds
+    the tuple of worker ids summed into it, in order), so a wrong stage, a
+    skipped rank, a raw slot read from the wrong source or a final sum sent to
+    the wrong owner changes the tuple (reading R3);
+  * flags: every waited flag is raised by exactly one item of one rank, and no
+    flag index is raised twice;
+  * deadlock freedom: executing each rank's program strictly in ticket order
+    with ONE worker per rank (the tightest case of the k_sched argument) never
+    stalls;
+  * raw inbox slots written by different (source rank, worker) never overlap.
+"""
+import pytest
+
+from paper_1805_07891_b200 import capi
+
+T_RAW, T_CHAIN, T_CRAW, T_CFIN = (capi.PHUB_ITEM_RAW_PUSH, capi.PHUB_ITEM_CHAIN,
+                                  capi.PHUB_ITEM_CONSUME_RAW, capi.PHUB_ITEM_CONSUME_FINAL)
+NOF = capi.PHUB_NO_FLAG
+
+
+def geometry(Ep, G, raw_frac, weights=None):
+    """Owner bounds (multiples of 8) and raw/chain splits."""
+    weights = weights or [1.0] * G
+    tot = sum(weights)
+    b, acc = [0], 0.0
+    for o in range(G - 1):
+        acc += weights[o]
+        b.append(int(Ep * acc / tot) // 8 * 8)
+    b.append(Ep)
+    split = [b[o] + int((b[o + 1] - b[o]) * raw_frac[o]) // 8 * 8 for o in range(G)]
+    return b, split
+
+
+def simulate(G, W, bounds, split, block, lag):
+    progs, nflags = [], None
+    for r in range(G):
+        items, nf = capi.phub_sched_plan(G, r, W, bounds, split, block, lag)
+        assert nflags in (None, nf)
+        nflags = nf
+        progs.append(list(items))
+    flags = [[0] * nflags for _ in range(G)]
+    raised = [[0] * nflags for _ in range(G)]
+    inbox = [dict() for _ in range(G)]          # (lo, hi) -> tuple of worker ids
+    raw = [dict() for _ in range(G)]            # (slot q*W+k, lo, hi) -> worker id
+    nag = [[] for _ in range(G)]                # (lo, hi, tuple)
+    pc = [0] * G
+    local = lambda r: tuple(range(r * W, (r + 1) * W))  # noqa: E731
+
+    def ready(r, it):
+        if it.type == T_CRAW:
+            return all(flags[r][it.wait_flag + q] for q in range(G) if q != r)
+        return it.wait_flag == NOF or flags[r][it.wait_flag] == 1
+
+    def raise_(dst, f):
+        assert raised[dst][f] == 0, f"flag {f} of rank {dst} raised twice"
+        raised[dst][f] = 1
+        flags[dst][f] = 1
+
+    while any(pc[r] < len(progs[r]) for r in range(G)):
+        moved = False
+        for r in range(G):
+            if pc[r] >= len(progs[r]):
+                continue
+            it = progs[r][pc[r]]
+            if not ready(r, it):
+                continue
+            key = (it.lo, it.hi)
+            if it.type == T_RAW:
+                for k in range(W):
+                    slot = (r * W + k, it.lo, it.hi)
+                    assert slot not in raw[it.dst], "raw slot written twice"
+                    raw[it.dst][slot] = r * W + k
+                raise_(it.dst, it.signal_flag)
+            elif it.type == T_CHAIN:
+                acc = (() if it.wait_flag == NOF else inbox[r].pop(key)) + local(r)
+                if it.dst >= 0:
+                    inbox[it.dst][key] = acc
+                    raise_(it.dst, it.signal_flag)
+                else:
+                    nag[r].append((it.lo, it.hi, acc))
+            elif it.type == T_CRAW:
+                acc = ()
+                for q in range(G):
+                    acc += local(r) if q == r else tuple(raw[r][(q * W + k, it.lo, it.hi)]
+                                                         for k in range(W))
+                nag[r].append((it.lo, it.hi, acc))
+            else:
+                nag[r].append((it.lo, it.hi, inbox[r].pop(key)))
+            pc[r] += 1
+            moved = True
+        assert moved, f"deadlock: ranks stuck at {pc} of {[len(p) for p in progs]}"
+    return nag, raised
+
+
+GEOMS = [
+    # (Ep, G, W, raw fractions per owner, owner weights, block, lag)
+    (65536, 1, 8, [0.5], None, 2048, 0),
+    (65536, 2, 4, [0.0, 0.0], [0.0, 1.0], 4096, 0),          # the chain (single owner)
+    (65536, 2, 4, [0.3, 0.6], None, 2048, 3),
+    (98304, 4, 2, [0.53, 0.0, 0.0, 0.17], [0.298, 0.193, 0.193, 0.316], 2048, 0),  # LP mix
+    (98304, 4, 2, [1.0, 0.0, 0.0, 0.0], [1, 2, 2, 3], 4096, 5),                   # simple hybrid
+    (131072, 8, 1, [1.0] * 8, None, 2048, 2),                                   # push exchange
+    (131072, 8, 1, [0.5] * 8, None, 2048, 0),
+    (40000, 3, 3, [0.4, 0.0, 0.2], [0.38, 0.15, 0.47], 2048, 1),               # ragged tail
+]
+
+
+@pytest.mark.parametrize("Ep,G,W,rf,wts,block,lag", GEOMS)
+def test_sched_program_semantics(Ep, G, W, rf, wts, block, lag):
+    bounds, split = geometry(Ep, G, rf, wts)
+    nag, raised = simulate(G, W, bounds, split, block, lag)
+    N = G * W
+    order = tuple(range(N))
+    covered = []
+    for r in range(G):
+        for lo, hi, acc in nag[r]:
+            assert acc == order, f"rank {r} [{lo},{hi}): sum order {acc}"
+            assert bounds[r] <= lo < hi <= bounds[r + 1], f"rank {r} optimizes [{lo},{hi})"
+            covered.append((lo, hi))
+    covered.sort()
+    pos = 0
+    for lo, hi in covered:
+        assert lo == pos, f"gap or overlap at {pos}"
+        pos = hi
+    assert pos == Ep
+
+
+def test_every_waited_flag_is_raised_once():
+    Ep, G, W = 98304, 4, 2
+    bounds, split = geometry(Ep, G, [0.5, 0.0, 0.25, 0.1])
+    progs = [capi.phub_sched_plan(G, r, W, bounds, split, 2048, 1)[0] for r in range(G)]
+    signals = {}
+    for r, prog in enumerate(progs):
+        for it in prog:
+            if it.dst >= 0:
+                k = (it.dst, it.signal_flag)
+                assert k not in signals
+                signals[k] = r
+    for r, prog in enumerate(progs):
+        for it in prog:
+            if it.type == T_CRAW:
+                for q in range(G):
+                    if q != r:
+                        assert signals[(r, it.wait_flag + q)] == q
+            elif it.wait_flag != NOF:
+                assert (r, it.wait_flag) in signals
+
+
+def test_endpoints_match_push_exchange_and_chain():
+    """All-RAW parts give the push exchange's items (no chain items); all-CHAIN
+    on the last owner gives the chained exchange (no raw items)."""
+    Ep = 65536
+    b, sp = geometry(Ep, 4, [1.0] * 4)
+    for r in range(4):
+        items, _ = capi.phub_sched_plan(4, r, 2, b, sp, 2048, 0)
+        assert {it.type for it in items} == {T_RAW, T_CRAW}
+    b = [0, 0, Ep]
+    for r in range(2):
+        items, _ = capi.phub_sched_plan(2, r, 4, b, [0, 0], 4096, 0)
+        assert {it.type for it in items} == {T_CHAIN}
+        assert all((it.dst == -1) == (r == 1) for it in items)
+
+
+@pytest.mark.parametrize("bad", [
+    dict(block=1000), dict(bounds=[8, 100, 200]), dict(split=[0, 300]), dict(bounds=[0, 101, 200]),
+    dict(rank=2), dict(W=0),
+])
+def test_plan_rejects_bad_geometry(bad):
+    kw = dict(G=2, rank=0, W=4, bounds=[0, 104, 200], split=[0, 104], block=2048)
+    kw.update(bad)
+    with pytest.raises(capi.PhubError) as e:
+        capi.phub_sched_plan(kw["G"], kw["rank"], kw["W"], kw["bounds"], kw["split"], kw["block"])
+    assert capi.STATUS_NAMES[e.value.status] == "PHUB_ERR_INVALID_ARGUMENT"
+
+
+def test_lp_table_is_balanced():
+    """The owner weights / raw fractions sharded.py uses come from the byte
+    model of scripts/sched_lp.py: the busiest NVLink port moves at most the
+    model's optimum (and never more than the push exchange)."""
+    from paper_1805_07891_b200.sharded import SCHED_TABLE, sched_port_bytes
+    best = {2: 1.0, 3: 1.7692, 4: 1.7895, 8: 1.75}       # scripts/sched_lp.py optimum
+    for G, (wts, rf) in SCHED_TABLE.items():
+        W = 8 // G if 8 % G == 0 else 3
+        loads = sched_port_bytes(G, W, wts, rf)
+        push = sched_port_bytes(G, W, [1.0 / G] * G, [1.0] * G)
+        assert max(push) == pytest.approx(1 + (G * W - W - 1) / G)   # closed form, push exchange
+        assert max(loads) <= max(push) + 1e-9
+        assert max(loads) == pytest.approx(best[G], abs=2e-4)
+        assert abs(sum(wts) - 1) < 1e-3 and all(0 <= r <= 1 for r in rf)
