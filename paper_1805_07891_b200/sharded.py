@@ -899,6 +899,33 @@ def sched_port_bytes(G: int, W: int, weights, raw_frac):
     return [max(i, x) for i, x in zip(inn, out)]
 
 
+def sched_nvlink_bytes(bounds, split, W: int, rank: int):
+    """(out, in) NVLink bytes of `rank` per round of the scheduled exchange with
+    owner bounds / RAW-CHAIN splits (padded elements), counted item by item:
+    RAW -- W raw slices of the owner's RAW part from every other rank; CHAIN --
+    one partial per hop 0 -> ... -> G-1 and the finished sum into the owner
+    unless it is the last rank; w' of every owner range into every other
+    replica."""
+    G = len(bounds) - 1
+    out = inn = 0
+    for o in range(G):
+        raw, ch, own = split[o] - bounds[o], bounds[o + 1] - split[o], bounds[o + 1] - bounds[o]
+        if o == rank:
+            inn += W * raw * (G - 1)
+            out += own * (G - 1)
+        else:
+            out += W * raw
+            inn += own
+        if rank < G - 1:
+            out += ch
+        if rank > 0:
+            inn += ch
+        if o != G - 1:
+            out += ch if rank == G - 1 else 0
+            inn += ch if rank == o else 0
+    return 4 * out, 4 * inn
+
+
 def sched_geometry(key_sizes, chunk_size_bytes: int, G: int, weights, raw_frac):
     """Owner bounds and RAW/CHAIN splits in the padded layout, snapped to chunk
     starts so every chunk has exactly one owner."""
@@ -1028,30 +1055,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
 
     def nvlink_bytes(self):
         """(out, in) bytes of this rank per round under the byte model."""
-        G, W, Ep = self.world, self.W, self.hub.E_padded
-        sh = [(self.bounds[o + 1] - self.bounds[o]) / Ep for o in range(G)]
-        rf = [(self.split[o] - self.bounds[o]) / max(self.bounds[o + 1] - self.bounds[o], 1)
-              for o in range(G)]
-        inn = out = 0.0
-        me = self.rank
-        for o in range(G):
-            raw, ch = sh[o] * rf[o], sh[o] * (1 - rf[o])
-            if o == me:
-                inn += W * raw * (G - 1)
-                out += sh[o] * (G - 1)
-            else:
-                out += W * raw
-                inn += sh[o]
-            if me < G - 1:
-                out += ch
-            if me > 0:
-                inn += ch
-            if o != G - 1:
-                if me == G - 1:
-                    out += ch
-                if me == o:
-                    inn += ch
-        return int(4 * Ep * out), int(4 * Ep * inn)
+        return sched_nvlink_bytes(self.bounds, self.split, self.W, self.rank)
 
     def exchange(self, slot: int = 0):
         """One round in one launch per GPU.  Raises ExchangeFailed if this rank's

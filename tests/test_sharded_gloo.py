@@ -97,3 +97,23 @@ def test_chain_block_choice():
                        ("vgg19", 12288)):
         b = chain_block_for(sum(manifest(name)))
         assert b == want and b % 2048 == 0
+
+
+SCHED_WORKER = os.path.join(ROOT, "tests", "dist", "gloo_sched_worker.py")
+
+
+@pytest.mark.parametrize("world,name,N", [(2, "resnet50", 8), (4, "vgg19", 8), (4, "tiny", 8),
+                                          (8, "resnet50", 8)])
+def test_gloo_sched_programs(world, name, N):
+    """Scheduled exchange host logic across processes: each rank plans only its
+    own item program; signals and waits match rank by rank (gloo, CPU)."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    for _attempt in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", SCHED_WORKER, name, str(N)]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count(" ok: ") == world
