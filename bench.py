@@ -737,7 +737,7 @@ def bench_multi(args, mname, N, cb):
                                 f"(raw worker slices stored into the owner) and a CHAIN part "
                                 f"(rank-by-rank worker-order partials, finished sum stored into "
                                 f"the owner), mixed per owner so the busiest NVLink port moves "
-                                f"the fewest bytes; owner shares {[round(x, 4) for x in sh.weights]}"
+                                f"the fewest bytes; owner shares {[round(x, 4) for x in sh.shares]}"
                                 f", RAW fractions {[round(x, 4) for x in sh.raw_frac]}, "
                                 f"{args.sched_block}-element blocks, lag {args.sched_lag}")
                                if sched else

@@ -977,11 +977,11 @@ class SchedShardedPHub(_DeviceWaitExchange):
                 weights, raw_frac = SCHED_TABLE[world]
             else:                                      # no table entry: the push exchange
                 weights, raw_frac = [1.0 / world] * world, [1.0] * world
-        self.weights, self.raw_frac = list(weights), list(raw_frac)
+        self.shares, self.raw_frac = list(weights), list(raw_frac)     # (weights() is the pull)
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
         Ep, self.bounds, self.split = sched_geometry(key_sizes, chunk_size_bytes, world,
-                                                     self.weights, self.raw_frac)
+                                                     self.shares, self.raw_frac)
         self.hub = PHub(key_sizes, self.W, chunk_size_bytes=chunk_size_bytes, lr=lr,
                         momentum=momentum, rescale=1.0 / num_workers, device=dev,
                         keep_aggregate=keep_aggregate)

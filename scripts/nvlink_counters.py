@@ -157,6 +157,41 @@ def run_p2p(sizes, G, N):
         h.close()
 
 
+def run_sched(sizes, G, N, block=16384, epoch=1):
+    """Scheduled exchange (SchedShardedPHub): one k_sched launch
+    per rank with its item program; every flag pre-raised (launches serialise
+    under ncu)."""
+    from paper_1805_07891_b200.sharded import SCHED_TABLE, sched_geometry, sched_nvlink_bytes
+    W = N // G
+    wts, rf = SCHED_TABLE.get(G, ([1.0 / G] * G, [1.0] * G))
+    Ep, bounds, split = sched_geometry(sizes, 32768, G, wts, rf)
+    hubs = [PHub(sizes, W, device=r, rescale=1.0 / N) for r in range(G)]
+    grads = [[torch.zeros(Ep, device=f"cuda:{r}") for _ in range(W)] for r in range(G)]
+    inbox = [torch.zeros(Ep, device=f"cuda:{r}") for r in range(G)]
+    raw = [torch.zeros(G * W * max(split[r] - bounds[r], 8), device=f"cuda:{r}") for r in range(G)]
+    flags = []
+    for r, h in enumerate(hubs):
+        items, nf = capi.phub_sched_plan(G, r, W, bounds, split, block, 0)
+        capi.phub_sched_load(h.ctx, G, r, items, nf)
+        flags.append(torch.full((max(nf, 1),), epoch, dtype=torch.int32, device=f"cuda:{r}"))
+        capi.phub_set_replicas(h.ctx, [hubs[q].weights_ptr() for q in range(G) if q != r])
+    torch.cuda.synchronize()
+    ptr = lambda ts: [t.data_ptr() for t in ts]  # noqa: E731
+    for r, h in enumerate(hubs):
+        for k in range(W):
+            h.push(k, grads[r][k])
+        capi.phub_sched_exchange(h.ctx, ptr(inbox), ptr(raw), ptr(flags), epoch,
+                                 torch.cuda.current_stream(r).cuda_stream)
+        torch.cuda.synchronize(r)
+        out, inn = sched_nvlink_bytes(bounds, split, W, r)
+        print(json.dumps({"kernel": "k_sched", "G": G, "rank": r, "W": W, "block": block,
+                          "analytic_out_bytes": out, "analytic_in_bytes": inn,
+                          "timeouts": capi.phub_sync_timeouts(h.ctx)}))
+    for h in hubs:
+        capi.phub_set_replicas(h.ctx, [])
+        h.close()
+
+
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "vgg19"
     sizes = manifest(name)
@@ -167,7 +202,12 @@ def main():
     run_racks(sizes, G, 8 // G, True, 12288)              # push exchange (bench default G >= 3)
     run_racks(sizes, G, 8, False, 32768)                  # hierarchical reduction (8 per rack)
     run_p2p(sizes, G, 8)
+    run_sched(sizes, G, 8)                                # scheduled exchange (8.6)
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 2 and sys.argv[2] == "sched":      # the scheduled exchange only
+        enable_peer_access(torch.cuda.device_count())
+        run_sched(manifest(sys.argv[1]), torch.cuda.device_count(), 8)
+    else:
+        main()
