@@ -82,6 +82,8 @@ def parse():
                     help="sched mode: elements per item block")
     ap.add_argument("--sched-lag", type=int, default=0,
                     help="sched mode: blocks of progress each chain stage / consumer lags")
+    ap.add_argument("--sched-consumers", type=int, default=0,
+                    help="sched mode: CTAs serving the consumer lane (0 = auto)")
     ap.add_argument("--sched-weights", default="",
                     help="sched mode: comma-separated owner shares (default: sharded.SCHED_TABLE)")
     ap.add_argument("--sched-raw", default="",
@@ -505,6 +507,7 @@ def bench_multi(args, mname, N, cb):
             fl = lambda x: [float(v) for v in x.split(",")] if x else None  # noqa: E731
             sh = SchedShardedPHub(sizes, N, chunk_size_bytes=cb, device=local,
                                   block=args.sched_block, lag=args.sched_lag,
+                                  consumer_ctas=args.sched_consumers,
                                   weights=fl(args.sched_weights), raw_frac=fl(args.sched_raw))
         elif chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
@@ -739,7 +742,8 @@ def bench_multi(args, mname, N, cb):
                                 f"the owner), mixed per owner so the busiest NVLink port moves "
                                 f"the fewest bytes; owner shares {[round(x, 4) for x in sh.shares]}"
                                 f", RAW fractions {[round(x, 4) for x in sh.raw_frac]}, "
-                                f"{args.sched_block}-element blocks, lag {args.sched_lag}")
+                                f"{args.sched_block}-element blocks, lag {args.sched_lag}, "
+                                f"consumer-lane CTAs {args.sched_consumers or 'auto'}")
                                if sched else
                                (f"M3 (full exchange) chain: rank-ordered partial sums over "
                                 f"NVLink, last rank fused Nesterov + replica stores, " +

@@ -487,6 +487,11 @@ typedef struct {
     float* const* raw_inbox;
     uint32_t* const* flags;
     uint32_t epoch;
+    int32_t consumer_ctas;       /* CTAs serving the consumer lane (CONSUME_* items); the
+                                    rest serve the producers (RAW_PUSH, CHAIN), each lane in
+                                    ticket order, so a consumer waiting for late data never
+                                    holds a CTA the chain needs.  0 = auto (the consumers'
+                                    share of the items' elements, clamped to [1/8, 1/2]) */
 } phub_sched;
 phub_status phub_sched_exchange(phub_ctx ctx, const phub_sched* s, void* stream);
 

@@ -82,6 +82,7 @@ struct phub_ctx_s {
     std::vector<float*> replicas;     // peer weight replicas written by the kernel
     uint64_t range_cursor = UINT64_MAX;   // phub_aggregate_range progress (UINT64_MAX: none)
     uint32_t* d_sync = nullptr;           // [0] CTA counter, [1] timeouts, [2] abandoned wait value,
+                                          // [5] consumer-lane ticket (k_sched), [6] spare,
                                           // [3] block ticket, [4] CTAs done (block streaming)
     uint32_t* h_err = nullptr;            // host-mapped word a kernel sets on an expired wait
     uint32_t* d_err = nullptr;            // its device address (kernel argument)
@@ -100,7 +101,8 @@ struct phub_ctx_s {
     int hier_occ[2] = {0, 0};                          // resident CTAs/SM of k_hier [worker_order]
     // scheduled exchange (phub_sched_load / phub_sched_exchange)
     phub::SchedItem* d_items = nullptr;
-    uint64_t n_items = 0;
+    uint64_t n_items = 0, n_prod = 0;    // items [0, n_prod) producer lane, the rest consumers
+    double cons_frac = 0.0;               // consumer share of the items' elements
     int sched_ranks = 0, sched_rank = -1;
     uint32_t sched_flags = 0;
     int sched_occ = 0;
@@ -407,7 +409,7 @@ phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
         (e = cudaMalloc(&c->d_v, bytes)) != cudaSuccess ||
         (c->keep_agg && (e = cudaMalloc(&c->d_agg, bytes)) != cudaSuccess) ||
         (e = cudaMalloc(&c->d_base, sizeof(uintptr_t) * c->base.size())) != cudaSuccess ||
-        (e = cudaMalloc(&c->d_sync, 5 * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&c->d_sync, 7 * sizeof(uint32_t))) != cudaSuccess ||
         (e = cudaHostAlloc(&c->h_err, sizeof(uint32_t), cudaHostAllocMapped)) != cudaSuccess ||
         (e = cudaHostGetDevicePointer(&c->d_err, c->h_err, 0)) != cudaSuccess ||
         (c->n_tiles && (e = cudaMalloc(&c->d_tiles, sizeof(Tile) * c->n_tiles)) != cudaSuccess)) {
@@ -417,7 +419,7 @@ phub_status phub_init(const phub_config* cfg, phub_ctx* out) {
         return PHUB_ERR_OUT_OF_MEMORY;
     }
     *c->h_err = 0;
-    bool ok = cudaMemset(c->d_sync, 0, 5 * sizeof(uint32_t)) == cudaSuccess &&
+    bool ok = cudaMemset(c->d_sync, 0, 7 * sizeof(uint32_t)) == cudaSuccess &&
               cudaMemset(c->d_w, 0, bytes) == cudaSuccess &&
               cudaMemset(c->d_v, 0, bytes) == cudaSuccess &&
               (!c->d_agg || cudaMemset(c->d_agg, 0, bytes) == cudaSuccess) &&
@@ -1387,11 +1389,28 @@ phub_status phub_sched_load(phub_ctx c, int32_t ranks, int32_t rank, const phub_
                            "dst %d)", (unsigned long long)t, it.type, (unsigned long long)it.lo,
                            (unsigned long long)it.hi, it.dst);
     }
+    // two lanes, each in ticket (key) order: producers (RAW_PUSH, CHAIN) first,
+    // then consumers (CONSUME_RAW, CONSUME_FINAL) -- see k_sched
+    std::vector<phub_sched_item> lanes;
+    lanes.reserve(count);
+    uint64_t prod_elems = 0, cons_elems = 0;
+    for (int pass = 0; pass < 2; ++pass)
+        for (uint64_t t = 0; t < count; ++t) {
+            const bool cons = items[t].type == PHUB_ITEM_CONSUME_RAW ||
+                              items[t].type == PHUB_ITEM_CONSUME_FINAL;
+            if (cons != (pass == 1)) continue;
+            lanes.push_back(items[t]);
+            (cons ? cons_elems : prod_elems) += items[t].hi - items[t].lo;
+        }
+    uint64_t n_prod = 0;
+    while (n_prod < count && lanes[n_prod].type != PHUB_ITEM_CONSUME_RAW &&
+           lanes[n_prod].type != PHUB_ITEM_CONSUME_FINAL)
+        ++n_prod;
     DeviceGuard g(c->device);
     phub::SchedItem* d = nullptr;
     if (count) {
         cudaError_t e = cudaMalloc(&d, count * sizeof(phub::SchedItem));
-        if (e == cudaSuccess) e = cudaMemcpy(d, items, count * sizeof(phub::SchedItem),
+        if (e == cudaSuccess) e = cudaMemcpy(d, lanes.data(), count * sizeof(phub::SchedItem),
                                              cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
             cudaFree(d);
@@ -1401,6 +1420,9 @@ phub_status phub_sched_load(phub_ctx c, int32_t ranks, int32_t rank, const phub_
     cudaFree(c->d_items);
     c->d_items = d;
     c->n_items = count;
+    c->n_prod = n_prod;
+    c->cons_frac = (prod_elems + cons_elems) ? (double)cons_elems / (double)(prod_elems + cons_elems)
+                                             : 0.0;
     c->sched_ranks = ranks;
     c->sched_rank = rank;
     c->sched_flags = num_flags;
@@ -1452,6 +1474,7 @@ phub_status phub_sched_exchange(phub_ctx c, const phub_sched* s, void* stream) {
     for (int r = 0; r < a.nrep; ++r) a.rep[r] = c->replicas[r];
     a.items = c->d_items;
     a.nitems = c->n_items;
+    a.nprod = c->n_prod;
     for (int q = 0; q < R; ++q) {
         a.inbox[q] = s->inbox[q];
         a.raw_inbox[q] = s->raw_inbox[q];
@@ -1465,6 +1488,18 @@ phub_status phub_sched_exchange(phub_ctx c, const phub_sched* s, void* stream) {
     c->launches = 0;
     if (!c->sched_occ) c->sched_occ = phub::sched_blocks_per_sm(c->N);
     const int grid = c->grid_override ? c->grid_override : c->num_sms * c->sched_occ;
+    // CTAs [0, grid_prod) take producer items, the rest consumer items: a CTA
+    // blocked on a consumer's wait never holds up the chain it waits for
+    const bool has_p = c->n_prod > 0, has_c = c->n_items > c->n_prod;
+    int cons_ctas = s->consumer_ctas > 0 ? s->consumer_ctas
+                                         : (int)std::lround(grid * std::min(0.5, std::max(0.125,
+                                                                              c->cons_frac)));
+    if (!has_c) cons_ctas = 0;
+    else if (!has_p) cons_ctas = grid;
+    cons_ctas = std::min(std::max(cons_ctas, has_c ? 1 : 0), grid - (has_p ? 1 : 0));
+    if (has_p && has_c && grid < 2)
+        return c->fail(PHUB_ERR_INVALID_ARGUMENT, "two item lanes need a grid of >= 2 CTAs");
+    a.grid_prod = grid - cons_ctas;
     cudaError_t e = phub::launch_sched(a, grid, static_cast<cudaStream_t>(stream), &c->launches);
     c->launches_total += (uint64_t)c->launches;
     if (e != cudaSuccess) return c->cuda_fail(e, "scheduled exchange launch");

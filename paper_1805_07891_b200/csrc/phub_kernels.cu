@@ -865,11 +865,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ S
     __shared__ uint64_t s_t;
     __shared__ int s_ok;
     const uint32_t* my_flags = a.flags[a.rank];
+    // two lanes with their own tickets: producers (RAW_PUSH, CHAIN) never wait on
+    // a consumer, so consumers blocked on late data cannot stall the chain
+    const bool cons_lane = (int)blockIdx.x >= a.grid_prod;
+    uint32_t* const tk = cons_lane ? a.ticket + 2 : a.ticket;
+    const uint64_t first = cons_lane ? a.nprod : 0, last = cons_lane ? a.nitems : a.nprod;
     for (;;) {
-        if (threadIdx.x == 0) s_t = atomicAdd(a.ticket, 1u);
+        if (threadIdx.x == 0) s_t = first + atomicAdd(tk, 1u);
         __syncthreads();
         const uint64_t t = s_t;
-        if (t >= a.nitems) break;
+        if (t >= last) break;
         const SchedItem it = a.items[t];
         if (threadIdx.x == 0) {
             int good = 1;
@@ -970,6 +975,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ S
     if (threadIdx.x == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x - 1) {
         a.ticket[0] = 0;
         a.ticket[1] = 0;
+        a.ticket[2] = 0;
     }
 }
 

@@ -91,13 +91,14 @@ struct SchedArgs {
     float lr, mu, rescale;
     int nrep;
     float* rep[kMaxReplicas];         // peer replicas receiving w' of every NAG item
-    const SchedItem* items;
-    uint64_t nitems;
+    const SchedItem* items;           // [0, nprod) producer lane, [nprod, nitems) consumer lane
+    uint64_t nitems, nprod;
+    int grid_prod;                    // CTAs [0, grid_prod) serve the producer lane
     float* inbox[kMaxRacks];          // rank q's partial/sum inbox (padded-based)
     float* raw_inbox[kMaxRacks];      // rank q's raw inbox
     uint32_t* flags[kMaxRacks];       // rank q's flags
     uint32_t epoch;
-    uint32_t* ticket;                 // [0] next item, [1] CTAs done
+    uint32_t* ticket;                 // [0] next producer item, [1] CTAs done, [2] next consumer
     uint32_t* timeouts;               // [0] expired waits, [1] abandoned epoch
     volatile uint32_t* err_host;
 };

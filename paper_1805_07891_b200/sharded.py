@@ -962,7 +962,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
                  device=None, group=None, block=16384, lag=0, weights=None, raw_frac=None,
-                 nslots=2, keep_aggregate=False):
+                 nslots=2, keep_aggregate=False, consumer_ctas=0):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -972,6 +972,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
             raise ValueError(f"{num_workers} workers cannot be hosted evenly on {world} ranks")
         self.rank, self.world, self.W = rank, world, num_workers // world
         self.block, self.lag = int(block), int(lag)
+        self.consumer_ctas = int(consumer_ctas)        # 0: auto (phub_sched.consumer_ctas)
         if weights is None or raw_frac is None:
             if world in SCHED_TABLE:
                 weights, raw_frac = SCHED_TABLE[world]
@@ -1069,7 +1070,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
             self.hub.push(k, self._own[(slot, k)], mode="borrow", n=Ep)
         self.epoch += 1
         capi.phub_sched_exchange(self.hub.ctx, self.inbox, self.raw_inbox, self.flags, self.epoch,
-                                 self.hub._stream(None))
+                                 self.hub._stream(None), consumer_ctas=self.consumer_ctas)
         self.barrier()                       # every rank's w' stores into this replica are done
 
     def exchange_host(self, host_grads: dict, host_out: dict, slot: int = 0):

@@ -38,19 +38,30 @@ def geometry(Ep, G, raw_frac, weights=None):
     return b, split
 
 
-def simulate(G, W, bounds, split, block, lag):
+def simulate(G, W, bounds, split, block, lag, lanes=False):
+    """lanes=False: each rank runs its whole program in ticket order on ONE
+    worker; lanes=True: as k_sched does, producers (RAW_PUSH, CHAIN) and
+    consumers (CONSUME_*) in two independent ticket-ordered lanes, one worker
+    each (phub_sched_load's stable partition)."""
     progs, nflags = [], None
     for r in range(G):
         items, nf = capi.phub_sched_plan(G, r, W, bounds, split, block, lag)
         assert nflags in (None, nf)
         nflags = nf
-        progs.append(list(items))
+        items = list(items)
+        if lanes:
+            cons = [it for it in items if it.type in (T_CRAW, T_CFIN)]
+            progs.append([it for it in items if it.type not in (T_CRAW, T_CFIN)])
+            progs.append(cons)
+        else:
+            progs.append(items)
+    owner = (lambda i: i // 2) if lanes else (lambda i: i)  # noqa: E731
     flags = [[0] * nflags for _ in range(G)]
     raised = [[0] * nflags for _ in range(G)]
     inbox = [dict() for _ in range(G)]          # (lo, hi) -> tuple of worker ids
     raw = [dict() for _ in range(G)]            # (slot q*W+k, lo, hi) -> worker id
     nag = [[] for _ in range(G)]                # (lo, hi, tuple)
-    pc = [0] * G
+    pc = [0] * len(progs)
     local = lambda r: tuple(range(r * W, (r + 1) * W))  # noqa: E731
 
     def ready(r, it):
@@ -63,12 +74,13 @@ def simulate(G, W, bounds, split, block, lag):
         raised[dst][f] = 1
         flags[dst][f] = 1
 
-    while any(pc[r] < len(progs[r]) for r in range(G)):
+    while any(pc[i] < len(progs[i]) for i in range(len(progs))):
         moved = False
-        for r in range(G):
-            if pc[r] >= len(progs[r]):
+        for i in range(len(progs)):
+            if pc[i] >= len(progs[i]):
                 continue
-            it = progs[r][pc[r]]
+            r = owner(i)
+            it = progs[i][pc[i]]
             if not ready(r, it):
                 continue
             key = (it.lo, it.hi)
@@ -93,7 +105,7 @@ def simulate(G, W, bounds, split, block, lag):
                 nag[r].append((it.lo, it.hi, acc))
             else:
                 nag[r].append((it.lo, it.hi, inbox[r].pop(key)))
-            pc[r] += 1
+            pc[i] += 1
             moved = True
         assert moved, f"deadlock: ranks stuck at {pc} of {[len(p) for p in progs]}"
     return nag, raised
@@ -112,10 +124,11 @@ GEOMS = [
 ]
 
 
+@pytest.mark.parametrize("lanes", [False, True])
 @pytest.mark.parametrize("Ep,G,W,rf,wts,block,lag", GEOMS)
-def test_sched_program_semantics(Ep, G, W, rf, wts, block, lag):
+def test_sched_program_semantics(Ep, G, W, rf, wts, block, lag, lanes):
     bounds, split = geometry(Ep, G, rf, wts)
-    nag, raised = simulate(G, W, bounds, split, block, lag)
+    nag, raised = simulate(G, W, bounds, split, block, lag, lanes)
     N = G * W
     order = tuple(range(N))
     covered = []
