@@ -516,6 +516,10 @@ enum {
     PHUB_OPT_TILE_ELEMS = 3,  /* max elements per CTA tile in the chunk-tile kernel (1024) */
     PHUB_OPT_CACHE = 4,       /* PHUB_CACHE_*: L2 policy of the pulled weights   */
                               /* (5, 6: removed in round 2 -- measured without gain)     */
+    PHUB_OPT_SCHED_TRACE = 9, /* diagnostic: device pointer to 4 x n_items uint64 that    */
+                              /* phub_sched_exchange fills per item (lane order: producers */
+                              /* then consumers): ticket taken, wait done, item done       */
+                              /* (%globaltimer ns), CTA << 32 | SM id; 0 = off             */
     PHUB_OPT_L2_RESIDENT = 8, /* PHUB_CACHE_RESIDENT: bytes of w kept L2-resident across  */
                               /* rounds (the tail of the owned range; default 32 MiB)    */
     PHUB_OPT_FLAT_ONESHOT = 7 /* flat kernels: 1 = one vector per thread, grid covering */

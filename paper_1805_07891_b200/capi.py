@@ -29,7 +29,7 @@ PHUB_OWNED_RANGE = -2
 PHUB_COPY, PHUB_BORROW = 0, 1
 PHUB_OWNER_LPT, PHUB_OWNER_CONTIG = 0, 1
 PHUB_OPT_KERNEL, PHUB_OPT_GRID, PHUB_OPT_TILE_ELEMS, PHUB_OPT_CACHE = 1, 2, 3, 4
-PHUB_OPT_FLAT_ONESHOT, PHUB_OPT_L2_RESIDENT = 7, 8
+PHUB_OPT_FLAT_ONESHOT, PHUB_OPT_L2_RESIDENT, PHUB_OPT_SCHED_TRACE = 7, 8, 9
 PHUB_CROSS_RACK_SHARDED, PHUB_CROSS_RACK_RING = 0, 1
 (PHUB_KERNEL_AUTO, PHUB_KERNEL_FLAT, PHUB_KERNEL_TILES, PHUB_KERNEL_FLAT128,
  PHUB_KERNEL_WIDE, PHUB_KERNEL_BULK) = range(6)

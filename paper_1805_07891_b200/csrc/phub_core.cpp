@@ -103,6 +103,7 @@ struct phub_ctx_s {
     phub::SchedItem* d_items = nullptr;
     uint64_t n_items = 0, n_prod = 0;    // items [0, n_prod) producer lane, the rest consumers
     double cons_frac = 0.0;               // consumer share of the items' elements
+    uint64_t* sched_trace = nullptr;      // PHUB_OPT_SCHED_TRACE (diagnostic)
     int sched_ranks = 0, sched_rank = -1;
     uint32_t sched_flags = 0;
     int sched_occ = 0;
@@ -1475,6 +1476,7 @@ phub_status phub_sched_exchange(phub_ctx c, const phub_sched* s, void* stream) {
     a.items = c->d_items;
     a.nitems = c->n_items;
     a.nprod = c->n_prod;
+    a.trace = c->sched_trace;
     for (int q = 0; q < R; ++q) {
         a.inbox[q] = s->inbox[q];
         a.raw_inbox[q] = s->raw_inbox[q];
@@ -1584,6 +1586,10 @@ phub_status phub_set_option(phub_ctx c, int32_t option, int64_t value) {
         case PHUB_OPT_GRID:
             if (value < 0 || value > (1 << 30)) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "bad grid");
             c->grid_override = (int)value;
+            return PHUB_OK;
+        case PHUB_OPT_SCHED_TRACE:
+            if (value % 8) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "trace buffer must be 8-B aligned");
+            c->sched_trace = reinterpret_cast<uint64_t*>(value);
             return PHUB_OK;
         case PHUB_OPT_L2_RESIDENT:
             if (value < 0) return c->fail(PHUB_ERR_INVALID_ARGUMENT, "resident bytes must be >= 0");

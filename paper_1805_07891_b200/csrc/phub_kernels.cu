@@ -879,6 +879,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ S
         if (threadIdx.x == 0) {
             int good = 1;
             const uint64_t t0 = globaltimer_ns();
+            if (a.trace) {
+                uint32_t smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                a.trace[4 * t] = t0;
+                a.trace[4 * t + 3] = ((uint64_t)blockIdx.x << 32) | smid;
+            }
             if (it.type == PHUB_ITEM_CONSUME_RAW) {
                 for (int q = 0; q < a.R && good; ++q)
                     if (q != a.rank) good = sched_wait(a, my_flags + it.wait_flag + q, t0);
@@ -886,6 +892,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ S
                 good = sched_wait(a, my_flags + it.wait_flag, t0);
             }
             s_ok = good;
+            if (a.trace) a.trace[4 * t + 1] = globaltimer_ns();
         }
         __syncthreads();
         const bool ok = s_ok != 0;
@@ -970,6 +977,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ S
             __threadfence_system();
             st_release_sys(a.flags[it.dst] + it.signal_flag, a.epoch);
         }
+        if (threadIdx.x == 0 && a.trace) a.trace[4 * t + 2] = globaltimer_ns();
     }
     if (a.nrep) __threadfence_system();
     if (threadIdx.x == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x - 1) {

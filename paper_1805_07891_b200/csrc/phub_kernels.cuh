@@ -94,6 +94,8 @@ struct SchedArgs {
     const SchedItem* items;           // [0, nprod) producer lane, [nprod, nitems) consumer lane
     uint64_t nitems, nprod;
     int grid_prod;                    // CTAs [0, grid_prod) serve the producer lane
+    uint64_t* trace;                  // diagnostic: per item (in lane order) 4 x u64 -- ticket,
+                                      // wait done, item done (%globaltimer ns), CTA << 32 | SM
     float* inbox[kMaxRacks];          // rank q's partial/sum inbox (padded-based)
     float* raw_inbox[kMaxRacks];      // rank q's raw inbox
     uint32_t* flags[kMaxRacks];       // rank q's flags
