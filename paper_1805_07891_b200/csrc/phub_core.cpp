@@ -1282,10 +1282,11 @@ phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_ran
             return PHUB_ERR_INVALID_ARGUMENT;
     struct Blk { int o; uint64_t lo, hi; uint64_t j, J; };
     std::vector<Blk> chain, raw;
-    for (int o = 0; o < G; ++o) {                     // chain parts, address order
+    for (int o = 0; o < G; ++o) {                     // chain parts, owner-major
         const uint64_t b = split[o], e = bounds[o + 1];
-        for (uint64_t lo = b; lo < e; lo += block_elems)
-            chain.push_back({o, lo, std::min(lo + block_elems, e), 0, 0});
+        const uint64_t J = (e - b + block_elems - 1) / block_elems;
+        for (uint64_t j = 0; j < J; ++j)
+            chain.push_back({o, b + j * block_elems, std::min(b + (j + 1) * block_elems, e), j, J});
     }
     for (int o = 0; o < G; ++o) {                     // raw parts, owner-major
         const uint64_t b = bounds[o], e = split[o];
@@ -1296,14 +1297,18 @@ phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_ran
     const uint64_t C = chain.size(), R = raw.size();
     const uint64_t nflags = 2 * C + R * (uint64_t)G;
     if (nflags >= 0xffffffffull) return PHUB_ERR_INVALID_ARGUMENT;
-    // (progress key, stage, item): progress = fraction of the block's part done
-    // before it, plus stage * lag; the same doubles on every rank
+    // (progress key, stage, item): progress = fraction of the block's own part
+    // done before it, plus stage * lag; the same doubles on every rank.  Every
+    // part -- each owner's RAW part and each owner's CHAIN part -- advances at
+    // the same relative pace, so at any moment each rank mixes all its kinds of
+    // work (e.g. the last rank's Nesterov + replica stores for its own chain
+    // part are spread over the round instead of trailing the other owners').
     struct Keyed { double t; int stage; phub_sched_item it; };
     std::vector<Keyed> v;
     const double lag_c = C ? (double)lag_blocks / (double)C : 0.0;
     for (uint64_t c = 0; c < C; ++c) {
         const Blk& b = chain[c];
-        const double t = (double)c / (double)C;
+        const double t = (double)b.j / (double)b.J;
         phub_sched_item it{};
         it.lo = b.lo;
         it.hi = b.hi;

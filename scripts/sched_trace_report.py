@@ -1,8 +1,7 @@
 """Summarise scripts/sched_trace.py output: per rank and item type, the time
 items spent waiting vs working, the busy CTAs over time, and when each rank's
-lanes finished (relative to the earliest ticket of the round on any rank --
-%globaltimer is one clock across the GPUs of a box only approximately, so
-cross-rank offsets are indicative).
+lanes finished (relative to the rank's first ticket of the round: the GPUs' %globaltimer
+clocks are not aligned, so ranks are not compared in absolute time).
 
     python scripts/sched_trace_report.py DIR
 """
@@ -17,10 +16,10 @@ NAMES = {1: "RAW_PUSH", 2: "CHAIN", 3: "CONSUME_RAW", 4: "CONSUME_FINAL"}
 def main():
     files = sorted(glob.glob(f"{sys.argv[1]}/trace_rank*.npz"))
     data = [np.load(f) for f in files]
-    t0 = min(int(d["t"][:, 0][d["t"][:, 0] > 0].min()) for d in data)
     for r, d in enumerate(data):
         t = d["t"].astype(np.int64)
         ok = t[:, 0] > 0
+        t0 = int(t[ok, 0].min())       # per rank: the GPUs' %globaltimer clocks are not aligned
         print(f"rank {r}: round {float(d['ms']):.3f} ms, {ok.sum()} items")
         for ty in (1, 2, 3, 4):
             m = ok & (d["type"] == ty)
