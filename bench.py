@@ -9,10 +9,13 @@ One step = one full parameter-exchange round of the 8-worker job: every
 worker's push, the fused tall aggregation + Nesterov update of every chunk,
 and the pull.  N = 1: all 8 workers' gradients are resident in HBM and pushed
 zero-copy (mode M1).  N > 1: one process per GPU, 8/N workers per
-GPU, chunks sharded by owner (mode M3); `--mode auto` runs the block-streamed
-chained exchange at N = 2 and the owner-sharded push exchange (every NVLink
-transfer a store) above; the owner-sharded peer-load kernel
-(p2p), NCCL send/recv and an NCCL all-reduce baseline are options.
+GPU, chunks sharded by owner (mode M3); `--mode auto` runs the scheduled
+exchange (one launch per GPU, each owner range moved partly as
+raw worker slices and partly as a rank-by-rank worker-order chain, mixed so
+the busiest NVLink port moves the fewest bytes -- the chain at N = 2, the push
+exchange at N = 8, a mix in between); the block-streamed chain (chain), the
+all-store push exchange (push), the owner-sharded peer-load kernel (p2p),
+NCCL send/recv and an NCCL all-reduce baseline are options.
 Total work is fixed as N grows ("scaling": "strong").  `--mode hier` is the
 hierarchical reduction (one 8-worker rack per GPU, weak scaling, NEXT-4).
 
@@ -78,10 +81,11 @@ def parse():
                     help="hier mode: elements per block flag")
     ap.add_argument("--push-block", type=int, default=12288,
                     help="push mode: elements per block flag")
-    ap.add_argument("--sched-block", type=int, default=16384,
-                    help="sched mode: elements per item block")
-    ap.add_argument("--sched-lag", type=int, default=0,
-                    help="sched mode: blocks of progress each chain stage / consumer lags")
+    ap.add_argument("--sched-block", type=int, default=0,
+                    help="sched mode: elements per item block (0: 16384 at G = 2, else 12288)")
+    ap.add_argument("--sched-lag", type=int, default=-1,
+                    help="sched mode: blocks of progress each chain stage / consumer lags "
+                         "(-1: 0 at G = 2, else 64)")
     ap.add_argument("--sched-consumers", type=int, default=0,
                     help="sched mode: CTAs serving the consumer lane (0 = auto)")
     ap.add_argument("--sched-weights", default="",
@@ -487,8 +491,8 @@ def bench_multi(args, mname, N, cb):
     dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
     rank, G = dist.get_rank(), dist.get_world_size()
     sizes = manifest(mname)
-    if args.mode == "auto":      # fewest NVLink bytes: chain at G = 2, owner-sharded (push) above
-        args.mode = "chain" if G == 2 else "push"
+    if args.mode == "auto":      # the scheduled exchange: byte-balanced ports at every G (8.6)
+        args.mode = "sched"
     hier = args.mode == "hier"
     push = args.mode == "push"
     sched = args.mode == "sched"
@@ -742,7 +746,7 @@ def bench_multi(args, mname, N, cb):
                                 f"the owner), mixed per owner so the busiest NVLink port moves "
                                 f"the fewest bytes; owner shares {[round(x, 4) for x in sh.shares]}"
                                 f", RAW fractions {[round(x, 4) for x in sh.raw_frac]}, "
-                                f"{args.sched_block}-element blocks, lag {args.sched_lag}, "
+                                f"{sh.block}-element blocks, lag {sh.lag}, "
                                 f"consumer-lane CTAs {args.sched_consumers or 'auto'}")
                                if sched else
                                (f"M3 (full exchange) chain: rank-ordered partial sums over "

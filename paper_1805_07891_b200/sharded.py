@@ -961,7 +961,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
     hosted in rank order (rank r: global workers [r*W, (r+1)*W))."""
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, block=16384, lag=0, weights=None, raw_frac=None,
+                 device=None, group=None, block=0, lag=-1, weights=None, raw_frac=None,
                  nslots=2, keep_aggregate=False, consumer_ctas=0):
         import torch
         import torch.distributed as dist
@@ -971,7 +971,10 @@ class SchedShardedPHub(_DeviceWaitExchange):
         if num_workers % world:
             raise ValueError(f"{num_workers} workers cannot be hosted evenly on {world} ranks")
         self.rank, self.world, self.W = rank, world, num_workers // world
-        self.block, self.lag = int(block), int(lag)
+        # measured defaults (profiles/r02_sched5/): G = 2 (the chain plan) 16K-element
+        # blocks, no lag; G >= 3 12K-element blocks, chain stages lagging 64 blocks
+        self.block = int(block) if block else (16384 if world == 2 else 12288)
+        self.lag = int(lag) if lag >= 0 else (0 if world == 2 else 64)
         self.consumer_ctas = int(consumer_ctas)        # 0: auto (phub_sched.consumer_ctas)
         if weights is None or raw_frac is None:
             if world in SCHED_TABLE:

@@ -1,6 +1,5 @@
 """Full-size multi-GPU parity worker (torchrun, NCCL): the exchange bench.py
-times at N > 1 (`--mode auto`: chained exchange with block-streaming flags at
-G = 2, owner-sharded push exchange above), at BASELINE.json's full model size,
+times at N > 1 (`--mode auto`: the scheduled exchange), at BASELINE.json's full model size,
 checked against the CPU oracle on sampled elements (the oracle computes them
 one by one from independently generated inputs).
 
@@ -49,7 +48,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=300))
     rank, G = dist.get_rank(), dist.get_world_size()
     if mode == "auto":                       # bench.py --mode auto
-        mode = "chain" if G == 2 else "push"
+        mode = "sched"
     sizes = manifest(name)
     E = sum(sizes)
     cls = {"chain": ChainShardedPHub, "p2p": P2PShardedPHub, "push": PushShardedPHub,
