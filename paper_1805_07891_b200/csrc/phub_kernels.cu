@@ -902,6 +902,30 @@ __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ S
                 // worker k of this rank -> slot (rank, k) of owner dst's raw part
                 float* dst = a.raw_inbox[it.dst];
                 const int nw = NW > 0 ? NW : a.nw;
+                if constexpr (NW == 1 || NW == 2) {
+                    // few workers: U = 4 / NW vectors per thread and iteration, so four
+                    // NVLink stores are in flight per thread (G = 8: one worker per GPU)
+                    constexpr int U = 4 / NW;
+                    for (uint64_t i0 = lo + threadIdx.x; i0 < hi; i0 += U * kThreads) {
+                        V8 gv[U][NW];
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int k = 0; k < NW; ++k)
+                                if (i0 + u * kThreads < hi)
+                                    gv[u][k] = ld_grad(reinterpret_cast<const V8*>(a.g[k]) + i0 +
+                                                       u * kThreads);
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int k = 0; k < NW; ++k) {
+                                const uint64_t i = i0 + u * kThreads;
+                                if (i < hi)
+                                    *reinterpret_cast<V8*>(dst + ((uint64_t)(a.rank * NW + k) * it.len +
+                                                                  8 * i - it.base)) = gv[u][k];
+                            }
+                    }
+                } else
                 for (uint64_t i = lo + threadIdx.x; i < hi; i += kThreads) {
                     const uint64_t x = 8 * i - it.base;
                     for (int k0 = 0; k0 < nw; k0 += 4) {
