@@ -491,7 +491,9 @@ typedef struct {
                                     rest serve the producers (RAW_PUSH, CHAIN), each lane in
                                     ticket order, so a consumer waiting for late data never
                                     holds a CTA the chain needs.  0 = auto (the consumers'
-                                    share of the items' elements, clamped to [1/8, 1/2]) */
+                                    share of the items' elements, clamped to [1/8, 1/2]).
+                                    A program without CHAIN items runs as ONE lane in
+                                    ticket order (the field is ignored). */
 } phub_sched;
 phub_status phub_sched_exchange(phub_ctx ctx, const phub_sched* s, void* stream);
 

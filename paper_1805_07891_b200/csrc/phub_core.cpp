@@ -1396,22 +1396,31 @@ phub_status phub_sched_load(phub_ctx c, int32_t ranks, int32_t rank, const phub_
                            (unsigned long long)it.hi, it.dst);
     }
     // two lanes, each in ticket (key) order: producers (RAW_PUSH, CHAIN) first,
-    // then consumers (CONSUME_RAW, CONSUME_FINAL) -- see k_sched
+    // then consumers (CONSUME_RAW, CONSUME_FINAL) -- see k_sched.  A program
+    // without CHAIN items (the push plan) keeps ONE lane in key order: its
+    // producers never wait, so a waiting consumer cannot hold up anything a
+    // CTA taking the next ticket would not reach anyway (k_hier's scheme), and
+    // the CTAs balance between pushes and consumers dynamically.
+    bool chain = false;
+    for (uint64_t t = 0; t < count; ++t) chain |= items[t].type == PHUB_ITEM_CHAIN;
     std::vector<phub_sched_item> lanes;
     lanes.reserve(count);
     uint64_t prod_elems = 0, cons_elems = 0;
-    for (int pass = 0; pass < 2; ++pass)
+    for (int pass = 0; pass < (chain ? 2 : 1); ++pass)
         for (uint64_t t = 0; t < count; ++t) {
             const bool cons = items[t].type == PHUB_ITEM_CONSUME_RAW ||
                               items[t].type == PHUB_ITEM_CONSUME_FINAL;
-            if (cons != (pass == 1)) continue;
+            if (chain && cons != (pass == 1)) continue;
             lanes.push_back(items[t]);
             (cons ? cons_elems : prod_elems) += items[t].hi - items[t].lo;
         }
-    uint64_t n_prod = 0;
-    while (n_prod < count && lanes[n_prod].type != PHUB_ITEM_CONSUME_RAW &&
-           lanes[n_prod].type != PHUB_ITEM_CONSUME_FINAL)
-        ++n_prod;
+    uint64_t n_prod = count;
+    if (chain) {
+        n_prod = 0;
+        while (n_prod < count && lanes[n_prod].type != PHUB_ITEM_CONSUME_RAW &&
+               lanes[n_prod].type != PHUB_ITEM_CONSUME_FINAL)
+            ++n_prod;
+    }
     DeviceGuard g(c->device);
     phub::SchedItem* d = nullptr;
     if (count) {

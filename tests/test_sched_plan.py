@@ -49,12 +49,14 @@ def simulate(G, W, bounds, split, block, lag, lanes=False):
         assert nflags in (None, nf)
         nflags = nf
         items = list(items)
-        if lanes:
+        if lanes and any(it.type == T_CHAIN for it in items):   # phub_sched_load's rule
             cons = [it for it in items if it.type in (T_CRAW, T_CFIN)]
             progs.append([it for it in items if it.type not in (T_CRAW, T_CFIN)])
             progs.append(cons)
         else:
             progs.append(items)
+            if lanes:
+                progs.append([])                # the push plan: one lane in key order
     owner = (lambda i: i // 2) if lanes else (lambda i: i)  # noqa: E731
     flags = [[0] * nflags for _ in range(G)]
     raised = [[0] * nflags for _ in range(G)]
