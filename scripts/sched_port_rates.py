@@ -1,9 +1,11 @@
 """Per-rank NVLink port rates over the round from a scripts/sched_trace.py
-trace (bytes of each item spread over its work interval, 100-us bins; G = 4,
-W = 2).  usage: python scripts/sched_port_rates.py TRACE_DIR"""
+trace (bytes of each item spread over its work interval, 100-us bins; G from
+the trace files, W = 8 / G).  usage: python scripts/sched_port_rates.py TRACE_DIR"""
 import numpy as np, sys
+import glob
 d0 = sys.argv[1]
-G=4; W=2
+G = len(glob.glob(f'{d0}/trace_rank*.npz'))
+W = 8 // G
 data=[np.load(f'{d0}/trace_rank{r}.npz') for r in range(G)]
 BIN=100
 nb=22
