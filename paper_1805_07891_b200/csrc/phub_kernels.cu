@@ -69,17 +69,12 @@ __device__ __forceinline__ V4 ld_grad(const V4* p) {
 }
 
 // Model state (w, v): read then rewritten by the same thread.  ENABLED: no
-// L2 hint; BYPASS: evict-first; RESIDENT: evict-last (the kept slice of w,
-// re-read from L2 next round).
+// L2 hint; BYPASS: evict-first.  (RESIDENT accesses w through a run-time
+// policy operand, ld_state_pol below.)
 template <int CACHE>
 __device__ __forceinline__ V8 ld_state(const V8* p) {
     V8 r;
-    if (CACHE == PHUB_CACHE_RESIDENT)
-        asm volatile("ld.global.L1::no_allocate.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
-                       "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
-                     : "l"(p));
-    else if (CACHE == PHUB_CACHE_BYPASS)
+    if (CACHE == PHUB_CACHE_BYPASS)
         asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]),
                        "=f"(r.x[5]), "=f"(r.x[6]), "=f"(r.x[7])
