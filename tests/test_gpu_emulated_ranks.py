@@ -19,7 +19,11 @@ Covered (the defaults of sharded.py at G >= 2):
     really waits on the producer's per-block flags; and the per-piece "flags"
     chain (k_prefix -> k_flat with stage flags);
   * an expired wait: one rank of a push exchange never launched -> the other
-    rank's next call fails with PHUB_ERR_SYNC_TIMEOUT.
+    rank's next call fails with PHUB_ERR_SYNC_TIMEOUT;
+  * k_sched (SchedShardedPHub, the multi-GPU default since round 2): the item
+    programs of the chain plan (R = 2), the LP mixes (R = 3, 4), a hybrid and
+    the push plan (R = 8), bit-exact vs the worker-order oracle, and its
+    missing-rank timeout.
 Every case asserts phub_sync_timeouts == 0 (except the forced one).
 """
 import numpy as np
