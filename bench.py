@@ -86,6 +86,8 @@ def parse():
     ap.add_argument("--sched-lag", type=int, default=-1,
                     help="sched mode: blocks of progress each chain stage / consumer lags "
                          "(-1: 0 at G = 2, else 64)")
+    ap.add_argument("--sched-taper", type=int, default=0,
+                    help="sched mode: blocks at each part's ends cut 4x finer")
     ap.add_argument("--sched-consumers", type=int, default=0,
                     help="sched mode: CTAs serving the consumer lane (0 = auto)")
     ap.add_argument("--sched-weights", default="",
@@ -511,7 +513,7 @@ def bench_multi(args, mname, N, cb):
             fl = lambda x: [float(v) for v in x.split(",")] if x else None  # noqa: E731
             sh = SchedShardedPHub(sizes, N, chunk_size_bytes=cb, device=local,
                                   block=args.sched_block, lag=args.sched_lag,
-                                  consumer_ctas=args.sched_consumers,
+                                  consumer_ctas=args.sched_consumers, taper=args.sched_taper,
                                   weights=fl(args.sched_weights), raw_frac=fl(args.sched_raw))
         elif chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,

@@ -450,7 +450,10 @@ typedef struct {
  * key every rank shares -- (normalized progress of the block in its part +
  * stage * lag, stage) -- so each item waits only on items with strictly
  * smaller keys on other ranks: deadlock-free with any number of co-resident
- * CTAs taking tickets in order.  lag_blocks shifts the chain
+ * CTAs taking tickets in order.  The first and last
+ * taper_blocks * block_elems elements of every part are cut into blocks 4x
+ * smaller (multiples of 8) so the pipeline fills and drains in finer steps
+ * (0 = uniform blocks).  lag_blocks shifts the chain
  * stages and consumers by that many blocks of progress (pipeline fill).
  * Flag layout (identical on every rank, *num_flags entries, zero initially):
  * chain block c: [c] partial arrival, [C + c] final arrival; raw block j
@@ -459,8 +462,8 @@ typedef struct {
  * if cap < count).  INVALID_ARGUMENT on bad geometry. */
 phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_rank,
                             const uint64_t* bounds, const uint64_t* split, uint64_t block_elems,
-                            uint64_t lag_blocks, phub_sched_item* out, uint64_t cap,
-                            uint64_t* count, uint32_t* num_flags);
+                            uint64_t lag_blocks, uint64_t taper_blocks, phub_sched_item* out,
+                            uint64_t cap, uint64_t* count, uint32_t* num_flags);
 
 /* Upload an item program (host array) to the context's device; validated
  * (types, ranges within E_padded and multiples of 8, dst < ranks, flag

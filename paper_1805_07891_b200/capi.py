@@ -133,7 +133,7 @@ _SIGS = {
     "phub_set_replicas": (C.c_int, [phub_ctx, C.POINTER(C.c_void_p), C.c_int32]),
     "phub_hier_exchange": (C.c_int, [phub_ctx, C.c_void_p, C.c_void_p]),
     "phub_sched_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _u64p, _u64p, C.c_uint64,
-                                  C.c_uint64, C.c_void_p, C.c_uint64, _u64p,
+                                  C.c_uint64, C.c_uint64, C.c_void_p, C.c_uint64, _u64p,
                                   C.POINTER(C.c_uint32)]),
     "phub_sched_load": (C.c_int, [phub_ctx, C.c_int32, C.c_int32, C.c_void_p, C.c_uint64,
                                   C.c_uint32]),
@@ -388,12 +388,13 @@ def phub_hier_exchange(ctx, num_racks: int, block: int, inbox, peer_inbox, flags
 
 
 def phub_sched_plan(ranks: int, rank: int, workers_per_rank: int, bounds, split,
-                    block_elems: int, lag_blocks: int = 0):
+                    block_elems: int, lag_blocks: int = 0, taper_blocks: int = 0):
     """Item program of `rank` (phub.h phub_sched_plan): (items array, num_flags)."""
     b = (C.c_uint64 * len(bounds))(*[int(x) for x in bounds])
     sp = (C.c_uint64 * len(split))(*[int(x) for x in split])
     n, nf = C.c_uint64(), C.c_uint32()
-    args = (ranks, rank, workers_per_rank, b, sp, int(block_elems), int(lag_blocks))
+    args = (ranks, rank, workers_per_rank, b, sp, int(block_elems), int(lag_blocks),
+            int(taper_blocks))
     _check(_lib.phub_sched_plan(*args, None, 0, C.byref(n), C.byref(nf)), "phub_sched_plan", None)
     items = (phub_sched_item * n.value)()
     _check(_lib.phub_sched_plan(*args, items, n.value, C.byref(n), C.byref(nf)),

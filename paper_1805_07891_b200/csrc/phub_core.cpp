@@ -1269,8 +1269,8 @@ static_assert(offsetof(phub_sched_item, signal_flag) == offsetof(phub::SchedItem
 
 phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_rank,
                             const uint64_t* bounds, const uint64_t* split, uint64_t block_elems,
-                            uint64_t lag_blocks, phub_sched_item* out, uint64_t cap,
-                            uint64_t* count, uint32_t* num_flags) {
+                            uint64_t lag_blocks, uint64_t taper_blocks, phub_sched_item* out,
+                            uint64_t cap, uint64_t* count, uint32_t* num_flags) {
     const int G = ranks, p = rank, W = workers_per_rank;
     if (G < 1 || G > phub::kMaxRacks || p < 0 || p >= G || W < 1 || W > phub::kMaxWorkers ||
         !bounds || !split || !count || !block_elems || block_elems % 2048 || (cap && !out))
@@ -1281,19 +1281,24 @@ phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_ran
             split[o] < bounds[o] || split[o] > bounds[o + 1])
             return PHUB_ERR_INVALID_ARGUMENT;
     struct Blk { int o; uint64_t lo, hi; uint64_t j, J; };
+    // Cut a part [b, e) into blocks: block_elems each, except its first and last
+    // taper_blocks * block_elems elements, cut 4x finer (multiples of 8) so the
+    // pipeline fills and drains in smaller steps.
+    const uint64_t fine = std::max<uint64_t>(256, block_elems / 4 / 8 * 8);
+    auto cut = [&](int o, uint64_t b, uint64_t e, std::vector<Blk>& outv) {
+        const uint64_t L = e - b, span = taper_blocks * block_elems;
+        const uint64_t head = std::min(span, L / 2 / 8 * 8);
+        const uint64_t tail = std::min(span, (L - head) / 8 * 8);
+        std::vector<std::pair<uint64_t, uint64_t>> r;
+        for (uint64_t x = b; x < b + head; x += fine) r.push_back({x, std::min(x + fine, b + head)});
+        for (uint64_t x = b + head; x < e - tail; x += block_elems)
+            r.push_back({x, std::min(x + block_elems, e - tail)});
+        for (uint64_t x = e - tail; x < e; x += fine) r.push_back({x, std::min(x + fine, e)});
+        for (size_t j = 0; j < r.size(); ++j) outv.push_back({o, r[j].first, r[j].second, j, r.size()});
+    };
     std::vector<Blk> chain, raw;
-    for (int o = 0; o < G; ++o) {                     // chain parts, owner-major
-        const uint64_t b = split[o], e = bounds[o + 1];
-        const uint64_t J = (e - b + block_elems - 1) / block_elems;
-        for (uint64_t j = 0; j < J; ++j)
-            chain.push_back({o, b + j * block_elems, std::min(b + (j + 1) * block_elems, e), j, J});
-    }
-    for (int o = 0; o < G; ++o) {                     // raw parts, owner-major
-        const uint64_t b = bounds[o], e = split[o];
-        const uint64_t J = (e - b + block_elems - 1) / block_elems;
-        for (uint64_t j = 0; j < J; ++j)
-            raw.push_back({o, b + j * block_elems, std::min(b + (j + 1) * block_elems, e), j, J});
-    }
+    for (int o = 0; o < G; ++o) cut(o, split[o], bounds[o + 1], chain);   // chain parts, owner-major
+    for (int o = 0; o < G; ++o) cut(o, bounds[o], split[o], raw);         // raw parts, owner-major
     const uint64_t C = chain.size(), R = raw.size();
     const uint64_t nflags = 2 * C + R * (uint64_t)G;
     if (nflags >= 0xffffffffull) return PHUB_ERR_INVALID_ARGUMENT;

@@ -962,7 +962,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
                  device=None, group=None, block=0, lag=-1, weights=None, raw_frac=None,
-                 nslots=2, keep_aggregate=False, consumer_ctas=0):
+                 nslots=2, keep_aggregate=False, consumer_ctas=0, taper=0):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -976,6 +976,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
         self.block = int(block) if block else (16384 if world == 2 else 12288)
         self.lag = int(lag) if lag >= 0 else (0 if world == 2 else 64)
         self.consumer_ctas = int(consumer_ctas)        # 0: auto (phub_sched.consumer_ctas)
+        self.taper = int(taper)                        # blocks cut 4x finer at each part's ends
         if weights is None or raw_frac is None:
             if world in SCHED_TABLE:
                 weights, raw_frac = SCHED_TABLE[world]
@@ -991,7 +992,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
                         keep_aggregate=keep_aggregate)
         assert self.hub.E_padded == Ep
         items, self.num_flags = capi.phub_sched_plan(world, rank, self.W, self.bounds, self.split,
-                                                     self.block, self.lag)
+                                                     self.block, self.lag, self.taper)
         capi.phub_sched_load(self.hub.ctx, world, rank, items, self.num_flags)
         self.nslots = int(nslots)
         self._own = {(sl, k): capi.phub_alloc_shared(dev, 4 * Ep)

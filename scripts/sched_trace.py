@@ -37,7 +37,7 @@ def main():
     rank, G = dist.get_rank(), dist.get_world_size()
     sizes = manifest("vgg19")
     sh = SchedShardedPHub(sizes, 8, device=local, block=block, lag=lag, consumer_ctas=cons)
-    items, _nf = capi.phub_sched_plan(G, rank, sh.W, sh.bounds, sh.split, block, lag)
+    items, _nf = capi.phub_sched_plan(G, rank, sh.W, sh.bounds, sh.split, block, lag, sh.taper)
     items = list(items)
     cons_t = (capi.PHUB_ITEM_CONSUME_RAW, capi.PHUB_ITEM_CONSUME_FINAL)
     lanes = [it for it in items if it.type not in cons_t] + [it for it in items if it.type in cons_t]

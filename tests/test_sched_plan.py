@@ -38,14 +38,14 @@ def geometry(Ep, G, raw_frac, weights=None):
     return b, split
 
 
-def simulate(G, W, bounds, split, block, lag, lanes=False):
+def simulate(G, W, bounds, split, block, lag, lanes=False, taper=0):
     """lanes=False: each rank runs its whole program in ticket order on ONE
     worker; lanes=True: as k_sched does, producers (RAW_PUSH, CHAIN) and
     consumers (CONSUME_*) in two independent ticket-ordered lanes, one worker
     each (phub_sched_load's stable partition)."""
     progs, nflags = [], None
     for r in range(G):
-        items, nf = capi.phub_sched_plan(G, r, W, bounds, split, block, lag)
+        items, nf = capi.phub_sched_plan(G, r, W, bounds, split, block, lag, taper)
         assert nflags in (None, nf)
         nflags = nf
         items = list(items)
@@ -126,11 +126,12 @@ GEOMS = [
 ]
 
 
+@pytest.mark.parametrize("taper", [0, 3])
 @pytest.mark.parametrize("lanes", [False, True])
 @pytest.mark.parametrize("Ep,G,W,rf,wts,block,lag", GEOMS)
-def test_sched_program_semantics(Ep, G, W, rf, wts, block, lag, lanes):
+def test_sched_program_semantics(Ep, G, W, rf, wts, block, lag, lanes, taper):
     bounds, split = geometry(Ep, G, rf, wts)
-    nag, raised = simulate(G, W, bounds, split, block, lag, lanes)
+    nag, raised = simulate(G, W, bounds, split, block, lag, lanes, taper)
     N = G * W
     order = tuple(range(N))
     covered = []
@@ -209,3 +210,16 @@ def test_lp_table_is_balanced():
         assert max(loads) <= max(push) + 1e-9
         assert max(loads) == pytest.approx(best[G], abs=2e-4)
         assert abs(sum(wts) - 1) < 1e-3 and all(0 <= r <= 1 for r in rf)
+
+
+def test_taper_cuts_the_ends_finer():
+    """taper_blocks: the first and last taper * block elements of every part
+    come in blocks of block/4, the middle in whole blocks, covering the part."""
+    Ep, block = 196608, 8192                  # 2 x 16384 ends + 20 whole blocks
+    b, sp = [0, Ep], [0, 0]                   # one owner, all chain
+    items, _ = capi.phub_sched_plan(1, 0, 2, b, sp, block, 0, 2)
+    sizes = sorted((it.lo, it.hi - it.lo) for it in items)
+    assert sizes[0][0] == 0 and sum(n for _, n in sizes) == Ep
+    assert [n for _, n in sizes[:8]] == [2048] * 8              # 2 blocks' worth, 4x finer
+    assert [n for _, n in sizes[-8:]] == [2048] * 8
+    assert all(n == block for _, n in sizes[8:-8])
