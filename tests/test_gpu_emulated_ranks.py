@@ -320,7 +320,7 @@ class EmulatedSched:
     local buffers stand in for the peer-mapped inboxes, raw inboxes, flags and
     replicas."""
 
-    def __init__(self, sizes, R, W, weights, raw_frac, block, lag, grid, seed, cb=32768):
+    def __init__(self, sizes, R, W, weights, raw_frac, block, lag, grid, seed, cb=32768, taper=0):
         from paper_1805_07891_b200 import PHub, capi
         from paper_1805_07891_b200.sharded import sched_geometry
         self.capi, self.R, self.W, self.seed = capi, R, W, seed
@@ -331,7 +331,7 @@ class EmulatedSched:
         self.E = h0.E
         self.nflags = None
         for r, h in enumerate(self.hubs):
-            items, nf = capi.phub_sched_plan(R, r, W, self.bounds, self.split, block, lag)
+            items, nf = capi.phub_sched_plan(R, r, W, self.bounds, self.split, block, lag, taper)
             capi.phub_sched_load(h.ctx, R, r, items, nf)
             self.nflags = nf
             h.set_option(capi.PHUB_OPT_GRID, grid)
@@ -380,7 +380,7 @@ class EmulatedSched:
 
 
 SCHED_CASES = [
-    # R, W, weights, raw fractions, manifest, block, lag, rounds
+    # R, W, weights, raw fractions, manifest, block, lag, rounds[, taper]
     (2, 4, [0.0, 1.0], [0.0, 0.0], "resnet50", 16384, 0, 2),                  # = the chain
     (2, 4, [0.45, 0.55], [0.5, 0.3], "small", 2048, 1, 2),
     (4, 2, [0.2982, 0.193, 0.193, 0.3158], [0.5294, 0.0, 0.0, 0.1667], "resnet50", 16384, 0, 2),
@@ -388,16 +388,20 @@ SCHED_CASES = [
     (4, 2, [0.125, 0.25, 0.25, 0.375], [1.0, 0.0, 0.0, 0.0], "tiny", 2048, 2, 2),
     (8, 1, [0.125] * 8, [1.0] * 8, "resnet50", 16384, 0, 2),                  # = push exchange
     (3, 3, [0.3846, 0.1538, 0.4616], [0.4, 0.0, 0.1667], "small", 2048, 0, 2),  # N = 9
+    (4, 2, [0.2982, 0.193, 0.193, 0.3158], [0.5294, 0.0, 0.0, 0.1667], "resnet50", 12288, 64, 2, 4),
 ]
 
 
-@pytest.mark.parametrize("R,W,wts,rf,name,block,lag,rounds", SCHED_CASES)
-def test_sched_exchange_emulated(R, W, wts, rf, name, block, lag, rounds):
+@pytest.mark.parametrize("case", SCHED_CASES)
+def test_sched_exchange_emulated(case):
     """k_sched == SchedShardedPHub's round: bit-exact vs the worker-order oracle
     over all R*W workers on every replica; v' and s bit-exact on each rank's
     Nesterov range."""
+    R, W, wts, rf, name, block, lag, rounds = case[:8]
+    taper = case[8] if len(case) > 8 else 0
     sizes = SMALL if name == "small" else manifest(name)
-    em = EmulatedSched(sizes, R, W, wts, rf, block, lag, grid=max(1, 360 // R), seed=100 + R)
+    em = EmulatedSched(sizes, R, W, wts, rf, block, lag, grid=max(1, 360 // R), seed=100 + R,
+                       taper=taper)
     w, v = fullmant_np(1 + 37 * 100, 0, em.E), fullmant_np(2 + 37 * 100, 0, em.E)
     for h in em.hubs:
         h.load_state(w, v)
