@@ -86,8 +86,9 @@ def parse():
     ap.add_argument("--sched-lag", type=int, default=-1,
                     help="sched mode: blocks of progress each chain stage / consumer lags "
                          "(-1: 0 at G = 2, else 64)")
-    ap.add_argument("--sched-taper", type=int, default=0,
-                    help="sched mode: blocks at each part's ends cut 4x finer")
+    ap.add_argument("--sched-taper", type=int, default=-1,
+                    help="sched mode: blocks at each part's ends cut 4x finer (-1: 0 at G = 2, "
+                         "else 8)")
     ap.add_argument("--sched-consumers", type=int, default=0,
                     help="sched mode: CTAs serving the consumer lane (0 = auto)")
     ap.add_argument("--sched-weights", default="",
@@ -748,7 +749,7 @@ def bench_multi(args, mname, N, cb):
                                 f"the owner), mixed per owner so the busiest NVLink port moves "
                                 f"the fewest bytes; owner shares {[round(x, 4) for x in sh.shares]}"
                                 f", RAW fractions {[round(x, 4) for x in sh.raw_frac]}, "
-                                f"{sh.block}-element blocks, lag {sh.lag}, "
+                                f"{sh.block}-element blocks, lag {sh.lag}, taper {sh.taper}, "
                                 f"consumer-lane CTAs {args.sched_consumers or 'auto'}")
                                if sched else
                                (f"M3 (full exchange) chain: rank-ordered partial sums over "

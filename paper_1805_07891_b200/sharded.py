@@ -962,7 +962,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
                  device=None, group=None, block=0, lag=-1, weights=None, raw_frac=None,
-                 nslots=2, keep_aggregate=False, consumer_ctas=0, taper=0):
+                 nslots=2, keep_aggregate=False, consumer_ctas=0, taper=-1):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -976,7 +976,8 @@ class SchedShardedPHub(_DeviceWaitExchange):
         self.block = int(block) if block else (16384 if world == 2 else 12288)
         self.lag = int(lag) if lag >= 0 else (0 if world == 2 else 64)
         self.consumer_ctas = int(consumer_ctas)        # 0: auto (phub_sched.consumer_ctas)
-        self.taper = int(taper)                        # blocks cut 4x finer at each part's ends
+        # blocks cut 4x finer at each part's ends: 8 at G >= 3 (profiles/r02_sched9/)
+        self.taper = int(taper) if taper >= 0 else (0 if world == 2 else 8)
         if weights is None or raw_frac is None:
             if world in SCHED_TABLE:
                 weights, raw_frac = SCHED_TABLE[world]
