@@ -10,6 +10,8 @@
  * Build: gcc -std=c11 -I include examples/phub_c_example.c \
  *          -L paper_1805_07891_b200 -lphub -L/usr/local/cuda/lib64 -lcudart \
  *          -Wl,-rpath,$PWD/paper_1805_07891_b200 -o phub_c_example
+ * A second context then runs the same round through the scheduled exchange
+ * (phub_sched_plan / phub_sched_load / phub_sched_exchange) on one rank.
  * Exit code 0 = every check passed.
  */
 #include <cuda_runtime.h>
@@ -81,6 +83,49 @@ int main(void) {
     printf("phub C example: %llu elements, %d mismatches, iteration %llu\n",
            (unsigned long long)E, bad, (unsigned long long)it);
     CHECK(phub_destroy(ctx));
+
+    /* The scheduled exchange's ABI from C on one rank: the
+     * host planner cuts the model into a RAW half and a CHAIN half, the item
+     * program is uploaded once and one k_sched launch runs the round -- the
+     * same S:193 bits. */
+    ctx = NULL;
+    CHECK(phub_init(&cfg, &ctx));
+    const uint64_t bounds[2] = {0, Epad}, split[1] = {Epad / 2 / 8 * 8};
+    uint64_t n_items = 0;
+    uint32_t n_flags = 0;
+    CHECK(phub_sched_plan(1, 0, 2, bounds, split, 2048, 0, 0, NULL, 0, &n_items, &n_flags));
+    phub_sched_item* items = (phub_sched_item*)malloc(n_items * sizeof(phub_sched_item));
+    CHECK(phub_sched_plan(1, 0, 2, bounds, split, 2048, 0, 0, items, n_items, &n_items, &n_flags));
+    CHECK(phub_sched_load(ctx, 1, 0, items, n_items, n_flags));
+    float *inbox = NULL, *raw = NULL;
+    uint32_t* flags = NULL;
+    if (cudaMalloc((void**)&inbox, Epad * sizeof(float)) != cudaSuccess ||
+        cudaMalloc((void**)&raw, 2 * Epad * sizeof(float)) != cudaSuccess ||
+        cudaMalloc((void**)&flags, (n_flags + 1) * sizeof(uint32_t)) != cudaSuccess)
+        return 1;
+    cudaMemset(flags, 0, (n_flags + 1) * sizeof(uint32_t));
+    CHECK(phub_push(ctx, 0, PHUB_ALL_KEYS, g0, Epad, PHUB_BORROW, NULL));
+    CHECK(phub_push(ctx, 1, PHUB_ALL_KEYS, g0, Epad, PHUB_BORROW, NULL));
+    float* ib[1] = {inbox};
+    float* rb[1] = {raw};
+    uint32_t* fb[1] = {flags};
+    phub_sched sch = {ib, rb, fb, 1, 0};
+    CHECK(phub_sched_exchange(ctx, &sch, NULL));
+    CHECK(phub_read_state(ctx, wout, vout, NULL));
+    int bad2 = 0;
+    for (uint64_t i = 0; i < E; ++i) {
+        memcpy(&wbits, &wout[i], 4);
+        memcpy(&vbits, &vout[i], 4);
+        bad2 += (wbits != 0x3F4F5C29u) || (vbits != 0x3F800000u);
+    }
+    printf("phub C example, scheduled exchange: %llu items, %d mismatches\n",
+           (unsigned long long)n_items, bad2);
+    CHECK(phub_destroy(ctx));
+    cudaFree(inbox);
+    cudaFree(raw);
+    cudaFree(flags);
+    free(items);
+    bad += bad2;
     cudaFree(g0);
     free(h);
     free(w0);
