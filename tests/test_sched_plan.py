@@ -223,3 +223,29 @@ def test_taper_cuts_the_ends_finer():
     assert [n for _, n in sizes[:8]] == [2048] * 8              # 2 blocks' worth, 4x finer
     assert [n for _, n in sizes[-8:]] == [2048] * 8
     assert all(n == block for _, n in sizes[8:-8])
+
+
+@pytest.mark.parametrize("name", ["vgg19", "resnet50", "resnet269", "tiny"])
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_geometry_snaps_to_chunk_starts(name, G):
+    """sharded.sched_geometry: every owner bound and RAW/CHAIN split is a chunk
+    start of the padded layout (each chunk has exactly one owner),
+    bounds are monotone from 0 to E_padded, and each owner's share is within
+    one chunk of the table's target."""
+    from paper_1805_07891_b200.sharded import SCHED_TABLE, sched_geometry
+    from workloads import manifest
+    sizes = manifest(name)
+    wts, rf = SCHED_TABLE[G]
+    Ep, bounds, split = sched_geometry(sizes, 32768, G, wts, rf)
+    _, offs, _ = capi.phub_plan_ranges(sizes, 32768, 1)
+    chunks, n = capi.phub_plan_chunks(sizes, 32768, 1, capi.PHUB_OWNER_CONTIG)
+    starts = {int(offs[chunks[i].key_id]) + int(chunks[i].offset) for i in range(n)} | {Ep}
+    assert bounds[0] == 0 and bounds[-1] == Ep
+    assert all(a <= b for a, b in zip(bounds, bounds[1:]))
+    for o in range(G):
+        assert bounds[o] in starts and split[o] in starts
+        assert bounds[o] <= split[o] <= bounds[o + 1]
+    if name != "tiny":                        # 37 chunks: too coarse for the shares
+        for o in range(G):
+            target = Ep * sum(wts[:o + 1]) / sum(wts)
+            assert abs(bounds[o + 1] - target) <= 8192 + 32      # one 32 KB chunk + padding
