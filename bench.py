@@ -56,7 +56,7 @@ def parse():
                          "every stream evict-first; enabled = all of w' evict-last (P:911)")
     ap.add_argument("--resident-mb", type=int, default=-1,
                     help="resident policy: MiB of w kept in L2 across rounds (-1: library default)")
-    ap.add_argument("--e2e-steps", type=int, default=8,
+    ap.add_argument("--e2e-steps", type=int, default=16,
                     help="e2e rounds timed (the pipeline's fill + drain is amortised over them)")
     ap.add_argument("--e2e-streams", type=int, default=1,
                     help="copy streams per direction in the 1-GPU e2e measurement")
