@@ -320,14 +320,17 @@ def run_reference(args):
     }))
 
 
-def pcie_probe(dev, mib=1024, reps=5):
+def pcie_probe(dev, mib=1024, reps=5, h_in=None, h_out=None):
     """Same-run PCIe ceiling for the e2e numbers: pinned host <-> device copies
     of `mib` MiB (H2D alone, D2H alone, both at once on two streams), best of
-    `reps` (CUDA events)."""
+    `reps` (CUDA events).  h_in / h_out: the e2e run's own pinned buffers (the
+    same host pages, hence the same NUMA placement, as the measurement it is
+    held against -- fresh allocations can land elsewhere and measure lower)."""
     import torch
     n = mib * (1 << 20) // 4
-    h_in = torch.ones(n, pin_memory=True)
-    h_out = torch.empty(n, pin_memory=True)
+    h_in = h_in[:n] if h_in is not None else torch.ones(n, pin_memory=True)
+    h_out = h_out[:n] if h_out is not None else torch.empty(n, pin_memory=True)
+    n = min(h_in.numel(), h_out.numel())
     d_in = torch.empty(n, device=dev)
     d_out = torch.ones(n, device=dev)
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
@@ -693,8 +696,9 @@ def bench_multi(args, mname, N, cb):
         te = float(t.item()) / 1e3
         if chain:
             sh.check()
+        w0 = sh.hosted[0]
+        probe = pcie_probe(dev, h_in=host_g[w0], h_out=host_o[w0])
         del host_g, host_o
-        probe = pcie_probe(dev)
         pr = [None] * G
         dist.all_gather_object(pr, probe)
         slowest = min(pr, key=lambda x: x["bidir_gbs_per_direction"])
@@ -1109,8 +1113,9 @@ def bench_e2e(hub, grads, N, E, Ep, stream, steps, nstreams=1):
     t1.record(s_c)
     torch.cuda.synchronize()
     t = t0.elapsed_time(t1) / 1e3 / steps
+    probe = pcie_probe(grads[0].device, h_in=host_g[0], h_out=host_w[0])
+    probe["fresh_buffers"] = pcie_probe(grads[0].device)
     del host_g, host_w
-    probe = pcie_probe(grads[0].device)
     per_dir = N * 4 * Ep / t / 1e9
     return {"value": round(N * 4 * E / t / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": N * 4 * Ep, "d2h_bytes_per_step": N * 4 * Ep,
