@@ -364,7 +364,7 @@ def pcie_probe(dev, mib=1024, reps=5, h_in=None, h_out=None):
     nb = 4 * n
     out = {"h2d_gbs": round(nb / th / 1e9, 2), "d2h_gbs": round(nb / td / 1e9, 2),
            "bidir_gbs_per_direction": round(nb / tb / 1e9, 2), "bytes": nb,
-           "how": f"pinned {mib} MiB copies, best of {reps}, CUDA events"}
+           "how": f"pinned {nb / 2**20:.0f} MiB copies, best of {reps}, CUDA events"}
     del h_in, h_out, d_in, d_out
     torch.cuda.empty_cache()
     return out
