@@ -437,3 +437,28 @@ def test_sched_exchange_missing_rank_times_out_loudly():
         h.read_state()
     assert em.capi.STATUS_NAMES[e.value.status] == "PHUB_ERR_SYNC_TIMEOUT"
     em.close()
+
+
+def test_sched_g8_bench_plan_full_vgg19_emulated():
+    """The G = 8 launch configuration bench.py would time on an 8-GPU box --
+    SCHED_TABLE[8] (the push plan, one ticket lane), 12K-element blocks, lag
+    64, taper 8, one worker per rank -- at BASELINE.json's full VGG-19 size,
+    eight ranks emulated on one GPU: every replica bit-exact vs the oracle
+    round, every owner's v' and s too (no 8-GPU runner was available)."""
+    from paper_1805_07891_b200.sharded import SCHED_TABLE
+    wts, rf = SCHED_TABLE[8]
+    sizes = manifest("vgg19")
+    em = EmulatedSched(sizes, 8, 1, wts, rf, 12288, 64, grid=45, seed=120, taper=8)
+    w, v = fullmant_np(1 + 37 * 120, 0, em.E), fullmant_np(2 + 37 * 120, 0, em.E)
+    for h in em.hubs:
+        h.load_state(w, v)
+    em.round(order=list(reversed(range(8))))
+    w, v, s = oracle.round_(sizes, em.host_grads(), w, v, 0.1, 0.9)
+    for r, h in enumerate(em.hubs):
+        assert em.capi.phub_sync_timeouts(h.ctx) == 0
+        gw, gv, gs = h.read_state()
+        assert_bits_equal(gw, w, f"rank {r} replica w'")
+        own = em.owned_mask(r)
+        assert_bits_equal(gv[own], v[own], f"rank {r} owned v'")
+        assert_bits_equal(gs[own], s[own], f"rank {r} owned s")
+    em.close()
