@@ -15,11 +15,16 @@ __attribute__((unused)) static const char* st(phub_status s) { return phub_statu
 int main(int argc, char** argv) {
     const int cache = argc > 1 ? atoi(argv[1]) : 2;
     const int data = argc > 2 ? atoi(argv[2]) : 0;   /* 0 zeros; 1 random grads; 2 + random w, v */
+    const int vgg = argc > 3 && atoi(argv[3]);       /* 1: the 38-key VGG-19 manifest */
+    static const uint64_t vgg19[38] = {
+        1728, 64, 36864, 64, 73728, 128, 147456, 128, 294912, 256, 589824, 256, 589824, 256,
+        589824, 256, 1179648, 512, 2359296, 512, 2359296, 512, 2359296, 512, 2359296, 512,
+        2359296, 512, 2359296, 512, 2359296, 512, 102760448, 4096, 16777216, 4096, 4096000, 1000};
     uint64_t keys[1] = {143667264ull};          /* one key = E_padded of VGG-19 */
     phub_config cfg;
     phub_config_default(&cfg);
-    cfg.key_num_elements = keys;
-    cfg.num_keys = 1;
+    cfg.key_num_elements = vgg ? vgg19 : keys;
+    cfg.num_keys = vgg ? 38 : 1;
     cfg.num_workers = 8;
     phub_ctx ctx = NULL;
     if (phub_init(&cfg, &ctx) != PHUB_OK) return 1;
@@ -36,6 +41,9 @@ int main(int argc, char** argv) {
         if (data) cudaMemcpy(g[w], h, keys[0] * 4, cudaMemcpyHostToDevice);
         else cudaMemset(g[w], 0, keys[0] * 4);
     }
+    uint64_t Ereal = 0, Epad = 0;
+    phub_layout(ctx, &Ereal, &Epad, NULL);
+    if (Epad != keys[0]) return 2;
     if (data == 2 && phub_load_state(ctx, h, h) != PHUB_OK) return 1;
     free(h);
     cudaEvent_t a, b;
@@ -51,7 +59,8 @@ int main(int argc, char** argv) {
     cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
-    printf("{\"harness\": \"C\", \"cache\": %d, \"data\": %d, \"ms\": %.4f}\n", cache, data, ms / 30);
+    printf("{\"harness\": \"C\", \"keys\": %d, \"cache\": %d, \"data\": %d, \"ms\": %.4f}\n",
+           cfg.num_keys, cache, data, ms / 30);
     phub_destroy(ctx);
     return 0;
 }
