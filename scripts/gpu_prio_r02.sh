@@ -1,6 +1,7 @@
 #!/bin/bash
 # kept-slice L2 priority (evict-last vs evict-normal) x size, bench-like setup,
 # one fresh process per setting.   usage: bash scripts/gpu_prio_r02.sh TAG
+# (the --resident-prio option was removed after this sweep: no gain, profiles/r02_prio/)
 OUT=gpurun_out/$1; mkdir -p $OUT
 B="python bench.py --steps 30 --warmup 10 --no-cpu --no-e2e"
 for rep in 1 2; do
