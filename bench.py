@@ -89,6 +89,8 @@ def parse():
     ap.add_argument("--sched-taper", type=int, default=-1,
                     help="sched mode: blocks at each part's ends cut 4x finer (-1: 0 at G = 2, "
                          "else 8)")
+    ap.add_argument("--sched-host-barrier", action="store_true",
+                    help="sched mode: NCCL start/end barriers instead of the in-kernel ones")
     ap.add_argument("--sched-consumers", type=int, default=0,
                     help="sched mode: CTAs serving the consumer lane (0 = auto)")
     ap.add_argument("--sched-weights", default="",
@@ -518,6 +520,7 @@ def bench_multi(args, mname, N, cb):
             sh = SchedShardedPHub(sizes, N, chunk_size_bytes=cb, device=local,
                                   block=args.sched_block, lag=args.sched_lag,
                                   consumer_ctas=args.sched_consumers, taper=args.sched_taper,
+                                  device_barrier=not args.sched_host_barrier,
                                   weights=fl(args.sched_weights), raw_frac=fl(args.sched_raw))
         elif chain:
             sh = ChainShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, pieces=args.pieces,
@@ -754,7 +757,9 @@ def bench_multi(args, mname, N, cb):
                                 f"the fewest bytes; owner shares {[round(x, 4) for x in sh.shares]}"
                                 f", RAW fractions {[round(x, 4) for x in sh.raw_frac]}, "
                                 f"{sh.block}-element blocks, lag {sh.lag}, taper {sh.taper}, "
-                                f"consumer-lane CTAs {args.sched_consumers or 'auto'}")
+                                f"consumer-lane CTAs {args.sched_consumers or 'auto'}, "
+                                f"{'NCCL' if args.sched_host_barrier else 'in-kernel'} round "
+                                f"barriers")
                                if sched else
                                (f"M3 (full exchange) chain: rank-ordered partial sums over "
                                 f"NVLink, last rank fused Nesterov + replica stores, " +

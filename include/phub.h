@@ -457,7 +457,8 @@ typedef struct {
  * stages and consumers by that many blocks of progress (pipeline fill).
  * Flag layout (identical on every rank, *num_flags entries, zero initially):
  * chain block c: [c] partial arrival, [C + c] final arrival; raw block j
- * (numbered owner-major): [2C + j*ranks + q] slices of rank q arrived.
+ * (numbered owner-major): [2C + j*ranks + q] slices of rank q arrived; the
+ * last 2 x ranks: the round barrier of phub_sched.device_barrier.
  * *count receives the item count (cap may be 0: count query; LENGTH_MISMATCH
  * if cap < count).  INVALID_ARGUMENT on bad geometry. */
 phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_rank,
@@ -497,6 +498,16 @@ typedef struct {
                                     share of the items' elements, clamped to [1/8, 1/2]).
                                     A program without CHAIN items runs as ONE lane in
                                     ticket order (the field is ignored). */
+    int32_t device_barrier;      /* nonzero: the launch brackets the round with in-kernel
+                                    barriers over the last 2 x ranks flags of the program
+                                    -- it tells every peer its replica is free when it
+                                    starts (so the caller orders its own replica reads
+                                    before the launch on `stream`), stores w' into a peer
+                                    replica only after that peer's launch has started,
+                                    and completes only once every peer has finished
+                                    storing into this rank's replica and reading its
+                                    inboxes -- replacing the caller's start and end
+                                    barriers (collectives).  0: the caller orders rounds. */
 } phub_sched;
 phub_status phub_sched_exchange(phub_ctx ctx, const phub_sched* s, void* stream);
 

@@ -66,7 +66,7 @@ class phub_sched_item(C.Structure):
 class phub_sched(C.Structure):
     _fields_ = [("inbox", C.POINTER(C.c_void_p)), ("raw_inbox", C.POINTER(C.c_void_p)),
                 ("flags", C.POINTER(C.c_void_p)), ("epoch", C.c_uint32),
-                ("consumer_ctas", C.c_int32)]
+                ("consumer_ctas", C.c_int32), ("device_barrier", C.c_int32)]
 
 
 class phub_config(C.Structure):
@@ -408,11 +408,12 @@ def phub_sched_load(ctx, ranks: int, rank: int, items, num_flags: int):
 
 
 def phub_sched_exchange(ctx, inbox, raw_inbox, flags, epoch: int, stream: int = 0,
-                        consumer_ctas: int = 0):
+                        consumer_ctas: int = 0, device_barrier: bool = False):
     """One scheduled round (phub.h phub_sched_exchange); pointer lists per rank."""
     R = len(inbox)
     arr = lambda xs: (C.c_void_p * R)(*[x or None for x in xs])  # noqa: E731
-    s = phub_sched(arr(inbox), arr(raw_inbox), arr(flags), int(epoch), int(consumer_ctas))
+    s = phub_sched(arr(inbox), arr(raw_inbox), arr(flags), int(epoch), int(consumer_ctas),
+                   int(bool(device_barrier)))
     _check(_lib.phub_sched_exchange(ctx, C.byref(s), stream), "phub_sched_exchange", ctx)
 
 

@@ -1300,7 +1300,10 @@ phub_status phub_sched_plan(int32_t ranks, int32_t rank, int32_t workers_per_ran
     for (int o = 0; o < G; ++o) cut(o, split[o], bounds[o + 1], chain);   // chain parts, owner-major
     for (int o = 0; o < G; ++o) cut(o, bounds[o], split[o], raw);         // raw parts, owner-major
     const uint64_t C = chain.size(), R = raw.size();
-    const uint64_t nflags = 2 * C + R * (uint64_t)G;
+    // + 2G round-barrier flags at the end (phub_sched.device_barrier):
+    //   [2C + RG + q]     rank q's replica is free for this epoch (its kernel started)
+    //   [2C + RG + G + q] rank q finished storing into this rank's replica
+    const uint64_t nflags = 2 * C + R * (uint64_t)G + 2 * (uint64_t)G;
     if (nflags >= 0xffffffffull) return PHUB_ERR_INVALID_ARGUMENT;
     // (progress key, stage, item): progress = fraction of the block's own part
     // done before it, plus stage * lag; the same doubles on every rank.  Every
@@ -1505,6 +1508,14 @@ phub_status phub_sched_exchange(phub_ctx c, const phub_sched* s, void* stream) {
     a.ticket = c->d_sync + 3;
     a.timeouts = c->d_sync + 1;
     a.err_host = c->d_err;
+    if (s->device_barrier) {
+        if (c->sched_flags < 2u * (uint32_t)R)
+            return c->fail(PHUB_ERR_INVALID_ARGUMENT, "device_barrier needs the program's 2 x ranks "
+                           "barrier flags (plans from phub_sched_plan carry them)");
+        a.bar = (int64_t)c->sched_flags - 2 * R;
+    } else {
+        a.bar = -1;
+    }
     DeviceGuard g(c->device);
     c->launches = 0;
     if (!c->sched_occ) c->sched_occ = phub::sched_blocks_per_sm(c->N);

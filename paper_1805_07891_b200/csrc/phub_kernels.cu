@@ -859,7 +859,17 @@ template <int NW>
 __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ SchedArgs a) {
     __shared__ uint64_t s_t;
     __shared__ int s_ok;
+    __shared__ int s_free;                             // every peer replica writable (barrier)
     const uint32_t* my_flags = a.flags[a.rank];
+    // In-kernel round barrier (a.bar >= 0), start half: this launch is stream-ordered
+    // after this rank's reads of its replica from the previous round, so it tells
+    // every peer "my replica is free for this epoch"; a CTA waits for every peer's
+    // such flag before its first replica store (below).
+    if (threadIdx.x == 0) s_free = a.bar < 0;
+    if (a.bar >= 0 && blockIdx.x == 0 && threadIdx.x == 0)
+        for (int q = 0; q < a.R; ++q)
+            if (q != a.rank) st_release_sys(a.flags[q] + a.bar + a.rank, a.epoch);
+    __syncthreads();
     // two lanes with their own tickets: producers (RAW_PUSH, CHAIN) never wait on
     // a consumer, so consumers blocked on late data cannot stall the chain
     const bool cons_lane = (int)blockIdx.x >= a.grid_prod;
@@ -885,6 +895,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ S
                     if (q != a.rank) good = sched_wait(a, my_flags + it.wait_flag + q, t0);
             } else if (it.wait_flag != kNoFlag) {
                 good = sched_wait(a, my_flags + it.wait_flag, t0);
+            }
+            // a Nesterov item stores w' into every peer replica: they must be free
+            if (good && !s_free && it.dst < 0) {
+                for (int q = 0; q < a.R && good; ++q)
+                    if (q != a.rank) good = sched_wait(a, my_flags + a.bar + q, t0);
+                s_free = good;
             }
             s_ok = good;
             if (a.trace) a.trace[4 * t + 1] = globaltimer_ns();
@@ -1000,6 +1016,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_sched(const __grid_constant__ S
     }
     if (a.nrep) __threadfence_system();
     if (threadIdx.x == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x - 1) {
+        if (a.bar >= 0) {
+            // end half: every CTA's replica stores are performed (each fenced before
+            // counting itself); tell every peer, then wait until every peer has done
+            // so -- the launch completes only once this rank's replica is complete
+            // and every peer has finished reading this round's inboxes.  A peer whose
+            // launch gave up never raises its flag, so this wait expires too.
+            __threadfence_system();
+            // a launch that skipped work (a wait given up) never reports done: its
+            // peers' end waits expire and fail loudly instead of trusting stale w'
+            const bool abandoned = *(volatile uint32_t*)(a.timeouts + 1) >= a.epoch;
+            for (int q = 0; q < a.R && !abandoned; ++q)
+                if (q != a.rank) st_release_sys(a.flags[q] + a.bar + a.R + a.rank, a.epoch);
+            const uint64_t t0 = globaltimer_ns();
+            for (int q = 0; q < a.R; ++q)
+                if (q != a.rank && !sched_wait(a, my_flags + a.bar + a.R + q, t0)) break;
+        }
         a.ticket[0] = 0;
         a.ticket[1] = 0;
         a.ticket[2] = 0;

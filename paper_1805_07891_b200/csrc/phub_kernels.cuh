@@ -100,6 +100,8 @@ struct SchedArgs {
     float* raw_inbox[kMaxRacks];      // rank q's raw inbox
     uint32_t* flags[kMaxRacks];       // rank q's flags
     uint32_t epoch;
+    int64_t bar;                      // >= 0: index of the 2R round-barrier flags (in-kernel
+                                      // start / end barriers instead of the caller's); -1: off
     uint32_t* ticket;                 // [0] next producer item, [1] CTAs done, [2] next consumer
     uint32_t* timeouts;               // [0] expired waits, [1] abandoned epoch
     volatile uint32_t* err_host;

@@ -962,7 +962,7 @@ class SchedShardedPHub(_DeviceWaitExchange):
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
                  device=None, group=None, block=0, lag=-1, weights=None, raw_frac=None,
-                 nslots=2, keep_aggregate=False, consumer_ctas=0, taper=-1):
+                 nslots=2, keep_aggregate=False, consumer_ctas=0, taper=-1, device_barrier=True):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -976,6 +976,9 @@ class SchedShardedPHub(_DeviceWaitExchange):
         self.block = int(block) if block else (16384 if world == 2 else 12288)
         self.lag = int(lag) if lag >= 0 else (0 if world == 2 else 64)
         self.consumer_ctas = int(consumer_ctas)        # 0: auto (phub_sched.consumer_ctas)
+        # round barriers inside the launch (phub_sched.device_barrier) instead of two
+        # NCCL all-reduces per round
+        self.device_barrier = bool(device_barrier)
         # blocks cut 4x finer at each part's ends: 8 at G >= 3 (profiles/r02_sched9/)
         self.taper = int(taper) if taper >= 0 else (0 if world == 2 else 8)
         if weights is None or raw_frac is None:
@@ -1068,15 +1071,21 @@ class SchedShardedPHub(_DeviceWaitExchange):
         context failed."""
         self._round(lambda: self._exchange(slot))
 
+    def _barriers_per_round(self):
+        return 0 if self.device_barrier else 2
+
     def _exchange(self, slot):
         Ep = self.hub.E_padded
-        self.barrier()                       # every replica and inbox free (previous round read)
+        if not self.device_barrier:
+            self.barrier()                   # every replica and inbox free (previous round read)
         for k in range(self.W):
             self.hub.push(k, self._own[(slot, k)], mode="borrow", n=Ep)
         self.epoch += 1
         capi.phub_sched_exchange(self.hub.ctx, self.inbox, self.raw_inbox, self.flags, self.epoch,
-                                 self.hub._stream(None), consumer_ctas=self.consumer_ctas)
-        self.barrier()                       # every rank's w' stores into this replica are done
+                                 self.hub._stream(None), consumer_ctas=self.consumer_ctas,
+                                 device_barrier=self.device_barrier)
+        if not self.device_barrier:
+            self.barrier()                   # every rank's w' stores into this replica are done
 
     def exchange_host(self, host_grads: dict, host_out: dict, slot: int = 0):
         g = self.gradients(slot)

@@ -362,17 +362,23 @@ class EmulatedSched:
     def owned_mask(self, r):
         return (self.pidx >= self.bounds[r]) & (self.pidx < self.bounds[r + 1])
 
-    def round(self, order=None):
+    def round(self, order=None, device_barrier=False):
+        """device_barrier=False: host synchronizes around the round (the caller's
+        barriers); True: no host synchronization at all -- the launches' in-kernel
+        round barriers alone must order consecutive rounds on the ranks' streams."""
         self.epoch += 1
-        torch.cuda.synchronize()                     # start barrier
+        if not device_barrier:
+            torch.cuda.synchronize()                 # start barrier
         ptr = lambda ts: [t.data_ptr() for t in ts]  # noqa: E731
         for r in (order or range(self.R)):
             h = self.hubs[r]
             for k in range(self.W):
                 h.push(k, self.grads[r][k])
             self.capi.phub_sched_exchange(h.ctx, ptr(self.inbox), ptr(self.raw), ptr(self.flags),
-                                          self.epoch, self.streams[r].cuda_stream)
-        torch.cuda.synchronize()                     # end barrier
+                                          self.epoch, self.streams[r].cuda_stream,
+                                          device_barrier=device_barrier)
+        if not device_barrier:
+            torch.cuda.synchronize()                 # end barrier
 
     def close(self):
         for h in self.hubs:
@@ -454,6 +460,39 @@ def test_sched_g8_bench_plan_full_vgg19_emulated():
         h.load_state(w, v)
     em.round(order=list(reversed(range(8))))
     w, v, s = oracle.round_(sizes, em.host_grads(), w, v, 0.1, 0.9)
+    for r, h in enumerate(em.hubs):
+        assert em.capi.phub_sync_timeouts(h.ctx) == 0
+        gw, gv, gs = h.read_state()
+        assert_bits_equal(gw, w, f"rank {r} replica w'")
+        own = em.owned_mask(r)
+        assert_bits_equal(gv[own], v[own], f"rank {r} owned v'")
+        assert_bits_equal(gs[own], s[own], f"rank {r} owned s")
+    em.close()
+
+
+@pytest.mark.parametrize("R,W,wts,rf,name,block,lag,taper", [
+    (2, 4, [0.0, 1.0], [0.0, 0.0], "resnet50", 16384, 0, 0),
+    (4, 2, [0.2982, 0.193, 0.193, 0.3158], [0.5294, 0.0, 0.0, 0.1667], "resnet50", 12288, 64, 8),
+    (8, 1, [0.125] * 8, [1.0] * 8, "small", 2048, 0, 0),
+])
+def test_sched_device_barrier_back_to_back_rounds(R, W, wts, rf, name, block, lag, taper):
+    """phub_sched.device_barrier: four rounds enqueued on the ranks' own streams
+    with NO host synchronization in between -- a rank may start round k+1 while
+    its peers still run round k; the in-kernel start flags keep its w' stores out
+    of replicas not yet released, the end flags keep inboxes from being
+    overwritten early.  Bit-exact vs four oracle rounds."""
+    sizes = SMALL if name == "small" else manifest(name)
+    em = EmulatedSched(sizes, R, W, wts, rf, block, lag, grid=max(2, 360 // R), seed=130 + R,
+                       taper=taper)
+    w, v = fullmant_np(1 + 37 * 130, 0, em.E), fullmant_np(2 + 37 * 130, 0, em.E)
+    for h in em.hubs:
+        h.load_state(w, v)
+    torch.cuda.synchronize()
+    flat = em.host_grads()
+    for i in range(4):
+        em.round(order=list(range(R)) if i % 2 else list(reversed(range(R))), device_barrier=True)
+        w, v, s = oracle.round_(sizes, flat, w, v, 0.1, 0.9)
+    torch.cuda.synchronize()
     for r, h in enumerate(em.hubs):
         assert em.capi.phub_sync_timeouts(h.ctx) == 0
         gw, gv, gs = h.read_state()
