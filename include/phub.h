@@ -376,6 +376,12 @@ typedef struct {
      * range into o's inbox (worker k at inbox + k*L + x, L = o's owned
      * length, so each slot holds N slices) and o sums them in worker order. */
     int32_t worker_order;
+    /* nonzero: in-kernel round barriers as phub_sched.device_barrier -- flags and
+     * peer_flags then hold 2 x num_racks more entries after the block flags, at
+     * [J*num_racks, J*num_racks + 2*num_racks), J = the block count of the
+     * LARGEST owner range (every rack's flag arrays sized alike).  0: the
+     * caller orders rounds. */
+    int32_t device_barrier;
 } phub_hier;
 phub_status phub_hier_exchange(phub_ctx ctx, const phub_hier* h, void* stream);
 

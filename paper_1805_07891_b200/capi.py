@@ -54,7 +54,8 @@ class phub_hier(C.Structure):
     _fields_ = [("num_racks", C.c_int32), ("block_elems", C.c_uint64),
                 ("inbox", C.POINTER(C.c_void_p)), ("peer_inbox", C.POINTER(C.c_void_p)),
                 ("flags", C.c_void_p), ("peer_flags", C.POINTER(C.c_void_p)),
-                ("epoch", C.c_uint32), ("worker_order", C.c_int32)]
+                ("epoch", C.c_uint32), ("worker_order", C.c_int32),
+                ("device_barrier", C.c_int32)]
 
 
 class phub_sched_item(C.Structure):
@@ -376,14 +377,16 @@ def phub_set_replicas(ctx, ptrs):
 
 
 def phub_hier_exchange(ctx, num_racks: int, block: int, inbox, peer_inbox, flags: int,
-                       peer_flags, epoch: int, stream: int = 0, worker_order: bool = False):
+                       peer_flags, epoch: int, stream: int = 0, worker_order: bool = False,
+                       device_barrier: bool = False):
     """Hierarchical reduction round (phub.h phub_hier_exchange); pointer lists
     have num_racks entries (this rack's entry ignored, may be 0)."""
     R = int(num_racks)
     def arr(xs):
         return (C.c_void_p * max(R, 1))(*[int(x or 0) for x in xs]) if xs else None
     ib, pib, pf = arr(inbox), arr(peer_inbox), arr(peer_flags)     # alive across the call
-    h = phub_hier(R, int(block), ib, pib, flags or None, pf, int(epoch), int(bool(worker_order)))
+    h = phub_hier(R, int(block), ib, pib, flags or None, pf, int(epoch), int(bool(worker_order)),
+                  int(bool(device_barrier)))
     _check(_lib.phub_hier_exchange(ctx, C.byref(h), stream), "phub_hier_exchange", ctx)
 
 

@@ -1246,6 +1246,8 @@ phub_status phub_hier_exchange(phub_ctx c, const phub_hier* h, void* stream) {
     a.flags = R > 1 ? h->flags : nullptr;
     a.epoch = h->epoch;
     a.worker_order = h->worker_order ? 1 : 0;
+    a.device_barrier = h->device_barrier ? 1 : 0;
+    if (a.device_barrier && R < 2) a.device_barrier = 0;   // one rack: nothing to order
     a.ticket = c->d_sync + 3;
     a.timeouts = c->d_sync + 1;
     a.err_host = c->d_err;

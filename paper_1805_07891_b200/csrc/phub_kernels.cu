@@ -641,6 +641,20 @@ __device__ __forceinline__ void local_sum(const HierArgs& a, uint64_t i, float a
     }
 }
 
+// Thread 0: bounded wait for *f >= epoch (0 = gave up or abandoned), as sched_wait.
+__device__ __forceinline__ int hier_wait(const HierArgs& a, const uint32_t* f, const uint64_t t0) {
+    volatile uint32_t* abandoned = a.timeouts + 1;
+    while (ld_acquire_sys(f) < a.epoch) {
+        if (*abandoned >= a.epoch) return 0;
+        if (globaltimer_ns() - t0 > 2000000000ull) {
+            record_timeout(a.timeouts, a.err_host, a.epoch);
+            return 0;
+        }
+        __nanosleep(100);
+    }
+    return 1;
+}
+
 template <int NW, bool WO>
 __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ HierArgs a) {
     const uint64_t B = a.block;
@@ -651,8 +665,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ Hi
         J = n > J ? n : J;
     }
     const uint64_t items = J * (uint64_t)R;
+    // in-kernel round barrier (a.device_barrier; the k_sched scheme): flags
+    // [J*R + q] "rank q's replica is free", [J*R + R + q] "rank q is done
+    // storing into this rank's replica"
+    const uint64_t bar = J * (uint64_t)R;
     __shared__ uint64_t s_item;
     __shared__ int ok;
+    __shared__ int s_free;
+    if (threadIdx.x == 0) s_free = !a.device_barrier;
+    if (a.device_barrier && blockIdx.x == 0 && threadIdx.x == 0)
+        for (int q = 0; q < R; ++q)
+            if (q != a.rack) st_release_sys(a.peer_flags[q] + bar + a.rack, a.epoch);
+    __syncthreads();
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(a.ticket, 1u);
         __syncthreads();
@@ -705,20 +729,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ Hi
             if (lo < hi) {
                 if (threadIdx.x == 0) {
                     int good = 1;
-                    volatile uint32_t* abandoned = a.timeouts + 1;
                     const uint64_t t0 = globaltimer_ns();
-                    for (int q = 0; q < R && good; ++q) {
-                        if (q == a.rack) continue;
-                        const uint32_t* f = a.flags + j * R + q;
-                        while (ld_acquire_sys(f) < a.epoch) {
-                            if (*abandoned >= a.epoch) { good = 0; break; }
-                            if (globaltimer_ns() - t0 > 2000000000ull) {
-                                record_timeout(a.timeouts, a.err_host, a.epoch);
-                                good = 0;
-                                break;
-                            }
-                            __nanosleep(100);
-                        }
+                    for (int q = 0; q < R && good; ++q)
+                        if (q != a.rack) good = hier_wait(a, a.flags + j * R + q, t0);
+                    // w' goes into every peer replica: each must be free (barrier)
+                    if (good && !s_free) {
+                        for (int q = 0; q < R && good; ++q)
+                            if (q != a.rack) good = hier_wait(a, a.flags + bar + q, t0);
+                        s_free = good;
                     }
                     ok = good;
                 }
@@ -775,6 +793,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_hier(const __grid_constant__ Hi
     }
     if (a.nrep) __threadfence_system();
     if (threadIdx.x == 0 && atomicAdd(a.ticket + 1, 1u) == gridDim.x - 1) {
+        if (a.device_barrier) {                        // end half (see k_sched)
+            __threadfence_system();
+            const bool abandoned = *(volatile uint32_t*)(a.timeouts + 1) >= a.epoch;
+            for (int q = 0; q < R && !abandoned; ++q)
+                if (q != a.rack) st_release_sys(a.peer_flags[q] + bar + R + a.rack, a.epoch);
+            const uint64_t t0 = globaltimer_ns();
+            for (int q = 0; q < R; ++q)
+                if (q != a.rack && !hier_wait(a, a.flags + bar + R + q, t0)) break;
+        }
         a.ticket[0] = 0;
         a.ticket[1] = 0;
     }

@@ -67,6 +67,7 @@ struct HierArgs {
     uint32_t* timeouts;               // [0] expired waits, [1] abandoned epoch
     volatile uint32_t* err_host;      // host-mapped sticky-error word (see FlatArgs)
     int worker_order;                 // 1: flat worker-order sum of raw slices (M3 exchange)
+    int device_barrier;               // 1: in-kernel round barrier over flags [J*R, J*R + 2R)
 };
 cudaError_t launch_hier(const HierArgs& a, int grid, cudaStream_t s, int* launches);
 int hier_blocks_per_sm(int nw, bool worker_order);

@@ -678,7 +678,7 @@ class HierPHub(_DeviceWaitExchange):
 
     def __init__(self, key_sizes, workers_per_rack=8, chunk_size_bytes=32768, lr=0.1,
                  momentum=0.9, device=None, group=None, block=32768, nslots=2,
-                 worker_order=False):
+                 worker_order=False, device_barrier=True):
         import torch
         import torch.distributed as dist
         from .phub import PHub, _CudaArray
@@ -690,6 +690,9 @@ class HierPHub(_DeviceWaitExchange):
         # worker_order: the flat worker-order sum of one job's R x P workers (raw
         # slices pushed to the owners) instead of the rack-grouped sum
         self.worker_order = bool(worker_order)
+        # round barriers inside the launch (phub_hier.device_barrier) instead of two
+        # NCCL all-reduces per round
+        self.device_barrier = bool(device_barrier) and world > 1
         S = self.P if self.worker_order else 1          # slices per (slot, source rack)
         self.device = torch.cuda.current_device() if device is None else int(device)
         dev = self.device
@@ -708,9 +711,13 @@ class HierPHub(_DeviceWaitExchange):
             t.zero_()
         # inbox: 2 epoch-parity slots x R source racks x S slices x L owned elements
         self._inbox = capi.phub_alloc_shared(dev, 4 * 2 * world * S * max(L, 1))
-        nblk = max(1, -(-L // self.block))
-        self._flags = capi.phub_alloc_shared(dev, 4 * nblk * world)
-        torch.as_tensor(_CudaArray(self._flags, nblk * world, self), device=f"cuda:{dev}").zero_()
+        # block flags sized by the LARGEST owner range (J blocks) on every rack, then
+        # the 2 x world round-barrier flags (phub_hier.device_barrier)
+        J = max(max(1, -(-(oe - ob) // self.block)) for ob, oe in
+                (self.hub.owner_range(o) for o in range(world)))
+        nfl = J * world + 2 * world
+        self._flags = capi.phub_alloc_shared(dev, 4 * nfl)
+        torch.as_tensor(_CudaArray(self._flags, nfl, self), device=f"cuda:{dev}").zero_()
         h = capi.phub_ipc_get_handle
         mine = (rank, b, e, h(dev, self._inbox), h(dev, self._flags),
                 h(dev, self.hub.weights_ptr()))
@@ -786,20 +793,27 @@ class HierPHub(_DeviceWaitExchange):
         context failed."""
         self._round(lambda: self._exchange(slot))
 
+    def _barriers_per_round(self):
+        return 0 if self.device_barrier else 2
+
     def _exchange(self, slot):
         Ep = self.hub.E_padded
         # start barrier: this round's kernels store w' into every rank's replica,
         # so every rank must be done reading its replica from the previous round
-        # (e.g. a pull enqueued after that round's end barrier)
-        self.barrier()
+        # (e.g. a pull enqueued after that round's end barrier) -- in-kernel flags
+        # with device_barrier (the launch is stream-ordered after those reads)
+        if not self.device_barrier:
+            self.barrier()
         for k in range(self.P):
             self.hub.push(k, self._own[(slot, k)], mode="borrow", n=Ep)
         self.epoch += 1
         par = self.epoch % 2
         capi.phub_hier_exchange(self.hub.ctx, self.R, self.block, self.inbox[par],
                                 self.peer_inbox[par], self._flags, self.peer_flags, self.epoch,
-                                self.hub._stream(None), worker_order=self.worker_order)
-        self.barrier()                       # every rack's w' stores into this replica are done
+                                self.hub._stream(None), worker_order=self.worker_order,
+                                device_barrier=self.device_barrier)
+        if not self.device_barrier:
+            self.barrier()                   # every rack's w' stores into this replica are done
 
     def weights(self):
         return self.replica
@@ -834,7 +848,7 @@ class PushShardedPHub(HierPHub):
     P2PShardedPHub (gradients() keyed by global worker id)."""
 
     def __init__(self, key_sizes, num_workers, chunk_size_bytes=32768, lr=0.1, momentum=0.9,
-                 device=None, group=None, block=12288, nslots=2):
+                 device=None, group=None, block=12288, nslots=2, device_barrier=True):
         import torch.distributed as dist
         world = dist.get_world_size(group)
         if num_workers % world:
@@ -842,7 +856,7 @@ class PushShardedPHub(HierPHub):
         super().__init__(key_sizes, workers_per_rack=num_workers // world,
                          chunk_size_bytes=chunk_size_bytes, lr=lr, momentum=momentum,
                          device=device, group=group, block=block, nslots=nslots,
-                         worker_order=True)
+                         worker_order=True, device_barrier=device_barrier)
         self.plan = ExchangePlan.build(key_sizes, num_workers, chunk_size_bytes, self.rack, world)
 
     @property

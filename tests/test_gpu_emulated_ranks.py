@@ -70,8 +70,10 @@ class EmulatedRacks:
         S = P if worker_order else 1
         self.S = S
         self.inbox = [torch.zeros(2 * R * S * max(e - b, 1), device=DEV) for b, e in self.ranges]
-        nblk = [max(1, -(-(e - b) // block)) for b, e in self.ranges]
-        self.flags = [torch.zeros(n * R, dtype=torch.int32, device=DEV) for n in nblk]
+        # block flags sized by the largest owner range on every rank, + the 2R
+        # round-barrier flags (phub_hier.device_barrier)
+        J = max(max(1, -(-(e - b) // block)) for b, e in self.ranges)
+        self.flags = [torch.zeros(J * R + 2 * R, dtype=torch.int32, device=DEV) for _ in range(R)]
         self.streams = [torch.cuda.Stream() for _ in range(R)]
         for r, h in enumerate(self.hubs):
             h.set_option(capi.PHUB_OPT_GRID, grid)
@@ -112,10 +114,11 @@ class EmulatedRacks:
             peer_flags[o] = self.flags[o].data_ptr()
         return inbox, peer_inbox, peer_flags
 
-    def round(self, ranks=None, order=None):
+    def round(self, ranks=None, order=None, device_barrier=False):
         self.epoch += 1
         par = self.epoch % 2
-        torch.cuda.synchronize()                     # start barrier (replicas free)
+        if not device_barrier:
+            torch.cuda.synchronize()                 # start barrier (replicas free)
         for r in (order or range(self.R)):
             if ranks is not None and r not in ranks:
                 continue
@@ -125,8 +128,10 @@ class EmulatedRacks:
             inbox, peer_inbox, peer_flags = self.pointers(r, par)
             self.capi.phub_hier_exchange(h.ctx, self.R, self.block, inbox, peer_inbox,
                                          self.flags[r].data_ptr(), peer_flags, self.epoch,
-                                         self.streams[r].cuda_stream, worker_order=self.wo)
-        torch.cuda.synchronize()                     # end barrier (replicas complete)
+                                         self.streams[r].cuda_stream, worker_order=self.wo,
+                                         device_barrier=device_barrier)
+        if not device_barrier:
+            torch.cuda.synchronize()                 # end barrier (replicas complete)
 
     def close(self):
         for h in self.hubs:
@@ -498,6 +503,37 @@ def test_sched_device_barrier_back_to_back_rounds(R, W, wts, rf, name, block, la
         gw, gv, gs = h.read_state()
         assert_bits_equal(gw, w, f"rank {r} replica w'")
         own = em.owned_mask(r)
+        assert_bits_equal(gv[own], v[own], f"rank {r} owned v'")
+        assert_bits_equal(gs[own], s[own], f"rank {r} owned s")
+    em.close()
+
+
+@pytest.mark.parametrize("R,P,wo,name,block", [
+    (2, 4, True, "resnet50", 12288), (4, 2, True, "small", 2048),
+    (2, 8, False, "resnet50", 32768), (4, 3, False, "small", 2048)])
+def test_hier_device_barrier_back_to_back_rounds(R, P, wo, name, block):
+    """phub_hier.device_barrier (push exchange wo = 1, hierarchical wo = 0):
+    three rounds on the ranks' own streams with NO host synchronization in
+    between, ordered only by the in-kernel start / done flags.  Bit-exact vs
+    the oracle (flat worker order, or rack order)."""
+    sizes = SMALL if name == "small" else manifest(name)
+    em = EmulatedRacks(sizes, R, P, wo, block, grid=max(2, 360 // R), seed=140 + R)
+    w, v = fullmant_np(1 + 37 * 140, 0, em.E), fullmant_np(2 + 37 * 140, 0, em.E)
+    em.load_state(w, v)
+    torch.cuda.synchronize()
+    rg = em.host_grads()
+    for i in range(3):
+        em.round(order=list(range(R)) if i % 2 else list(reversed(range(R))), device_barrier=True)
+        if wo:
+            w, v, s = oracle.round_(sizes, [g for rack in rg for g in rack], w, v, 0.1, 0.9)
+        else:
+            w, v, s = oracle.hier_round(sizes, rg, w, v, 0.1, 0.9)
+    torch.cuda.synchronize()
+    for r, h in enumerate(em.hubs):
+        assert em.capi.phub_sync_timeouts(h.ctx) == 0
+        gw, gv, gs = h.read_state()
+        assert_bits_equal(gw, w, f"rank {r} replica w'")
+        own = _owned_mask(h, sizes)
         assert_bits_equal(gv[own], v[own], f"rank {r} owned v'")
         assert_bits_equal(gs[own], s[own], f"rank {r} owned s")
     em.close()
