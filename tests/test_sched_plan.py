@@ -249,3 +249,38 @@ def test_geometry_snaps_to_chunk_starts(name, G):
         for o in range(G):
             target = Ep * sum(wts[:o + 1]) / sum(wts)
             assert abs(bounds[o + 1] - target) <= 8192 + 32      # one 32 KB chunk + padding
+
+
+def test_random_geometries_property():
+    """Property check over random plans (hypothesis, bounded): any G in 1..8,
+    W in 1..4, owner shares, RAW fractions, block size, lag and taper give
+    programs whose symbolic execution sums every element in worker order
+    exactly once at its owner, raises every flag once and never stalls --
+    with one worker per rank and with the two ticket lanes."""
+    hyp = pytest.importorskip("hypothesis")
+    st = hyp.strategies
+
+    @hyp.settings(max_examples=60, deadline=None, derandomize=True)
+    @hyp.given(G=st.integers(1, 8), W=st.integers(1, 4), data=st.data())
+    def check(G, W, data):
+        Ep = data.draw(st.integers(1, 24)) * 2048 + data.draw(st.integers(0, 255)) * 8
+        wts = [data.draw(st.floats(0.0, 1.0)) + 1e-3 for _ in range(G)]
+        rf = [data.draw(st.sampled_from([0.0, 0.25, 0.5, 1.0, data.draw(st.floats(0, 1))]))
+              for _ in range(G)]
+        block = data.draw(st.sampled_from([2048, 4096, 8192]))
+        lag = data.draw(st.integers(0, 8))
+        taper = data.draw(st.integers(0, 3))
+        lanes = data.draw(st.booleans())
+        bounds, split = geometry(Ep, G, rf, wts)
+        nag, _ = simulate(G, W, bounds, split, block, lag, lanes, taper)
+        order = tuple(range(G * W))
+        covered = sorted((lo, hi) for r in range(G) for lo, hi, acc in nag[r]
+                         if acc == order and bounds[r] <= lo < hi <= bounds[r + 1])
+        assert sum(len(nag[r]) for r in range(G)) == len(covered)
+        pos = 0
+        for lo, hi in covered:
+            assert lo == pos
+            pos = hi
+        assert pos == Ep
+
+    check()
