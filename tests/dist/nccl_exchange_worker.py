@@ -46,12 +46,15 @@ def main():
         sh = PushShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048)
     elif mode == "sched":
         sh = SchedShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048, lag=1)
+    elif mode == "sched_raw":        # the G = 8 plan (all RAW, one lane) at any G
+        sh = SchedShardedPHub(sizes, N, chunk_size_bytes=cb, device=local, block=2048,
+                              weights=[1.0 / G] * G, raw_frac=[1.0] * G)
     elif mode == "allreduce":
         sh = AllReduceBaseline(sizes, N, chunk_size_bytes=cb, device=local)
     else:
         cls = P2PShardedPHub if mode == "p2p" else ShardedPHub
         sh = cls(sizes, N, chunk_size_bytes=cb, device=local)
-    fused = mode in ("p2p", "push", "sched") or mode.startswith("chain")
+    fused = mode in ("p2p", "push", "sched", "sched_raw") or mode.startswith("chain")
     w_ref, v_ref = fullmant_np(1, 0, E), fullmant_np(2, 0, E)
     sh.hub.load_state(w_ref, v_ref)
     idx = torch.as_tensor(sh.hub.padded_index(), device=dev)
@@ -69,7 +72,7 @@ def main():
         hg = [fullmant_np(grad_stream(w) + 37 * r, 0, E) for w in range(N)]
         w_ref, v_ref, _ = oracle.round_(sizes, hg, w_ref, v_ref, 0.1, 0.9, chunk_bytes=cb)
     torch.cuda.synchronize()
-    if mode.startswith("chain") or mode in ("push", "sched"):
+    if mode.startswith("chain") or mode in ("push", "sched", "sched_raw"):
         sh.check()                   # collective: raises on every rank if a device wait expired
     got = sh.weights()[idx].cpu().numpy()
     bad = int(np.sum(got.view(np.uint32) != w_ref.view(np.uint32)))

@@ -27,8 +27,8 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("mode", ["nccl", "p2p", "push", "sched", "chain", "chain_flags",
-                                  "chain_barrier", "allreduce"])
+@pytest.mark.parametrize("mode", ["nccl", "p2p", "push", "sched", "sched_raw", "chain",
+                                  "chain_flags", "chain_barrier", "allreduce"])
 @pytest.mark.parametrize("G,name,N,cb,rounds", [
     (2, "small", 8, 32768, 2), (2, "tiny", 4, 4096, 1), (4, "resnet50", 8, 32768, 2),
     (8, "resnet50", 8, 32768, 2), (8, "small", 8, 64, 1), (2, "one", 2, 32768, 2),
